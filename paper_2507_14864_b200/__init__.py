@@ -1,0 +1,226 @@
+"""Python binding of libfj (include/fj.h) — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``csrc/``; this module
+converts arrays to pointers and C structs to Python values.  It never computes
+on the host and has no fallback: if ``libfj.so`` is missing or fails to load,
+every entry point raises.
+
+Arrays may be numpy arrays (host memory) or torch tensors (host or CUDA); the
+library detects the memory space of each pointer (fj.h "Memory").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfj.so")
+_LIB = None
+
+FJ_OK, FJ_ERR_INVALID, FJ_ERR_NUMERIC, FJ_ERR_CUDA = 0, 2, 3, 4
+METHODS = {"auto": 0, "async": 1, "colored": 2, "push": 3}
+
+#: every symbol include/fj.h declares
+EXPORTS = ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve", "fj_solve_ex",
+           "fj_measures", "fj_measures_ex", "fj_opts_default", "fj_last_error",
+           "fj_abi_version")
+
+
+class FJError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[fj status {status}] {msg}")
+        self.status = status
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("sigma", ctypes.c_double), ("c", ctypes.c_double), ("method", ctypes.c_int),
+                ("max_sweeps", ctypes.c_int), ("cert_rounds", ctypes.c_int),
+                ("certify", ctypes.c_int), ("zprime_out", ctypes.c_void_p)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("sweeps", ctypes.c_int64), ("phases", ctypes.c_int64),
+                ("relaxations", ctypes.c_int64), ("edge_updates", ctypes.c_int64),
+                ("rows_read", ctypes.c_int64), ("arcs_read", ctypes.c_int64),
+                ("cert_rounds", ctypes.c_int64), ("cert_ratio", ctypes.c_double),
+                ("c", ctypes.c_double), ("eps_prime", ctypes.c_double),
+                ("colors", ctypes.c_int), ("status", ctypes.c_int), ("reason", ctypes.c_int),
+                ("solve_ms", ctypes.c_double), ("sweep_ms", ctypes.c_double),
+                ("cert_ms", ctypes.c_double)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("m", ctypes.c_int64), ("directed", ctypes.c_int),
+                ("weighted", ctypes.c_int), ("max_out_degree", ctypes.c_int64),
+                ("empty_rows", ctypes.c_int64), ("tasks", ctypes.c_int64),
+                ("colors", ctypes.c_int), ("num_sms", ctypes.c_int)]
+
+
+class _Measures(ctypes.Structure):
+    _fields_ = [("polarization", ctypes.c_double), ("disagreement", ctypes.c_double),
+                ("internal_conflict", ctypes.c_double), ("controversy", ctypes.c_double)]
+
+
+def lib():
+    """Load libfj.so (built by ``__graft_entry__.build()``); raise if absent."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i64, d, i = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+        L.fj_graph_create.argtypes = [i64, i64, P, P, P, i, P, ctypes.POINTER(P)]
+        L.fj_graph_destroy.argtypes = [P]
+        L.fj_graph_get_info.argtypes = [P, ctypes.POINTER(_Info)]
+        L.fj_solve.argtypes = [P, P, d, d, P]
+        L.fj_solve_ex.argtypes = [P, P, d, d, ctypes.POINTER(_Opts), P, ctypes.POINTER(_Stats)]
+        L.fj_measures.argtypes = [P, P, ctypes.POINTER(d), ctypes.POINTER(d)]
+        L.fj_measures_ex.argtypes = [P, P, P, ctypes.POINTER(_Measures)]
+        L.fj_opts_default.argtypes = [ctypes.POINTER(_Opts)]
+        L.fj_opts_default.restype = None
+        L.fj_last_error.restype = ctypes.c_char_p
+        for f in ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve",
+                  "fj_solve_ex", "fj_measures", "fj_measures_ex"):
+            getattr(L, f).restype = i
+        _LIB = L
+    return _LIB
+
+
+def _check(st: int):
+    if st != FJ_OK:
+        raise FJError(st, lib().fj_last_error().decode(errors="replace"))
+
+
+def _ptr(a):
+    """Pointer of a numpy array or torch tensor (None → NULL)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(a.data_ptr())
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("array must be C-contiguous")
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _dtype_ok(a, name: str, kind: str):
+    if a is None:
+        return
+    dt = str(a.dtype)
+    if kind not in dt:
+        raise TypeError(f"{name} must be {kind}, got {dt}")
+
+
+def _stream_of(*arrays):
+    for a in arrays:
+        if a is not None and getattr(a, "is_cuda", False):
+            import torch
+            return ctypes.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)
+    return None
+
+
+@dataclass
+class SolveStats:
+    sweeps: int
+    phases: int
+    relaxations: int
+    edge_updates: int
+    rows_read: int
+    arcs_read: int
+    cert_rounds: int
+    cert_ratio: float
+    c: float
+    eps_prime: float
+    colors: int
+    status: int
+    reason: int
+    solve_ms: float
+    sweep_ms: float
+    cert_ms: float
+
+
+class Graph:
+    """Owning handle of an ``fj_graph_t`` (§8 row a1).
+
+    ``row_ptr`` int64[n+1], ``col`` int32[m], ``w`` float32[m] or None: the
+    in-CSR (row v lists the u with an arc u→v, u listens to v)."""
+
+    def __init__(self, n, row_ptr, col, w=None, directed=True, stream=None):
+        _dtype_ok(row_ptr, "row_ptr", "int64")
+        _dtype_ok(col, "col", "int32")
+        _dtype_ok(w, "w", "float32")
+        self._h = ctypes.c_void_p()
+        nnz = int(row_ptr[-1])
+        st = stream if stream is not None else _stream_of(row_ptr, col, w)
+        _check(lib().fj_graph_create(int(n), nnz, _ptr(row_ptr), _ptr(col), _ptr(w),
+                                     1 if directed else 0, st, ctypes.byref(self._h)))
+        self.n = int(n)
+        self.directed = bool(directed)
+
+    def info(self) -> dict:
+        i = _Info()
+        _check(lib().fj_graph_get_info(self._h, ctypes.byref(i)))
+        return {k: getattr(i, k) for k, _ in _Info._fields_}
+
+    def close(self):
+        if self._h:
+            lib().fj_graph_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "auto",
+          sigma: float = 1e-5, c: float = 0.0, max_sweeps: int = 0, cert_rounds: int = -1,
+          certify: bool = True, zprime_out=None, raise_on_numeric: bool = True) -> SolveStats:
+    """fj_solve_ex: writes z into ``z_out`` (float32[n]); returns the stats."""
+    _dtype_ok(s, "s", "float32")
+    _dtype_ok(z_out, "z_out", "float32")
+    _dtype_ok(zprime_out, "zprime_out", "float64")
+    o = _Opts()
+    lib().fj_opts_default(ctypes.byref(o))
+    o.sigma, o.c, o.method = sigma, c, METHODS[method]
+    o.max_sweeps, o.cert_rounds, o.certify = max_sweeps, cert_rounds, int(certify)
+    zp = _ptr(zprime_out)
+    o.zprime_out = zp.value if zp is not None else None
+    st = _Stats()
+    rc = lib().fj_solve_ex(g._h, _ptr(s), float(eps), float(omega), ctypes.byref(o),
+                           _ptr(z_out), ctypes.byref(st))
+    stats = SolveStats(**{k: getattr(st, k) for k, _ in _Stats._fields_})
+    if rc == FJ_ERR_NUMERIC and not raise_on_numeric:
+        return stats
+    _check(rc)
+    return stats
+
+
+def solve_simple(g: Graph, s, z_out, eps: float, omega: float = 1.0):
+    """The plain ABI call fj_solve(graph, s, eps, omega, z_out)."""
+    _check(lib().fj_solve(g._h, _ptr(s), float(eps), float(omega), _ptr(z_out)))
+
+
+def measures(g: Graph, z, s=None) -> dict:
+    """fj_measures_ex: P, D (and I, C) of Table tab:measures."""
+    _dtype_ok(z, "z", "float32")
+    _dtype_ok(s, "s", "float32")
+    m = _Measures()
+    _check(lib().fj_measures_ex(g._h, _ptr(z), _ptr(s), ctypes.byref(m)))
+    return dict(P=m.polarization, D=m.disagreement, I=m.internal_conflict, C=m.controversy)
+
+
+def measures_pd(g: Graph, z):
+    """The plain ABI call fj_measures(graph, z, &P, &D)."""
+    P, D = ctypes.c_double(), ctypes.c_double()
+    _check(lib().fj_measures(g._h, _ptr(z), ctypes.byref(P), ctypes.byref(D)))
+    return P.value, D.value

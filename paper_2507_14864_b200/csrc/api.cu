@@ -1,0 +1,85 @@
+// api.cu — error state, pointer classification, small C-ABI entry points.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "fj_internal.cuh"
+
+namespace fj {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // clear: unregistered host memory on old runtimes
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void Layout::release() {
+  cudaFree(perm);
+  cudaFree(iperm);
+  cudaFree(rp);
+  cudaFree(col);
+  cudaFree(w);
+  cudaFree(d1);
+  cudaFree(tasks);
+  cudaFree(d_phase_begin);
+  perm = iperm = nullptr;
+  rp = nullptr;
+  col = nullptr;
+  w = nullptr;
+  d1 = nullptr;
+  tasks = nullptr;
+  d_phase_begin = nullptr;
+  ntasks = 0;
+  ncolors = 0;
+  phase_begin.clear();
+}
+
+}  // namespace fj
+
+extern "C" {
+
+const char *fj_last_error(void) { return fj::g_err; }
+
+int fj_abi_version(void) { return FJ_ABI_VERSION; }
+
+void fj_opts_default(fj_opts *o) {
+  if (!o) return;
+  o->sigma = 1e-5;
+  o->c = 0.0;
+  o->method = FJ_METHOD_AUTO;
+  o->max_sweeps = 1000000;
+  o->cert_rounds = 3;
+  o->certify = 1;
+  o->zprime_out = nullptr;
+}
+
+fj_status fj_graph_get_info(fj_graph_t g, fj_graph_info *info) {
+  if (!g || !info) {
+    fj::set_error("fj_graph_get_info: null argument");
+    return FJ_ERR_INVALID;
+  }
+  info->n = g->n;
+  info->m = g->m;
+  info->directed = g->directed;
+  info->weighted = g->weighted;
+  info->max_out_degree = g->async_layout.max_len;
+  info->empty_rows = g->async_layout.empty_rows;
+  info->tasks = g->async_layout.ntasks;
+  info->colors = g->ncolors;
+  info->num_sms = g->num_sms;
+  return FJ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,342 @@
+// graph.cu — fj_graph_create / fj_graph_destroy (§8 row a1).
+//
+// Steps (all on the graph's stream):
+//   1. stage the caller's in-CSR into library-owned device memory;
+//   2. validate row_ptr, columns, weights (FJ_ERR_INVALID on failure);
+//   3. canonicalise the in-CSR (rows sorted by column) with one radix sort of
+//      (v, u) keys; adjacent equal keys are duplicate arcs, u == v self-loops;
+//   4. transpose to the pull (out-) CSR with a second sort of (u, v) keys and
+//      reduce its rows to d_u = Σ_v a_uv in fp64 (reading R3);
+//   5. undirected input: check the arc set is symmetric with equal weights;
+//   6. build the sweep layout (layout.cu).
+// Sorting and scans use CUB (toolkit library primitives); every kernel here
+// is a one-pass O(m) integer/fp64 kernel.
+#include <cub/cub.cuh>
+
+#include "fj_internal.cuh"
+
+namespace fj {
+
+static int bits_for(int64_t n) {
+  int b = 1;
+  while ((int64_t(1) << b) < n) b++;
+  return b;
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void k_validate_rowptr(int64_t n, int64_t m, const int64_t *__restrict__ rp,
+                                  int *__restrict__ err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  int64_t x = rp[i];
+  if (i == 0 && x != 0) atomicOr(err, 1);
+  if (i == n && x != m) atomicOr(err, 1);
+  if (i < n && rp[i + 1] < x) atomicOr(err, 1);
+  if (x < 0 || x > m) atomicOr(err, 1);
+}
+
+// one warp per row: keys[(v,u)] for the in-CSR arcs of row v, with column and
+// weight checks
+__global__ void k_in_keys(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                          const float *__restrict__ w, int nb, uint64_t *__restrict__ keys,
+                          int *__restrict__ err) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) {
+      int32_t u = col[e];
+      if (u < 0 || u >= n) { atomicOr(err, 2); u = 0; }
+      if (u == v) atomicOr(err, 4);
+      if (w) {
+        float x = w[e];
+        if (!(x > 0.0f) || !isfinite(x)) atomicOr(err, 8);
+      }
+      keys[e] = ((uint64_t)v << nb) | (uint64_t)u;
+    }
+  }
+}
+
+__global__ void k_iota_u32(int64_t m, uint32_t *__restrict__ x) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) x[i] = (uint32_t)i;
+}
+
+// after sorting: duplicates; split keys into (row, col); permute weights
+__global__ void k_unpack_sorted(int64_t m, int nb, const uint64_t *__restrict__ keys,
+                                const uint32_t *__restrict__ idx, const float *__restrict__ w_src,
+                                int32_t *__restrict__ col, float *__restrict__ w_dst,
+                                int *__restrict__ err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  uint64_t k = keys[i];
+  if (i > 0 && keys[i - 1] == k) atomicOr(err, 16);
+  col[i] = (int32_t)(k & ((uint64_t(1) << nb) - 1));
+  if (w_dst) w_dst[i] = w_src[idx[i]];
+}
+
+// out-CSR keys (u, v) from the canonical in-CSR: arc u→v sits in row v, col u
+__global__ void k_out_keys(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                           int nb, uint64_t *__restrict__ keys, int64_t *__restrict__ cnt) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps)
+    for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) {
+      uint64_t u = (uint64_t)col[e];
+      keys[e] = (u << nb) | (uint64_t)v;
+      atomicAdd((unsigned long long *)&cnt[u], 1ull);
+    }
+}
+
+// d_u = Σ_v a_uv over the out-row u (warp per row, fixed lane order + fixed
+// shuffle tree ⇒ deterministic fp64 sums)
+__global__ void k_row_sums(int64_t n, const int64_t *__restrict__ rp, const float *__restrict__ w,
+                           double *__restrict__ d) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t u = warp; u < n; u += nwarps) {
+    int64_t b = rp[u], e = rp[u + 1];
+    double s = 0.0;
+    if (w) {
+      for (int64_t k = b + lane; k < e; k += 32) s += (double)w[k];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    } else {
+      s = (double)(e - b);
+    }
+    if (lane == 0) d[u] = s;
+  }
+}
+
+template <class T>
+__global__ void k_neq(int64_t m, const T *__restrict__ a, const T *__restrict__ b,
+                      int *__restrict__ err, int bit) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m && a[i] != b[i]) atomicOr(err, bit);
+}
+
+static unsigned grid_for(int64_t work, int per_block = kBlock) {
+  int64_t b = (work + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > (1 << 30)) b = 1 << 30;
+  return (unsigned)b;
+}
+
+// Sort `m` keys (and a 32-bit index payload) on bits [0, nbits).
+static fj_status sort_pairs(uint64_t *&keys, uint64_t *&keys_alt, uint32_t *&idx,
+                            uint32_t *&idx_alt, int64_t m, int nbits, cudaStream_t st) {
+  if (m == 0) return FJ_OK;
+  cub::DoubleBuffer<uint64_t> dk(keys, keys_alt);
+  cub::DoubleBuffer<uint32_t> dv(idx, idx_alt);
+  size_t tmp = 0;
+  FJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, m, 0, nbits, st));
+  void *t = nullptr;
+  FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+  FJ_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, m, 0, nbits, st));
+  FJ_CUDA(cudaFreeAsync(t, st));
+  if (dk.Current() != keys) std::swap(keys, keys_alt);
+  if (dv.Current() != idx) std::swap(idx, idx_alt);
+  return FJ_OK;
+}
+
+static fj_status exclusive_scan_i64(int64_t *in, int64_t *out, int64_t count, cudaStream_t st) {
+  size_t tmp = 0;
+  FJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, count, st));
+  void *t = nullptr;
+  FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+  FJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, count, st));
+  FJ_CUDA(cudaFreeAsync(t, st));
+  return FJ_OK;
+}
+
+// Transpose the canonical in-CSR into the pull CSR (row u lists v with a_uv),
+// rows sorted.  Caller frees *ort, *ocol, *ow (cudaFree).
+fj_status transpose_in_csr(fj_graph *g, int64_t **ort, int32_t **ocol, float **ow) {
+  cudaStream_t st = g->stream;
+  const int64_t n = g->n, m = g->m;
+  const int nb = bits_for(n);
+  uint64_t *k0 = nullptr, *k1 = nullptr;
+  uint32_t *i0 = nullptr, *i1 = nullptr;
+  int64_t *cnt = nullptr;
+  FJ_CUDA(cudaMallocAsync(&k0, sizeof(uint64_t) * (m + 1), st));
+  FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint64_t) * (m + 1), st));
+  FJ_CUDA(cudaMallocAsync(&i0, sizeof(uint32_t) * (m + 1), st));
+  FJ_CUDA(cudaMallocAsync(&i1, sizeof(uint32_t) * (m + 1), st));
+  FJ_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * (n + 1), st));
+  FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (n + 1), st));
+  FJ_CUDA(cudaMalloc(ort, sizeof(int64_t) * (n + 1)));
+  FJ_CUDA(cudaMalloc(ocol, sizeof(int32_t) * (m + 1)));
+  *ow = nullptr;
+  if (g->in_w) FJ_CUDA(cudaMalloc(ow, sizeof(float) * (m + 1)));
+  k_out_keys<<<grid_for(n * 32), kBlock, 0, st>>>(n, g->in_rp, g->in_col, nb, k0, cnt);
+  k_iota_u32<<<grid_for(m), kBlock, 0, st>>>(m, i0);
+  FJ_TRY(sort_pairs(k0, k1, i0, i1, m, 2 * nb, st));
+  int *err = nullptr;
+  FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
+  FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  if (m > 0)
+    k_unpack_sorted<<<grid_for(m), kBlock, 0, st>>>(m, nb, k0, i0, g->in_w, *ocol, *ow, err);
+  FJ_TRY(exclusive_scan_i64(cnt, *ort, n + 1, st));
+  FJ_CUDA(cudaFreeAsync(err, st));
+  FJ_CUDA(cudaFreeAsync(k0, st));
+  FJ_CUDA(cudaFreeAsync(k1, st));
+  FJ_CUDA(cudaFreeAsync(i0, st));
+  FJ_CUDA(cudaFreeAsync(i1, st));
+  FJ_CUDA(cudaFreeAsync(cnt, st));
+  FJ_CUDA(cudaGetLastError());
+  return FJ_OK;
+}
+
+static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const int32_t *col_in,
+                             const float *w_in, int directed, cudaStream_t st, fj_graph *g) {
+  g->n = n;
+  g->m = nnz;
+  g->directed = directed ? 1 : 0;
+  g->weighted = w_in ? 1 : 0;
+  g->stream = st;
+  int dev = 0;
+  FJ_CUDA(cudaGetDevice(&dev));
+  FJ_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t m = nnz;
+  const int nb = bits_for(n);
+
+  // 1. stage
+  FJ_CUDA(cudaMalloc(&g->in_rp, sizeof(int64_t) * (n + 1)));
+  FJ_CUDA(cudaMalloc(&g->in_col, sizeof(int32_t) * (m + 1)));
+  if (w_in) FJ_CUDA(cudaMalloc(&g->in_w, sizeof(float) * (m + 1)));
+  int32_t *col_raw = nullptr;
+  float *w_raw = nullptr;
+  FJ_CUDA(cudaMallocAsync(&col_raw, sizeof(int32_t) * (m + 1), st));
+  if (w_in) FJ_CUDA(cudaMallocAsync(&w_raw, sizeof(float) * (m + 1), st));
+  FJ_CUDA(cudaMemcpyAsync(g->in_rp, rp_in, sizeof(int64_t) * (n + 1), cudaMemcpyDefault, st));
+  if (m > 0) {
+    FJ_CUDA(cudaMemcpyAsync(col_raw, col_in, sizeof(int32_t) * m, cudaMemcpyDefault, st));
+    if (w_in) FJ_CUDA(cudaMemcpyAsync(w_raw, w_in, sizeof(float) * m, cudaMemcpyDefault, st));
+  }
+
+  // 2. validate row_ptr before anything indexes with it
+  int *err = nullptr;
+  FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
+  FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  k_validate_rowptr<<<grid_for(n + 1), kBlock, 0, st>>>(n, m, g->in_rp, err);
+  int herr = 0;
+  FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  if (herr) {
+    cudaFreeAsync(err, st);
+    cudaFreeAsync(col_raw, st);
+    cudaFreeAsync(w_raw, st);
+    set_error("fj_graph_create: in_row_ptr must start at 0, be non-decreasing and end at nnz");
+    return FJ_ERR_INVALID;
+  }
+
+  // 3. canonical in-CSR
+  uint64_t *k0 = nullptr, *k1 = nullptr;
+  uint32_t *i0 = nullptr, *i1 = nullptr;
+  FJ_CUDA(cudaMallocAsync(&k0, sizeof(uint64_t) * (m + 1), st));
+  FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint64_t) * (m + 1), st));
+  FJ_CUDA(cudaMallocAsync(&i0, sizeof(uint32_t) * (m + 1), st));
+  FJ_CUDA(cudaMallocAsync(&i1, sizeof(uint32_t) * (m + 1), st));
+  k_in_keys<<<grid_for(n * 32), kBlock, 0, st>>>(n, g->in_rp, col_raw, w_raw, nb, k0, err);
+  k_iota_u32<<<grid_for(m), kBlock, 0, st>>>(m, i0);
+  FJ_TRY(sort_pairs(k0, k1, i0, i1, m, 2 * nb, st));
+  if (m > 0)
+    k_unpack_sorted<<<grid_for(m), kBlock, 0, st>>>(m, nb, k0, i0, w_raw, g->in_col, g->in_w, err);
+  FJ_CUDA(cudaFreeAsync(k0, st));
+  FJ_CUDA(cudaFreeAsync(k1, st));
+  FJ_CUDA(cudaFreeAsync(i0, st));
+  FJ_CUDA(cudaFreeAsync(i1, st));
+  FJ_CUDA(cudaFreeAsync(col_raw, st));
+  if (w_raw) FJ_CUDA(cudaFreeAsync(w_raw, st));
+  FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  FJ_CUDA(cudaGetLastError());
+  if (herr) {
+    cudaFreeAsync(err, st);
+    set_error("fj_graph_create: %s%s%s%s",
+              herr & 2 ? "column index out of range; " : "", herr & 4 ? "self-loop; " : "",
+              herr & 8 ? "weight not positive and finite; " : "",
+              herr & 16 ? "duplicate arc; " : "");
+    return FJ_ERR_INVALID;
+  }
+
+  // 4. pull CSR + degrees
+  int64_t *ort = nullptr;
+  int32_t *ocol = nullptr;
+  float *ow = nullptr;
+  FJ_TRY(transpose_in_csr(g, &ort, &ocol, &ow));
+  FJ_CUDA(cudaMalloc(&g->deg, sizeof(double) * n));
+  k_row_sums<<<grid_for(n * 32), kBlock, 0, st>>>(n, ort, ow, g->deg);
+
+  // 5. symmetry of undirected input
+  if (!g->directed && m > 0) {
+    k_neq<int64_t><<<grid_for(n + 1), kBlock, 0, st>>>(n + 1, ort, g->in_rp, err, 32);
+    k_neq<int32_t><<<grid_for(m), kBlock, 0, st>>>(m, ocol, g->in_col, err, 32);
+    if (ow) k_neq<float><<<grid_for(m), kBlock, 0, st>>>(m, ow, g->in_w, err, 32);
+    FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FJ_CUDA(cudaStreamSynchronize(st));
+    if (herr) {
+      cudaFree(ort);
+      cudaFree(ocol);
+      cudaFree(ow);
+      cudaFreeAsync(err, st);
+      set_error("fj_graph_create: directed = 0 but the arc set is not symmetric with equal weights");
+      return FJ_ERR_INVALID;
+    }
+  }
+  FJ_CUDA(cudaFreeAsync(err, st));
+
+  // 6. sweep layout (1 color)
+  fj_status s = build_layout_from_out(g, ort, ocol, ow, nullptr, 1, &g->async_layout);
+  cudaFree(ort);
+  cudaFree(ocol);
+  cudaFree(ow);
+  if (s != FJ_OK) return s;
+  FJ_CUDA(cudaStreamSynchronize(st));
+  FJ_CUDA(cudaGetLastError());
+  return FJ_OK;
+}
+
+}  // namespace fj
+
+extern "C" {
+
+fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t *in_row_ptr, const int32_t *in_col,
+                          const float *in_w, int directed, void *cuda_stream, fj_graph_t *out) {
+  if (!out) {
+    fj::set_error("fj_graph_create: out is NULL");
+    return FJ_ERR_INVALID;
+  }
+  *out = nullptr;
+  if (n < 1 || n >= (int64_t(1) << 31) || nnz < 0 || nnz >= (int64_t(1) << 40) || !in_row_ptr ||
+      (nnz > 0 && !in_col)) {
+    fj::set_error("fj_graph_create: need 1 <= n < 2^31, nnz >= 0, non-null row_ptr/col");
+    return FJ_ERR_INVALID;
+  }
+  fj_graph *g = new fj_graph();
+  fj_status s = fj::create_impl(n, nnz, in_row_ptr, in_col, in_w, directed,
+                                (cudaStream_t)cuda_stream, g);
+  if (s != FJ_OK) {
+    fj_graph_destroy(g);
+    return s;
+  }
+  *out = g;
+  return FJ_OK;
+}
+
+fj_status fj_graph_destroy(fj_graph_t g) {
+  if (!g) return FJ_OK;
+  cudaStreamSynchronize(g->stream);
+  cudaFree(g->in_rp);
+  cudaFree(g->in_col);
+  cudaFree(g->in_w);
+  cudaFree(g->deg);
+  cudaFree(g->colors);
+  g->async_layout.release();
+  g->color_layout.release();
+  delete g;
+  return FJ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,206 @@
+// layout.cu — the sweep layout (§8 row a1, K3): rows of the pull CSR
+// permuted to (color, length class, id) order so that every task handles rows
+// of one color and of similar length, and the work list (tasks) that the
+// persistent sweep kernel claims dynamically.
+//
+// Permuted ids make the per-row state (s, ẑ, 1+d) streams coalesced; within
+// one class the original id order is kept (stable), so R-MAT hubs (low ids)
+// and lattice neighbours stay close in memory.
+#include <algorithm>
+#include <cub/cub.cuh>
+
+#include "fj_internal.cuh"
+
+namespace fj {
+
+static constexpr int kRowsPerGroupPerTask = 4;
+static constexpr int kClasses = 7;  // 0..5 GROUP (G = 1<<k), 6 long
+
+__host__ __device__ static inline int row_class(int64_t L) {
+  if (L <= 4) return 0;
+  if (L <= 8) return 1;
+  if (L <= 16) return 2;
+  if (L <= 32) return 3;
+  if (L <= 64) return 4;
+  if (L <= 256) return 5;
+  return 6;
+}
+
+static unsigned gridn(int64_t work) {
+  int64_t b = (work + kBlock - 1) / kBlock;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 1 << 30));
+}
+
+__global__ void k_layout_keys(int64_t n, const int64_t *__restrict__ ort,
+                              const int32_t *__restrict__ color, int ncolors,
+                              uint64_t *__restrict__ keys, unsigned long long *__restrict__ gcount) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  int64_t L = ort[u + 1] - ort[u];
+  uint64_t grp;
+  if (L == 0) {
+    grp = (uint64_t)ncolors * kClasses;  // empty rows last, never swept
+  } else {
+    int c = color ? color[u] : 0;
+    grp = (uint64_t)c * kClasses + (uint64_t)(kClasses - 1 - row_class(L));
+  }
+  atomicAdd(&gcount[grp], 1ull);
+  keys[u] = (grp << 31) | (uint64_t)u;
+}
+
+__global__ void k_perm(int64_t n, const uint64_t *__restrict__ keys, const int64_t *__restrict__ ort,
+                       int32_t *__restrict__ perm, int32_t *__restrict__ iperm,
+                       int64_t *__restrict__ len) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t u = (int32_t)(keys[i] & 0x7fffffffull);
+  perm[i] = u;
+  iperm[u] = (int32_t)i;
+  len[i] = ort[u + 1] - ort[u];
+}
+
+// warp per new row: copy the out-row of perm[i] with relabelled columns
+__global__ void k_copy_rows(int64_t n, const int32_t *__restrict__ perm,
+                            const int32_t *__restrict__ iperm, const int64_t *__restrict__ ort,
+                            const int32_t *__restrict__ ocol, const float *__restrict__ ow,
+                            const double *__restrict__ deg, const int64_t *__restrict__ rp,
+                            int32_t *__restrict__ col, float *__restrict__ w,
+                            double *__restrict__ d1) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    int32_t u = perm[i];
+    int64_t b = ort[u], e = ort[u + 1], o = rp[i];
+    for (int64_t k = lane; k < e - b; k += 32) {
+      col[o + k] = iperm[ocol[b + k]];
+      if (w) w[o + k] = ow[b + k];
+    }
+    if (lane == 0 && d1) d1[i] = 1.0 + deg[u];
+  }
+}
+
+fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *ocol,
+                                const float *ow, const int32_t *color, int ncolors, Layout *L) {
+  cudaStream_t st = g->stream;
+  const int64_t n = g->n, m = g->m;
+  L->release();
+  L->n = n;
+  L->m = m;
+  L->ncolors = ncolors;
+  const int ngroups = ncolors * kClasses + 1;
+
+  uint64_t *k0 = nullptr, *k1 = nullptr;
+  unsigned long long *gcount = nullptr;
+  int64_t *len = nullptr;
+  FJ_CUDA(cudaMallocAsync(&k0, sizeof(uint64_t) * n, st));
+  FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint64_t) * n, st));
+  FJ_CUDA(cudaMallocAsync(&gcount, sizeof(unsigned long long) * ngroups, st));
+  FJ_CUDA(cudaMemsetAsync(gcount, 0, sizeof(unsigned long long) * ngroups, st));
+  FJ_CUDA(cudaMallocAsync(&len, sizeof(int64_t) * (n + 1), st));
+  FJ_CUDA(cudaMemsetAsync(len + n, 0, sizeof(int64_t), st));
+  k_layout_keys<<<gridn(n), kBlock, 0, st>>>(n, ort, color, ncolors, k0, gcount);
+
+  int gbits = 1;
+  while ((1 << gbits) <= ngroups) gbits++;
+  {
+    cub::DoubleBuffer<uint64_t> dk(k0, k1);
+    size_t tmp = 0;
+    FJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, dk, n, 0, 31 + gbits, st));
+    void *t = nullptr;
+    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    FJ_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, dk, n, 0, 31 + gbits, st));
+    FJ_CUDA(cudaFreeAsync(t, st));
+    if (dk.Current() != k0) std::swap(k0, k1);
+  }
+  FJ_CUDA(cudaMalloc(&L->perm, sizeof(int32_t) * n));
+  FJ_CUDA(cudaMalloc(&L->iperm, sizeof(int32_t) * n));
+  FJ_CUDA(cudaMalloc(&L->rp, sizeof(int64_t) * (n + 1)));
+  FJ_CUDA(cudaMalloc(&L->col, sizeof(int32_t) * (m + 1)));
+  if (ow) FJ_CUDA(cudaMalloc(&L->w, sizeof(float) * (m + 1)));
+  if (g->weighted) FJ_CUDA(cudaMalloc(&L->d1, sizeof(double) * n));
+  k_perm<<<gridn(n), kBlock, 0, st>>>(n, k0, ort, L->perm, L->iperm, len);
+  {
+    size_t tmp = 0;
+    FJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, len, L->rp, n + 1, st));
+    void *t = nullptr;
+    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    FJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, len, L->rp, n + 1, st));
+    FJ_CUDA(cudaFreeAsync(t, st));
+  }
+  k_copy_rows<<<gridn(n * 32), kBlock, 0, st>>>(n, L->perm, L->iperm, ort, ocol, ow, g->deg, L->rp,
+                                                L->col, L->w, L->d1);
+
+  int64_t *dmax = nullptr;
+  int64_t hmax = 0;
+  FJ_CUDA(cudaMallocAsync(&dmax, sizeof(int64_t), st));
+  {
+    size_t tmp = 0;
+    FJ_CUDA(cub::DeviceReduce::Max(nullptr, tmp, len, dmax, n, st));
+    void *t = nullptr;
+    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    FJ_CUDA(cub::DeviceReduce::Max(t, tmp, len, dmax, n, st));
+    FJ_CUDA(cudaFreeAsync(t, st));
+  }
+  FJ_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaFreeAsync(dmax, st));
+  std::vector<unsigned long long> hcount(ngroups);
+  FJ_CUDA(cudaMemcpyAsync(hcount.data(), gcount, sizeof(unsigned long long) * ngroups,
+                          cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+
+  // group g covers new rows [gstart[g], gstart[g] + hcount[g])
+  std::vector<int64_t> gstart(ngroups + 1, 0);
+  for (int q = 0; q < ngroups; q++) gstart[q + 1] = gstart[q] + (int64_t)hcount[q];
+  L->empty_rows = (int64_t)hcount[ngroups - 1];
+  L->active_rows = n - L->empty_rows;
+
+  // lengths of long rows (class 6) for piece counts
+  std::vector<Task> tasks;
+  L->phase_begin.assign(ncolors + 1, 0);
+  int slot = 0;
+  for (int c = 0; c < ncolors; c++) {
+    L->phase_begin[c] = (int)tasks.size();
+    for (int cd = 0; cd < kClasses; cd++) {  // cd = 6 - class: long rows first
+      int q = c * kClasses + cd;
+      int cls = kClasses - 1 - cd;
+      int64_t r0 = gstart[q], r1 = gstart[q + 1];
+      if (r1 <= r0) continue;
+      if (cls == 6) {
+        std::vector<int64_t> rph(r1 - r0 + 1);
+        FJ_CUDA(cudaMemcpy(rph.data(), L->rp + r0, sizeof(int64_t) * (r1 - r0 + 1),
+                           cudaMemcpyDeviceToHost));
+        for (int64_t i = r0; i < r1; i++) {
+          int64_t len_i = rph[i - r0 + 1] - rph[i - r0];
+          int np = (int)((len_i + kPiece - 1) / kPiece);
+          for (int p = 0; p < np; p++)
+            tasks.push_back(Task{(int32_t)i, p, kLong | (np << 8), slot});
+          slot += np;
+        }
+      } else {
+        int G = 1 << cls;
+        int64_t per = (int64_t)(kBlock / G) * kRowsPerGroupPerTask;
+        for (int64_t a = r0; a < r1; a += per)
+          tasks.push_back(Task{(int32_t)a, (int32_t)std::min(r1, a + per), cls, 0});
+      }
+    }
+  }
+  L->phase_begin[ncolors] = (int)tasks.size();
+  L->ntasks = (int)tasks.size();
+  L->npartials = slot;
+  L->max_len = hmax;
+  FJ_CUDA(cudaMalloc(&L->tasks, sizeof(Task) * std::max<size_t>(1, tasks.size())));
+  if (!tasks.empty())
+    FJ_CUDA(cudaMemcpy(L->tasks, tasks.data(), sizeof(Task) * tasks.size(), cudaMemcpyHostToDevice));
+  FJ_CUDA(cudaMalloc(&L->d_phase_begin, sizeof(int) * (ncolors + 1)));
+  FJ_CUDA(cudaMemcpy(L->d_phase_begin, L->phase_begin.data(), sizeof(int) * (ncolors + 1),
+                     cudaMemcpyHostToDevice));
+  FJ_CUDA(cudaFreeAsync(k0, st));
+  FJ_CUDA(cudaFreeAsync(k1, st));
+  FJ_CUDA(cudaFreeAsync(gcount, st));
+  FJ_CUDA(cudaFreeAsync(len, st));
+  FJ_CUDA(cudaGetLastError());
+  return FJ_OK;
+}
+
+}  // namespace fj

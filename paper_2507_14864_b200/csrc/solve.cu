@@ -1,0 +1,785 @@
+// solve.cu — the hot path (§8 rows a2–a7): shift/init, persistent sweep
+// kernel with on-device loop control, fp64 residual certificate, unshift,
+// and the measures.
+//
+// Method.  The paper's push loop (Alg. 1/3, P:204–228,
+// P:436–463) relaxes one queued node at a time; Theorem 3 shows
+// each relaxation is a Gauss–Seidel update of row v of (I+L)ẑ = s with the
+// residual r_v = s_v − ((I+L)ẑ)_v, and Lemma 3 shows the estimate is
+// correct for any order and amount of relaxation.  A sweep here evaluates the
+// residual of every non-empty row from the current ẑ (a pull over the row's
+// arcs, fp64 accumulation) and relaxes exactly the rows the paper would have
+// queued, |r_v| > h_v (P:221/453/458):
+//        ẑ_v ← ẑ_v + ω r_v / (1 + d_v)                      (equ:sor1)
+// ASYNC: one phase per sweep, rows updated in place (later rows see earlier
+// updates, as in Gauss–Seidel).  COLORED: one phase per color; rows of one
+// color share no arc, so each phase equals sequential SOR over that color.
+// The loop ends on the first sweep that relaxes nothing: every residual was
+// then evaluated on the final ẑ and is ≤ h — the paper's "Q = ∅".
+// A separate compensated fp64 pass (certificate) re-checks max |r_v|/h_v.
+#include <cuda/atomic>
+#include <cub/cub.cuh>
+
+#include "fj_internal.cuh"
+
+namespace fj {
+
+enum Mode { RELAX = 0, CERT = 1, DIS = 2 };
+
+struct Scalars {
+  double c;        // shift (Alg. 2; reading R5)
+  double eps_p;    // ε' = σε/(c+σ)
+  double hs;       // h = hs·s'            (s_min ≥ 0)
+  double heps;     // h = heps·max(hs·s', σ) (s_min < 0, floored, R5)
+  double sigma;
+  double sentinel; // divergence sentinel 1e6·max|s'|
+  int floored;
+  int bad_input;
+};
+
+struct SweepCounters {
+  unsigned long long upd, eu;
+  unsigned long long bad, pad;
+};
+
+struct KP {
+  const int64_t *__restrict__ rp;
+  const int32_t *__restrict__ col;
+  const float *__restrict__ w;
+  const double *__restrict__ d1;
+  const Task *__restrict__ tasks;
+  const float *__restrict__ s;  // layout order
+  double *z;                    // ẑ' (RELAX/CERT) or z (DIS), layout order
+  const Scalars *sc;
+  double omega;
+  double2 *partial;
+  int *arrive;
+  const int *phase_begin;
+  int ncolors;
+  int ntasks_all;
+  int max_sweeps;
+  unsigned *ctr;          // [3]
+  SweepCounters *cnt;     // [3]
+  unsigned *bar;          // [2]
+  unsigned long long *out;  // [4] sweeps, relaxations, edge updates, reason
+  unsigned long long *cert_max;  // double bits
+  double *dis;
+};
+
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ void dd_add(dd &a, double x) {
+  double s = a.hi + x;
+  double bb = s - a.hi;
+  a.lo += (a.hi - (s - bb)) + (x - bb);
+  a.hi = s;
+}
+__device__ __forceinline__ void dd_addprod(dd &a, double x, double y) {
+  double p = x * y;
+  double e = fma(x, y, -p);
+  dd_add(a, p);
+  a.lo += e;
+}
+
+template <int MODE>
+struct AccT {
+  using T = double;
+};
+template <>
+struct AccT<CERT> {
+  using T = dd;
+};
+
+__device__ __forceinline__ void acc_zero(double &a) { a = 0.0; }
+__device__ __forceinline__ void acc_zero(dd &a) { a.hi = a.lo = 0.0; }
+__device__ __forceinline__ double acc_shfl(double a, unsigned mask, int off) {
+  return __shfl_xor_sync(mask, a, off);
+}
+__device__ __forceinline__ dd acc_shfl(dd a, unsigned mask, int off) {
+  dd b;
+  b.hi = __shfl_xor_sync(mask, a.hi, off);
+  b.lo = __shfl_xor_sync(mask, a.lo, off);
+  return b;
+}
+__device__ __forceinline__ void acc_merge(double &a, double b) { a += b; }
+__device__ __forceinline__ void acc_merge(dd &a, dd b) {
+  dd_add(a, b.hi);
+  a.lo += b.lo;
+}
+
+struct TAcc {
+  unsigned long long upd, eu, bad;
+  double certmax, dis;
+};
+
+// ---------------------------------------------------------- per-row finish
+__device__ __forceinline__ double threshold(const Scalars &S, double sp) {
+  // h_v (reading R5): ε' s'_v, or (ε/2)·max(σ s'_v/(c+σ), σ) for signed s
+  return S.floored ? S.heps * fmax(S.hs * sp, S.sigma) : S.hs * sp;
+}
+
+template <bool W>
+__device__ __forceinline__ void relax_row(const KP &p, const Scalars &S, int row, int len,
+                                          double total, TAcc &t) {
+  const double sp = (double)p.s[row] + S.c;              // s' = s + c
+  const double h = threshold(S, sp);
+  const double zi = __ldcg(p.z + row);
+  const double d1 = W ? p.d1[row] : (double)(len + 1);   // a_ii = 1 + d_i (Thm 3)
+  const double rho = (sp - d1 * zi) + total;              // r_i = s'_i − ((I+L)ẑ)_i
+  const double ar = fabs(rho);
+  if (ar > h) {                                           // |r_i| > h_i
+    __stcg(p.z + row, zi + p.omega * rho / d1);           // equ:sor1
+    t.upd++;
+    t.eu += (unsigned long long)len;
+  }
+  if (!(ar <= S.sentinel)) t.bad = 1;
+}
+
+template <bool W>
+__device__ __forceinline__ void cert_row(const KP &p, const Scalars &S, int row, int len, dd total,
+                                         TAcc &t) {
+  const double sp = (double)p.s[row] + S.c;
+  const double h = threshold(S, sp);
+  const double zi = p.z[row];
+  const double d1 = W ? p.d1[row] : (double)(len + 1);
+  dd_add(total, sp);
+  dd_addprod(total, -d1, zi);
+  const double ratio = fabs(total.hi + total.lo) / h;
+  if (!(ratio <= t.certmax)) t.certmax = ratio;  // NaN sticks
+}
+
+// arc accumulation
+template <int MODE, bool W>
+__device__ __forceinline__ void arc_acc(typename AccT<MODE>::T &a, const KP &p, int64_t k,
+                                        double zr) {
+  const int j = __ldg(p.col + k);
+  const double wk = W ? (double)__ldg(p.w + k) : 1.0;
+  if constexpr (MODE == RELAX) {
+    a = fma(wk, __ldcg(p.z + j), a);
+  } else if constexpr (MODE == CERT) {
+    if (W) dd_addprod(a, wk, p.z[j]);
+    else dd_add(a, p.z[j]);
+  } else {
+    const double dz = zr - p.z[j];
+    a = fma(wk * dz, dz, a);
+  }
+}
+
+template <int MODE, int G, bool W>
+__device__ __forceinline__ void do_group(const KP &p, const Scalars &S, int rb, int re, TAcc &t) {
+  using A = typename AccT<MODE>::T;
+  const int lane = threadIdx.x & (G - 1);
+  const int grp = threadIdx.x / G;
+  const unsigned gmask =
+      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  for (int row = rb + grp; row < re; row += kBlock / G) {
+    const int64_t beg = p.rp[row], end = p.rp[row + 1];
+    const double zr = (MODE == DIS) ? p.z[row] : 0.0;
+    A a;
+    acc_zero(a);
+#pragma unroll 4
+    for (int64_t k = beg + lane; k < end; k += G) arc_acc<MODE, W>(a, p, k, zr);
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) acc_merge(a, acc_shfl(a, gmask, off));
+    if (lane == 0) {
+      const int len = (int)(end - beg);
+      if constexpr (MODE == RELAX) relax_row<W>(p, S, row, len, a, t);
+      else if constexpr (MODE == CERT) cert_row<W>(p, S, row, len, a, t);
+      else t.dis += a;
+    }
+  }
+}
+
+// block-wide deterministic reduction; result valid in thread 0
+template <class A>
+__device__ __forceinline__ A block_reduce(A a, A *sm) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc_merge(a, acc_shfl(a, 0xffffffffu, off));
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sm[w] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < kBlock / 32; i++) acc_merge(a, sm[i]);
+  }
+  __syncthreads();
+  return a;
+}
+
+template <int MODE, bool W>
+__device__ __forceinline__ void do_long(const KP &p, const Scalars &S, const Task &tk, TAcc &t,
+                                        void *smem) {
+  using A = typename AccT<MODE>::T;
+  const int row = tk.a, piece = tk.b, np = tk.kind >> 8, slot = tk.slot;
+  const int64_t beg = p.rp[row], end = p.rp[row + 1];
+  const int64_t a0 = beg + (int64_t)piece * kPiece;
+  const int64_t a1 = min(end, a0 + (int64_t)kPiece);
+  const double zr = (MODE == DIS) ? p.z[row] : 0.0;
+  A a;
+  acc_zero(a);
+#pragma unroll 4
+  for (int64_t k = a0 + threadIdx.x; k < a1; k += kBlock) arc_acc<MODE, W>(a, p, k, zr);
+  a = block_reduce<A>(a, (A *)smem);
+  if (threadIdx.x != 0) return;
+  const int len = (int)(end - beg);
+  if constexpr (MODE == DIS) {
+    t.dis += a;
+  } else {
+    if (np > 1) {
+      double2 v;
+      if constexpr (MODE == CERT) v = make_double2(a.hi, a.lo);
+      else v = make_double2(a, 0.0);
+      __stcg(p.partial + slot + piece, v);
+      __threadfence();
+      const int old = atomicAdd(p.arrive + slot, 1);
+      if (old != np - 1) return;
+      __threadfence();
+      acc_zero(a);
+      for (int q = 0; q < np; q++) {  // fixed order ⇒ deterministic row sum
+        const double2 x = __ldcg(p.partial + slot + q);
+        if constexpr (MODE == CERT) acc_merge(a, dd{x.x, x.y});
+        else a += x.x;
+      }
+      p.arrive[slot] = 0;
+    }
+    if constexpr (MODE == RELAX) relax_row<W>(p, S, row, len, a, t);
+    else cert_row<W>(p, S, row, len, a, t);
+  }
+}
+
+template <int MODE, bool W>
+__device__ __forceinline__ void dispatch(const KP &p, const Scalars &S, const Task &tk, TAcc &t,
+                                         void *smem) {
+  switch (tk.kind & 0xff) {
+    case kG1: do_group<MODE, 1, W>(p, S, tk.a, tk.b, t); break;
+    case kG2: do_group<MODE, 2, W>(p, S, tk.a, tk.b, t); break;
+    case kG4: do_group<MODE, 4, W>(p, S, tk.a, tk.b, t); break;
+    case kG8: do_group<MODE, 8, W>(p, S, tk.a, tk.b, t); break;
+    case kG16: do_group<MODE, 16, W>(p, S, tk.a, tk.b, t); break;
+    case kG32: do_group<MODE, 32, W>(p, S, tk.a, tk.b, t); break;
+    default: do_long<MODE, W>(p, S, tk, t, smem); break;
+  }
+}
+
+// Grid-wide barrier of a cooperative launch (all CTAs co-resident).
+__device__ __forceinline__ void grid_sync(unsigned *bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    cuda::atomic_ref<unsigned, cuda::thread_scope_device> cnt(bar[0]), gen(bar[1]);
+    const unsigned g = gen.load(cuda::memory_order_relaxed);
+    __threadfence();
+    if (cnt.fetch_add(1u, cuda::memory_order_acq_rel) == gridDim.x - 1) {
+      cnt.store(0u, cuda::memory_order_relaxed);
+      gen.store(g + 1u, cuda::memory_order_release);
+    } else {
+      while (gen.load(cuda::memory_order_acquire) == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int claim(unsigned *ctr, int *s_task) {
+  if (threadIdx.x == 0) *s_task = (int)atomicAdd(ctr, 1u);
+  __syncthreads();
+  const int t = *s_task;
+  __syncthreads();
+  return t;
+}
+
+// ------------------------------------------------------ persistent sweeps
+template <bool W>
+__global__ void __launch_bounds__(kBlock) k_sweep(KP p) {
+  __shared__ int s_task;
+  __shared__ double s_red[kBlock / 32];
+  __shared__ unsigned long long s_dec[3];
+  const Scalars S = *p.sc;
+  TAcc t{};
+  unsigned long long tot_upd = 0, tot_eu = 0;
+  int sweeps = 0, reason = 1;
+  int phase = 0;
+  for (int sw = 0; sw < p.max_sweeps; ++sw) {
+    for (int k = 0; k < p.ncolors; ++k, ++phase) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[(phase + 2) % 3] = 0u;
+      const int t0 = p.phase_begin[k], nt = p.phase_begin[k + 1] - t0;
+      for (;;) {
+        const int ti = claim(p.ctr + phase % 3, &s_task);
+        if (ti >= nt) break;
+        const Task tk = p.tasks[t0 + ti];
+        dispatch<RELAX, W>(p, S, tk, t, s_red);
+      }
+      if (k + 1 < p.ncolors) grid_sync(p.bar);
+    }
+    // commit this sweep's counters (warp-aggregated atomics)
+    unsigned long long u = t.upd, e = t.eu, b = t.bad;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      u += __shfl_xor_sync(0xffffffffu, u, off);
+      e += __shfl_xor_sync(0xffffffffu, e, off);
+      b |= __shfl_xor_sync(0xffffffffu, b, off);
+    }
+    SweepCounters *c = p.cnt + sw % 3;
+    if ((threadIdx.x & 31) == 0 && (u | e | b)) {
+      atomicAdd(&c->upd, u);
+      atomicAdd(&c->eu, e);
+      if (b) atomicOr(&c->bad, b);
+    }
+    t.upd = t.eu = t.bad = 0;
+    grid_sync(p.bar);
+    if (threadIdx.x == 0) {
+      s_dec[0] = __ldcg(&c->upd);
+      s_dec[1] = __ldcg(&c->eu);
+      s_dec[2] = __ldcg(&c->bad);
+      if (blockIdx.x == 0) {
+        SweepCounters *z = p.cnt + (sw + 2) % 3;
+        z->upd = z->eu = z->bad = 0;
+      }
+    }
+    __syncthreads();
+    tot_upd += s_dec[0];
+    tot_eu += s_dec[1];
+    sweeps = sw + 1;
+    const bool bad = s_dec[2] != 0, done = s_dec[0] == 0;
+    __syncthreads();
+    if (bad) { reason = 2; break; }
+    if (done) { reason = 0; break; }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.out[0] = (unsigned long long)sweeps;
+    p.out[1] = tot_upd;
+    p.out[2] = tot_eu;
+    p.out[3] = (unsigned long long)reason;
+  }
+}
+
+// ------------------------------------------ one pass over all tasks (CERT/DIS)
+template <int MODE, bool W>
+__global__ void __launch_bounds__(kBlock) k_pass(KP p) {
+  __shared__ int s_task;
+  __shared__ dd s_red[kBlock / 32];
+  Scalars S{};
+  if (MODE == CERT) S = *p.sc;
+  TAcc t{};
+  for (;;) {
+    const int ti = claim(p.ctr, &s_task);
+    if (ti >= p.ntasks_all) break;
+    const Task tk = p.tasks[ti];
+    dispatch<MODE, W>(p, S, tk, t, s_red);
+  }
+  if constexpr (MODE == CERT) {
+    double m = t.certmax;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (isnan(t.certmax)) m = t.certmax;
+    if ((threadIdx.x & 31) == 0 && m != 0.0)
+      atomicMax(p.cert_max, (unsigned long long)__double_as_longlong(m));
+  } else {
+    double sdis = t.dis;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sdis += __shfl_xor_sync(0xffffffffu, sdis, off);
+    if ((threadIdx.x & 31) == 0 && sdis != 0.0) atomicAdd(p.dis, sdis);
+  }
+}
+
+// ----------------------------------------------------------- node kernels
+__global__ void k_scalars(const float *__restrict__ smin, const float *__restrict__ smax,
+                          double eps, double sigma, double c_override, Scalars *S) {
+  const double lo = (double)*smin, hi = (double)*smax;
+  Scalars s{};
+  s.bad_input = !(isfinite(lo) && isfinite(hi));
+  s.sigma = sigma;
+  s.c = c_override > 0 ? c_override : sigma + fmax(0.0, -lo);   // reading R5
+  s.eps_p = sigma / (s.c + sigma) * eps;
+  s.floored = lo < 0.0;
+  s.hs = s.floored ? sigma / (s.c + sigma) : s.eps_p;
+  s.heps = 0.5 * eps;
+  s.sentinel = 1e6 * fmax(fabs(hi + s.c), fabs(lo + s.c));
+  *S = s;
+}
+
+// s into layout order; ẑ' = 0 (Alg. 1 init) except rows with no arcs,
+// whose equation is (1 + 0) z_v = s'_v: solved exactly (ẑ'_v = s'_v)
+__global__ void k_init(int64_t n, const int32_t *__restrict__ perm, const int64_t *__restrict__ rp,
+                       const float *__restrict__ s, const Scalars *__restrict__ S,
+                       float *__restrict__ s_l, double *__restrict__ z) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float si = s[perm[i]];
+  s_l[i] = si;
+  z[i] = (rp[i + 1] == rp[i]) ? (double)si + S->c : 0.0;
+}
+
+__global__ void k_finalize(int64_t n, const int32_t *__restrict__ iperm, const double *__restrict__ z,
+                           const Scalars *__restrict__ S, float *__restrict__ zout,
+                           double *__restrict__ zprime) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const double zp = z[iperm[u]];
+  zout[u] = (float)(zp - S->c);  // ẑ_v − c
+  if (zprime) zprime[u] = zp;
+}
+
+// measures node pass: z into layout order (fp64) + Σz
+__global__ void k_meas_nodes1(int64_t n, const int32_t *__restrict__ perm,
+                              const float *__restrict__ z, double *__restrict__ zl,
+                              double *__restrict__ sums) {
+  __shared__ double sm[kBlock / 32];
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (i < n) {
+    v = (double)z[perm[i]];
+    zl[i] = v;
+  }
+  v = block_reduce<double>(v, sm);
+  if (threadIdx.x == 0) atomicAdd(sums, v);
+}
+
+// Σ (z − mean)², Σ (z − s)², Σ z²  (two-pass mean, reading R15)
+__global__ void k_meas_nodes2(int64_t n, const float *__restrict__ z, const float *__restrict__ s,
+                              double *__restrict__ sums) {
+  __shared__ double sm[kBlock / 32];
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const double mean = sums[0] / (double)n;
+  double P = 0, I = 0, C = 0;
+  if (i < n) {
+    const double zi = (double)z[i];
+    P = (zi - mean) * (zi - mean);
+    C = zi * zi;
+    if (s) I = (zi - (double)s[i]) * (zi - (double)s[i]);
+  }
+  P = block_reduce<double>(P, sm);
+  I = block_reduce<double>(I, sm);
+  C = block_reduce<double>(C, sm);
+  if (threadIdx.x == 0) {
+    atomicAdd(sums + 1, P);
+    atomicAdd(sums + 2, I);
+    atomicAdd(sums + 3, C);
+  }
+}
+
+// ------------------------------------------------------------- host side
+static unsigned gridn(int64_t work) {
+  int64_t b = (work + kBlock - 1) / kBlock;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 1 << 30));
+}
+
+static int persistent_grid(const void *fn, int num_sms) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0);
+  if (per_sm < 1) per_sm = 1;
+  return per_sm * num_sms;
+}
+
+struct Staged {
+  const float *dev = nullptr;
+  float *owned = nullptr;
+};
+
+static fj_status stage_in(const float *src, int64_t n, cudaStream_t st, Staged &out) {
+  if (is_device_ptr(src)) {
+    out.dev = src;
+    return FJ_OK;
+  }
+  FJ_CUDA(cudaMallocAsync(&out.owned, sizeof(float) * n, st));
+  FJ_CUDA(cudaMemcpyAsync(out.owned, src, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+  out.dev = out.owned;
+  return FJ_OK;
+}
+
+static KP make_kp(const fj_graph *g, const Layout &L) {
+  KP p{};
+  p.rp = L.rp;
+  p.col = L.col;
+  p.w = L.w;
+  p.d1 = L.d1;
+  p.tasks = L.tasks;
+  p.phase_begin = L.d_phase_begin;
+  p.ncolors = L.ncolors;
+  p.ntasks_all = L.ntasks;
+  return p;
+}
+
+fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, const fj_opts *o,
+                     float *z_out, fj_stats *st_out) {
+  cudaStream_t st = g->stream;
+  const int64_t n = g->n;
+  fj_stats stats{};
+  int method = o->method;
+  if (method == FJ_METHOD_AUTO) method = (omega == 1.0) ? FJ_METHOD_ASYNC : FJ_METHOD_COLORED;
+  if (method == FJ_METHOD_COLORED && !g->colors) FJ_TRY(build_coloring(g));
+  if (method == FJ_METHOD_PUSH) {
+    set_error("fj_solve: FJ_METHOD_PUSH is not available in this build");
+    return FJ_ERR_INVALID;
+  }
+  const Layout &L = (method == FJ_METHOD_COLORED) ? g->color_layout : g->async_layout;
+  const bool W = g->weighted != 0;
+
+  cudaEvent_t e0, e1, es0, es1, ec0, ec1;
+  FJ_CUDA(cudaEventCreate(&e0));
+  FJ_CUDA(cudaEventCreate(&e1));
+  FJ_CUDA(cudaEventCreate(&es0));
+  FJ_CUDA(cudaEventCreate(&es1));
+  FJ_CUDA(cudaEventCreate(&ec0));
+  FJ_CUDA(cudaEventCreate(&ec1));
+  FJ_CUDA(cudaEventRecord(e0, st));
+
+  Staged s{};
+  FJ_TRY(stage_in(s_in, n, st, s));
+  const bool zdev = is_device_ptr(z_out);
+  const bool zpdev = o->zprime_out && is_device_ptr(o->zprime_out);
+
+  // workspace (stream-ordered pool allocations)
+  float *s_l = nullptr, *smin = nullptr, *smax = nullptr, *zo = nullptr;
+  double *z = nullptr, *zp = nullptr;
+  double2 *partial = nullptr;
+  int *arrive = nullptr;
+  Scalars *S = nullptr;
+  unsigned *ctl = nullptr;  // ctr[3] + bar[2]
+  SweepCounters *cnt = nullptr;
+  unsigned long long *outv = nullptr, *certbits = nullptr;
+  FJ_CUDA(cudaMallocAsync(&s_l, sizeof(float) * n, st));
+  FJ_CUDA(cudaMallocAsync(&z, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&smin, sizeof(float) * 2, st));
+  smax = smin + 1;
+  FJ_CUDA(cudaMallocAsync(&S, sizeof(Scalars), st));
+  FJ_CUDA(cudaMallocAsync(&partial, sizeof(double2) * std::max(1, L.npartials), st));
+  FJ_CUDA(cudaMallocAsync(&arrive, sizeof(int) * std::max(1, L.npartials), st));
+  FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
+  FJ_CUDA(cudaMallocAsync(&ctl, sizeof(unsigned) * 8, st));
+  FJ_CUDA(cudaMallocAsync(&cnt, sizeof(SweepCounters) * 3, st));
+  FJ_CUDA(cudaMallocAsync(&outv, sizeof(unsigned long long) * 8, st));
+  certbits = outv + 4;
+  if (!zdev) FJ_CUDA(cudaMallocAsync(&zo, sizeof(float) * n, st));
+  if (o->zprime_out && !zpdev) FJ_CUDA(cudaMallocAsync(&zp, sizeof(double) * n, st));
+
+  // a2: shift and init (Alg. 2)
+  {
+    size_t tmp = 0;
+    FJ_CUDA(cub::DeviceReduce::Min(nullptr, tmp, s.dev, smin, n, st));
+    size_t tmp2 = 0;
+    FJ_CUDA(cub::DeviceReduce::Max(nullptr, tmp2, s.dev, smax, n, st));
+    tmp = std::max(tmp, tmp2);
+    void *t = nullptr;
+    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    FJ_CUDA(cub::DeviceReduce::Min(t, tmp, s.dev, smin, n, st));
+    FJ_CUDA(cub::DeviceReduce::Max(t, tmp, s.dev, smax, n, st));
+    FJ_CUDA(cudaFreeAsync(t, st));
+  }
+  k_scalars<<<1, 1, 0, st>>>(smin, smax, eps, o->sigma, o->c, S);
+  k_init<<<gridn(n), kBlock, 0, st>>>(n, L.perm, L.rp, s.dev, S, s_l, z);
+
+  KP p = make_kp(g, L);
+  p.s = s_l;
+  p.z = z;
+  p.sc = S;
+  p.omega = omega;
+  p.partial = partial;
+  p.arrive = arrive;
+  p.max_sweeps = o->max_sweeps;
+  p.ctr = ctl;
+  p.bar = ctl + 3;
+  p.cnt = cnt;
+  p.out = outv;
+  p.cert_max = certbits;
+
+  const void *fn = W ? (const void *)k_sweep<true> : (const void *)k_sweep<false>;
+  const int grid = persistent_grid(fn, g->num_sms);
+  float ms_sweep = 0, ms_cert = 0;
+  int rounds = 0;
+  stats.colors = L.ncolors;
+  for (;;) {
+    // a3–a5: persistent sweeps with on-device loop control
+    FJ_CUDA(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * 8, st));
+    FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(SweepCounters) * 3, st));
+    FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 8, st));
+    void *args[] = {&p};
+    FJ_CUDA(cudaEventRecord(es0, st));
+    FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, 0, st));
+    FJ_CUDA(cudaEventRecord(es1, st));
+    // fp64 compensated certificate over every non-empty row
+    if (o->certify) {
+      KP q = p;
+      q.ctr = ctl + 5;
+      FJ_CUDA(cudaEventRecord(ec0, st));
+      const void *cf = W ? (const void *)k_pass<CERT, true> : (const void *)k_pass<CERT, false>;
+      void *cargs[] = {&q};
+      FJ_CUDA(cudaLaunchKernel(cf, persistent_grid(cf, g->num_sms), kBlock, cargs, 0, st));
+      FJ_CUDA(cudaEventRecord(ec1, st));
+    }
+    unsigned long long h[8];
+    FJ_CUDA(cudaMemcpyAsync(h, outv, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FJ_CUDA(cudaStreamSynchronize(st));
+    float a = 0;
+    FJ_CUDA(cudaEventElapsedTime(&a, es0, es1));
+    ms_sweep += a;
+    if (o->certify) {
+      FJ_CUDA(cudaEventElapsedTime(&a, ec0, ec1));
+      ms_cert += a;
+    }
+    stats.sweeps += (int64_t)h[0];
+    stats.relaxations += (int64_t)h[1];
+    stats.edge_updates += (int64_t)h[2];
+    stats.reason = (int)h[3];
+    stats.cert_ratio = o->certify ? __builtin_bit_cast(double, h[4]) : 0.0;
+    if (stats.reason != 0) break;
+    if (!o->certify || stats.cert_ratio <= 1.0 || rounds >= o->cert_rounds) break;
+    rounds++;  // resume from ẑ (Lemma 3: ẑ fully determines r)
+  }
+  stats.cert_rounds = rounds;
+  stats.phases = stats.sweeps * L.ncolors;
+  stats.rows_read = stats.sweeps * L.active_rows;
+  stats.arcs_read = stats.sweeps * L.m;
+  stats.relaxations += L.empty_rows;  // rows solved exactly at init
+
+  // a6: unshift
+  k_finalize<<<gridn(n), kBlock, 0, st>>>(n, L.iperm, z, S, zdev ? z_out : zo,
+                                          o->zprime_out ? (zpdev ? o->zprime_out : zp) : nullptr);
+  if (!zdev) FJ_CUDA(cudaMemcpyAsync(z_out, zo, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+  if (o->zprime_out && !zpdev)
+    FJ_CUDA(cudaMemcpyAsync(o->zprime_out, zp, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  Scalars hs{};
+  FJ_CUDA(cudaMemcpyAsync(&hs, S, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaEventRecord(e1, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  float ms = 0;
+  FJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  stats.solve_ms = ms;
+  stats.sweep_ms = ms_sweep;
+  stats.cert_ms = ms_cert;
+  stats.c = hs.c;
+  stats.eps_prime = hs.eps_p;
+
+  cudaFreeAsync(s_l, st);
+  cudaFreeAsync(z, st);
+  cudaFreeAsync(smin, st);
+  cudaFreeAsync(S, st);
+  cudaFreeAsync(partial, st);
+  cudaFreeAsync(arrive, st);
+  cudaFreeAsync(ctl, st);
+  cudaFreeAsync(cnt, st);
+  cudaFreeAsync(outv, st);
+  if (zo) cudaFreeAsync(zo, st);
+  if (zp) cudaFreeAsync(zp, st);
+  if (s.owned) cudaFreeAsync(s.owned, st);
+  for (cudaEvent_t e : {e0, e1, es0, es1, ec0, ec1}) cudaEventDestroy(e);
+  FJ_CUDA(cudaGetLastError());
+
+  fj_status rc = FJ_OK;
+  if (hs.bad_input) {
+    set_error("fj_solve: s contains a non-finite value");
+    rc = FJ_ERR_INVALID;
+  } else if (stats.reason == 1) {
+    set_error("fj_solve: watchdog, %lld sweeps without convergence", (long long)stats.sweeps);
+    rc = FJ_ERR_NUMERIC;
+  } else if (stats.reason == 2) {
+    set_error("fj_solve: divergence sentinel |r| > 1e6 max|s'| (omega = %g)", omega);
+    rc = FJ_ERR_NUMERIC;
+  } else if (o->certify && !(stats.cert_ratio <= 1.0)) {
+    set_error("fj_solve: fp64 residual certificate failed (max |r|/h = %g)", stats.cert_ratio);
+    rc = FJ_ERR_NUMERIC;
+  }
+  stats.status = rc;
+  if (st_out) *st_out = stats;
+  return rc;
+}
+
+fj_status measures_impl(fj_graph *g, const float *z_in, const float *s_in, fj_measures_t *out) {
+  cudaStream_t st = g->stream;
+  const int64_t n = g->n;
+  const Layout &L = g->async_layout;
+  Staged z{}, s{};
+  FJ_TRY(stage_in(z_in, n, st, z));
+  if (s_in) FJ_TRY(stage_in(s_in, n, st, s));
+  double *zl = nullptr, *sums = nullptr;
+  unsigned *ctr = nullptr;
+  FJ_CUDA(cudaMallocAsync(&zl, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&sums, sizeof(double) * 5, st));
+  FJ_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * 5, st));
+  FJ_CUDA(cudaMallocAsync(&ctr, sizeof(unsigned), st));
+  FJ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), st));
+  k_meas_nodes1<<<gridn(n), kBlock, 0, st>>>(n, L.perm, z.dev, zl, sums);
+  k_meas_nodes2<<<gridn(n), kBlock, 0, st>>>(n, z.dev, s.dev, sums);
+  KP p = make_kp(g, L);
+  p.z = zl;
+  p.ctr = ctr;
+  p.dis = sums + 4;
+  const bool W = g->weighted != 0;
+  const void *fn = W ? (const void *)k_pass<DIS, true> : (const void *)k_pass<DIS, false>;
+  void *args[] = {&p};
+  FJ_CUDA(cudaLaunchKernel(fn, persistent_grid(fn, g->num_sms), kBlock, args, 0, st));
+  double h[5];
+  FJ_CUDA(cudaMemcpyAsync(h, sums, sizeof(h), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(zl, st);
+  cudaFreeAsync(sums, st);
+  cudaFreeAsync(ctr, st);
+  if (z.owned) cudaFreeAsync(z.owned, st);
+  if (s.owned) cudaFreeAsync(s.owned, st);
+  FJ_CUDA(cudaGetLastError());
+  out->polarization = h[1];
+  // each undirected edge is stored as two arcs (reading R14)
+  out->disagreement = g->directed ? h[4] : 0.5 * h[4];
+  out->internal_conflict = s_in ? h[2] : 0.0;
+  out->controversy = h[3];
+  return FJ_OK;
+}
+
+}  // namespace fj
+
+extern "C" {
+
+fj_status fj_solve_ex(fj_graph_t g, const float *s, double eps, double omega, const fj_opts *o,
+                      float *z_out, fj_stats *st) {
+  fj_opts d;
+  fj_opts_default(&d);
+  if (o) {
+    d = *o;
+    if (!(d.sigma > 0)) d.sigma = 1e-5;
+    if (d.max_sweeps <= 0) d.max_sweeps = 1000000;
+    if (d.cert_rounds < 0) d.cert_rounds = 3;
+  }
+  if (!g || !s || !z_out) {
+    fj::set_error("fj_solve: null argument");
+    return FJ_ERR_INVALID;
+  }
+  if (!(eps > 0.0 && eps < 1.0)) {
+    fj::set_error("fj_solve: eps must lie in (0, 1), got %g", eps);
+    return FJ_ERR_INVALID;
+  }
+  if (!(omega > 0.0 && omega < 2.0)) {
+    fj::set_error("fj_solve: omega must lie in (0, 2), got %g", omega);
+    return FJ_ERR_INVALID;
+  }
+  if (d.method < FJ_METHOD_AUTO || d.method > FJ_METHOD_PUSH) {
+    fj::set_error("fj_solve: unknown method %d", d.method);
+    return FJ_ERR_INVALID;
+  }
+  return fj::solve_impl(g, s, eps, omega, &d, z_out, st);
+}
+
+fj_status fj_solve(fj_graph_t g, const float *s, double eps, double omega, float *z_out) {
+  return fj_solve_ex(g, s, eps, omega, nullptr, z_out, nullptr);
+}
+
+fj_status fj_measures_ex(fj_graph_t g, const float *z, const float *s, fj_measures_t *out) {
+  if (!g || !z || !out) {
+    fj::set_error("fj_measures: null argument");
+    return FJ_ERR_INVALID;
+  }
+  return fj::measures_impl(g, z, s, out);
+}
+
+fj_status fj_measures(fj_graph_t g, const float *z, double *polarization, double *disagreement) {
+  if (!polarization || !disagreement) {
+    fj::set_error("fj_measures: null output");
+    return FJ_ERR_INVALID;
+  }
+  fj_measures_t m;
+  fj_status s = fj_measures_ex(g, z, nullptr, &m);
+  if (s != FJ_OK) return s;
+  *polarization = m.polarization;
+  *disagreement = m.disagreement;
+  return FJ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,297 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star):
+  * z: max_v |ẑ_v − z_or,v| / max(|z_or,v|, σ) ≤ 1e-4 against the oracle's
+    converged z at the same ε;
+  * ε guarantee, independently: the oracle's compensated fp64 certificate of
+    the GPU's ẑ' gives max |R_v|/h_v ≤ 1 ⇒ |ẑ − z| ≤ ε·max(|z|, σ);
+  * P and D: relative error ≤ 1e-5.
+"""
+import numpy as np
+import pytest
+
+import fjgen
+import oracle
+from oracle import closed_forms as cf
+from tests import graphs as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+fj = pytest.importorskip("paper_2507_14864_b200")
+
+SIG = oracle.SIGMA
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def _t(a, dev):
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def gpu_solve(dev, rp, col, w, s, eps, omega=1.0, directed=True, method="auto", host=False,
+              raise_on_numeric=True):
+    n = len(rp) - 1
+    if host:
+        g = fj.Graph(n, rp, col, w, directed=directed)
+        z = np.empty(n, np.float32)
+        zp = np.empty(n, np.float64)
+        st = fj.solve(g, np.ascontiguousarray(s, np.float32), z, eps, omega, method=method,
+                      zprime_out=zp, raise_on_numeric=raise_on_numeric)
+        return g, z.astype(np.float64), zp, st
+    g = fj.Graph(n, _t(rp, dev), _t(col, dev), _t(w, dev), directed=directed)
+    z = torch.empty(n, dtype=torch.float32, device=dev)
+    zp = torch.empty(n, dtype=torch.float64, device=dev)
+    st = fj.solve(g, _t(np.asarray(s, np.float32), dev), z, eps, omega, method=method,
+                  zprime_out=zp, raise_on_numeric=raise_on_numeric)
+    torch.cuda.synchronize()
+    return g, z.cpu().numpy().astype(np.float64), zp.cpu().numpy(), st
+
+
+def rel_err(z, ref):
+    return np.max(np.abs(z - ref) / np.maximum(np.abs(ref), SIG)) if len(z) else 0.0
+
+
+def check_parity(dev, rp, col, w, s, eps, omega, directed, method="auto", ref_omega=None):
+    g, z, zp, st = gpu_solve(dev, rp, col, w, s, eps, omega, directed, method)
+    assert st.status == 0 and st.cert_ratio <= 1.0, st
+    # independent certificate by the oracle's own routine
+    ratio, _ = oracle.certificate(rp, col, w, s, zp, eps)
+    assert ratio <= 1.0, ratio
+    # oracle z at the same ε (reading R11: ω = 1 reference for directed SOR)
+    ro = omega if ref_omega is None else ref_omega
+    ref = oracle.solve(rp, col, w, s, eps, ro)
+    assert ref.status == 0
+    assert rel_err(z, ref.z) <= 1e-4
+    # measures: GPU reduction on GPU z vs oracle measures of oracle z
+    m = fj.measures(g, torch.from_numpy(z.astype(np.float32)).to(dev))
+    om = oracle.measures(rp, col, w, ref.z, directed=directed)
+    for k in ("P", "D"):
+        assert abs(m[k] - om[k]) <= 1e-5 * abs(om[k]) + 1e-300, (k, m[k], om[k])
+    # reduction alone: same fp32 input on both sides
+    om2 = oracle.measures(rp, col, w, z.astype(np.float32).astype(np.float64), directed=directed)
+    for k in ("P", "D"):
+        assert abs(m[k] - om2[k]) <= 1e-9 * abs(om2[k]) + 1e-300
+    g.close()
+    return st, z, ref
+
+
+# ------------------------------------------------------------------ golden
+@pytest.mark.parametrize("host", [False, True])
+def test_golden_examples(dev, host):
+    import json, os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+    for ex in gold["examples"]:
+        if ex.get("directed"):
+            rp, col, w = G.in_csr_from_arcs(ex["n"], ex["arcs"])
+        else:
+            rp, col, w = G.in_csr_from_edges(ex["n"], ex["edges"])
+        s = np.array(ex["s"], np.float32)
+        for omega in (1.0, 1.5):
+            g, z, zp, st = gpu_solve(dev, rp, col, w, s, 1e-6, omega, ex.get("directed", False),
+                                     host=host)
+            zt = np.array(ex["z"])
+            assert np.all(np.abs(z - zt) <= 1e-6 * np.maximum(np.abs(zt), SIG) + 1e-7), ex["name"]
+            g.close()
+    m = gold["measures"][0]
+    rp, col, w = G.in_csr_from_edges(2, [(0, 1)])
+    g = fj.Graph(2, rp, col, None, directed=False)
+    out = fj.measures(g, np.array(m["z"], np.float32), np.array(m["s"], np.float32))
+    for k in "IDPC":
+        assert out[k] == pytest.approx(m[k], rel=1e-6)
+    P, D = fj.measures_pd(g, np.array(m["z"], np.float32))
+    assert P == pytest.approx(m["P"], rel=1e-6) and D == pytest.approx(m["D"], rel=1e-6)
+    g.close()
+
+
+# -------------------------------------------------------------- tiny suite
+TINY = {
+    "er2000": lambda: (*fjgen.er_graph(2000, 10.0, 11), None, fjgen.uniform(2000, 11), False),
+    "rmat12": lambda: (*fjgen.rmat_graph(12, 16, 12), None, fjgen.uniform(4096, 12), True),
+    "rmat12w": lambda: (lambda rp, col: (rp, col, fjgen.arc_weights(rp, col, 13),
+                                         fjgen.beta25(4096, 13), True))(*fjgen.rmat_graph(12, 16, 13)),
+    "chunglu4k": lambda: (lambda rp, col: (rp, col, None,
+                                           fjgen.zero_mask(fjgen.uniform(4096, 14, -1, 1), 2048, 14),
+                                           False))(*fjgen.chunglu_graph(4096, 2.1, 20, 14)),
+    "lattice64": lambda: (*fjgen.lattice_graph(64, 0.01, 15), None, fjgen.step_noise(64, 15), False),
+    "dirw-dense": lambda: (*G.random_directed(300, 0.05, 16, weighted=True),
+                           fjgen.uniform(300, 16), True),
+}
+
+
+@pytest.mark.parametrize("name", sorted(TINY))
+def test_tiny_async(dev, name):
+    rp, col, w, s, directed = TINY[name]()
+    check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed)
+
+
+@pytest.mark.parametrize("name", ["er2000", "chunglu4k", "lattice64"])
+@pytest.mark.parametrize("omega", [1.25, 1.5, 1.8])
+def test_tiny_colored_sor_undirected(dev, name, omega):
+    rp, col, w, s, directed = TINY[name]()
+    check_parity(dev, rp, col, w, s, 1e-6, omega, directed)
+
+
+@pytest.mark.parametrize("name", ["rmat12", "rmat12w", "dirw-dense"])
+@pytest.mark.parametrize("omega", [1.2, 1.4])
+def test_tiny_colored_sor_directed(dev, name, omega):
+    """Reading R11: directed SOR is compared with the oracle at ω = 1."""
+    rp, col, w, s, directed = TINY[name]()
+    check_parity(dev, rp, col, w, s, 1e-6, omega, directed, ref_omega=1.0)
+
+
+@pytest.mark.parametrize("omega", [1.0, 1.3])
+def test_async_vs_colored_methods(dev, omega):
+    rp, col, w, s, directed = TINY["er2000"]()
+    if omega == 1.0:
+        check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="colored")
+    else:
+        # ASYNC with ω > 1 is not guaranteed; if it converges it is certified
+        g, z, zp, st = gpu_solve(dev, rp, col, w, s, 1e-6, omega, directed, method="async",
+                                 raise_on_numeric=False)
+        if st.status == 0:
+            assert oracle.certificate(rp, col, w, s, zp, 1e-6)[0] <= 1.0
+        g.close()
+
+
+# ------------------------------------------------------------- edge cases
+def test_single_isolated_node(dev):
+    rp = np.array([0, 0], np.int64)
+    col = np.zeros(0, np.int32)
+    g, z, zp, st = gpu_solve(dev, rp, col, None, np.array([0.4], np.float32), 1e-6)
+    assert z[0] == pytest.approx(0.4, abs=1e-7) and st.sweeps == 1
+    g.close()
+
+
+def test_no_arcs_ragged(dev):
+    n = 1237
+    rp = np.zeros(n + 1, np.int64)
+    s = fjgen.uniform(n, 3)
+    g, z, _, st = gpu_solve(dev, rp, np.zeros(0, np.int32), None, s, 1e-6, 1.5)
+    np.testing.assert_allclose(z, s, atol=1e-7)
+    g.close()
+
+
+def test_constant_and_zero_opinions(dev):
+    rp, col, w, _, _ = TINY["lattice64"]()
+    n = len(rp) - 1
+    g, z, _, st = gpu_solve(dev, rp, col, w, np.full(n, 0.4, np.float32), 1e-6, 1.0, False)
+    assert np.all(np.abs(z - 0.4) <= 1e-6 * 0.4 + 1e-7)
+    g.close()
+    g, z, _, st = gpu_solve(dev, rp, col, w, np.zeros(n, np.float32), 1e-6, 1.0, False)
+    assert np.all(np.abs(z) <= 1e-6 * SIG + 1e-12)
+    g.close()
+
+
+@pytest.mark.parametrize("hub_deg", [300, 2048, 2049, 20000])
+def test_long_rows_star(dev, hub_deg):
+    """Hub rows above 256 arcs are split in 2048-arc pieces reduced across
+    CTAs (deterministic partials); the star has a closed form for the hub."""
+    n = hub_deg + 1
+    edges = [(0, i) for i in range(1, n)]
+    rp, col, w = G.in_csr_from_edges(n, edges)
+    s = fjgen.uniform(n, 5)
+    check_parity(dev, rp, col, w, s, 1e-6, 1.0, False)
+    check_parity(dev, rp, col, w, s, 1e-6, 1.5, False)
+
+
+def test_determinism_colored(dev):
+    """COLORED sweeps read only other colors' values: bit-reproducible."""
+    rp, col, w, s, directed = TINY["rmat12w"]()
+    a = gpu_solve(dev, rp, col, w, s, 1e-6, 1.2, directed, method="colored")
+    b = gpu_solve(dev, rp, col, w, s, 1e-6, 1.2, directed, method="colored")
+    assert np.array_equal(a[2], b[2])
+    a[0].close(); b[0].close()
+
+
+def test_invalid_inputs(dev):
+    def create(n, arcs, w=None, directed=True, rp=None, col=None):
+        if rp is None:
+            rp, col, _ = G.in_csr_from_arcs(n, arcs)
+        return fj.Graph(n, rp, col, w, directed=directed)
+    with pytest.raises(fj.FJError, match="self-loop"):
+        create(3, [(0, 0), (1, 2)])
+    rp = np.array([0, 2, 2], np.int64)
+    with pytest.raises(fj.FJError, match="duplicate"):
+        create(2, None, rp=rp, col=np.array([1, 1], np.int32))
+    with pytest.raises(fj.FJError, match="range"):
+        create(2, None, rp=rp, col=np.array([1, 5], np.int32))
+    with pytest.raises(fj.FJError, match="row_ptr"):
+        create(2, None, rp=np.array([0, 3, 2], np.int64), col=np.array([1, 0], np.int32))
+    with pytest.raises(fj.FJError, match="symmetric"):
+        create(3, [(0, 1), (1, 2), (2, 1)], directed=False)
+    rp, col, _ = G.in_csr_from_arcs(2, [(0, 1)])
+    with pytest.raises(fj.FJError, match="weight"):
+        fj.Graph(2, rp, col, np.array([-1.0], np.float32))
+    g = fj.Graph(2, rp, col, None)
+    z = np.empty(2, np.float32)
+    for eps, om in [(0.0, 1.0), (1.0, 1.0), (1e-3, 0.0), (1e-3, 2.0)]:
+        with pytest.raises(fj.FJError) as e:
+            fj.solve(g, np.ones(2, np.float32), z, eps, om)
+        assert e.value.status == fj.FJ_ERR_INVALID
+    with pytest.raises(fj.FJError) as e:
+        fj.solve(g, np.array([np.nan, 1], np.float32), z, 1e-3, 1.0)
+    assert e.value.status == fj.FJ_ERR_INVALID
+    g.close()
+
+
+def test_divergence_reported(dev):
+    """A directed graph where ω = 1.9 over-relaxation diverges must come back
+    as FJ_ERR_NUMERIC (sentinel), not as a wrong answer."""
+    rp, col, w, s, _ = TINY["rmat12w"]()
+    g, z, zp, st = gpu_solve(dev, rp, col, w, s, 1e-6, 1.95, True, raise_on_numeric=False)
+    if st.status == 0:
+        assert oracle.certificate(rp, col, w, s, zp, 1e-6)[0] <= 1.0
+    else:
+        assert st.status == fj.FJ_ERR_NUMERIC and st.reason in (1, 2)
+    g.close()
+
+
+def test_simple_abi_calls(dev):
+    rp, col, w, s, directed = TINY["er2000"]()
+    g = fj.Graph(2000, _t(rp, dev), _t(col, dev), None, directed=False)
+    z = torch.empty(2000, dtype=torch.float32, device=dev)
+    fj.solve_simple(g, _t(s, dev), z, 1e-6, 1.0)
+    ref = oracle.solve(rp, col, w, s, 1e-6, 1.0)
+    assert rel_err(z.cpu().numpy().astype(np.float64), ref.z) <= 1e-4
+    P, D = fj.measures_pd(g, z)
+    om = oracle.measures(rp, col, w, ref.z, directed=False)
+    assert P == pytest.approx(om["P"], rel=1e-5) and D == pytest.approx(om["D"], rel=1e-5)
+    g.close()
+
+
+# ------------------------------------------------- full-size closed forms
+def test_full_lattice_eigenmode(dev):
+    """Config 5's 4096² grid (no shortcuts) with a cosine eigenmode opinion
+    vector: the exact z is known at full size (oracle/closed_forms.py)."""
+    N = 4096
+    rp, col = fjgen.lattice_graph(N, 0.0, 0)
+    s, zt = cf.grid_mode(N, 3, 5)
+    s32 = s.astype(np.float32)
+    # closed form of the fp32-rounded input: z(s32) = z(s) + (I+L)^{-1}(s32 − s),
+    # and |(I+L)^{-1}(s32 − s)| ≤ max|s32 − s| (row-stochastic)
+    slack = np.max(np.abs(s32 - s))
+    eps = 1e-6
+    g, z, zp, st = gpu_solve(dev, rp, col, None, s32, eps, 1.0, False)
+    assert np.all(np.abs(z - zt) <= eps * np.abs(zt) + slack + 6e-8 * np.abs(zt))
+    g.close()
+
+
+def test_full_lattice_step_1d(dev):
+    """Noise-free step on the 4096² grid reduces to the 1-D tridiagonal
+    system (I + L_path) g = f (oracle/closed_forms.py)."""
+    N = 4096
+    rp, col = fjgen.lattice_graph(N, 0.0, 0)
+    f = (np.arange(N) < N // 2).astype(np.float64)
+    zt = cf.grid_rows_constant(N, f)
+    eps = 1e-6
+    for omega in (1.0, 1.25):
+        g, z, zp, st = gpu_solve(dev, rp, col, None, np.tile(f, N).astype(np.float32), eps,
+                                 omega, False)
+        assert np.all(np.abs(z - zt) <= eps * np.maximum(np.abs(zt), SIG) + 6e-8 * np.abs(zt))
+        g.close()
