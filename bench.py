@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the FJ hot path on B200 (BASELINE.json metric: edge-updates/s
+and time-to-ε on R-MAT-24, achieved HBM GB/s vs peak).
+
+One STEP = one pass of every §8(a) row over the config-4 workload (directed
+weighted R-MAT-24, s ~ Beta(2,5), ε = 1e-6) with inputs resident in HBM:
+fj_graph_create (a1) → fj_solve_ex (a2–a6) → fj_measures (a7) → destroy.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--omega 1.0] [--impl reference]
+
+N > 1 (torchrun): independent replicas, one per GPU ("replicas only", the
+path has no exchange step).  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "edge-updates/s (time-to-eps on R-MAT-24; achieved HBM GB/s vs peak)"
+UNIT = "edge-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--shrink", type=int, default=0, help="smaller size of the same recipe (dev only)")
+    ap.add_argument("--omega", type=float, default=1.0)
+    ap.add_argument("--method", default="auto")
+    ap.add_argument("--eps", type=float, default=1e-6)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--out", default=None, help="also write the JSON line here")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > i + 2 and r[i + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    return world, rank, local
+
+
+def config_dict(prob, args, extra=None):
+    d = {"workload": f"config{args.config}:{prob.name}", "n": prob.n, "m": prob.m,
+         "eps": args.eps, "omega": args.omega, "directed": prob.directed,
+         "weighted": prob.w is not None, "opinions": prob.meta.get("kind"),
+         "seed": prob.meta.get("seed"),
+         "l2": "inputs larger than L2 (CSR > 126 MB), no flush needed",
+         "parallelism": "replicas" if args.gpus > 1 else "single-gpu"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, prob, world, rank):
+    """The oracle (fp64 FIFO ImprovedBLI, single thread) timed on the host
+    cores, each step a bounded sample of the config-4 workload: the first
+    `pushes` pops of Alg. 2+1 on the full graph."""
+    import oracle
+    if rank != 0:
+        return None
+    total = args.steps + args.warmup
+    budget_s = max(2.0, min(15.0, 150.0 / max(1, total)))
+    # calibrate pushes/second on a short bounded run
+    cal = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0, max_pushes=200_000)
+    rate = cal.pushes / max(cal.seconds, 1e-6)
+    pushes = int(rate * budget_s)
+    times, eus = [], []
+    for i in range(total):
+        r = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0, max_pushes=pushes)
+        if i >= args.warmup:
+            times.append(r.seconds)
+            eus.append(r.touched)
+    v = sum(eus) / sum(times)
+    sample = (f"first {pushes} pops of ImprovedBLI (Alg. 2+1, FIFO, fp64) on the full "
+              f"{prob.name} graph (n={prob.n}, m={prob.m}); ~{budget_s:.0f} s per step")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (fjgen seeded R-MAT-24, Beta(2,5) opinions)",
+            "config": config_dict(prob, args, {"omega": 1.0}),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+def cpu_baseline(prob, args):
+    import oracle
+    cal = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0, max_pushes=200_000)
+    rate = cal.pushes / max(cal.seconds, 1e-6)
+    pushes = int(rate * 15.0)
+    r = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0, max_pushes=pushes)
+    return {"value": r.touched / r.seconds, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {r.pushes} pops ({r.touched} edge updates, {r.seconds:.1f} s) of "
+                      f"ImprovedBLI (Alg. 2+1, FIFO, fp64) on the full {prob.name} graph"}
+
+
+# ----------------------------------------------------------------- our arm
+def algorithmic_bytes(st, weighted: bool):
+    """Bytes the sweep kernel must move: per arc read col (4)
+    + w (4, weighted); per evaluated row rp (8) + s (4) + ẑ (8) + 1+d (8,
+    weighted); per relaxation an 8-byte ẑ write.  ẑ gathers are not counted
+    (L2-resident), which makes `achieved` a lower bound."""
+    per_arc = 8 if weighted else 4
+    per_row = 28 if weighted else 20
+    swept_relax = st.relaxations  # includes init-solved empty rows (no bytes in the sweep)
+    return st.arcs_read * per_arc + st.rows_read * per_row + 8 * swept_relax
+
+
+def run_ours(args, prob, world, rank, local):
+    import torch
+
+    import paper_2507_14864_b200 as fj
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    rp = torch.from_numpy(prob.row_ptr).to(dev)
+    col = torch.from_numpy(prob.col).to(dev)
+    w = None if prob.w is None else torch.from_numpy(prob.w).to(dev)
+    s = torch.from_numpy(prob.s).to(dev)
+    z = torch.empty(prob.n, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        g = fj.Graph(prob.n, rp, col, w, directed=prob.directed)
+        st = fj.solve(g, s, z, args.eps, args.omega, method=args.method)
+        m = fj.measures(g, z)
+        g.close()
+        return st, m
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    launches0 = fj.lib().fj_kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            stats.append(step())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = fj.lib().fj_kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    eu_rank = sum(st.edge_updates for st, _ in stats)
+    value = eu_rank * world / (ms / 1e3)
+    st0, m0 = stats[-1]
+    solve_ms = statistics.median(st.solve_ms for st, _ in stats)
+    sweep_ms = statistics.median(st.sweep_ms for st, _ in stats)
+
+    # roofline of the dominant kernel (k_sweep), CUDA events on the graph stream
+    pk = peaks()
+    peak = pk["hbm_gbs"] if pk else 6650.0
+    ab = algorithmic_bytes(st0, prob.w is not None)
+    achieved = ab / (st0.sweep_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_sweep_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, prob, fj, torch, dev, stream, world)
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (fjgen seeded R-MAT-24 weights U(0,1], Beta(2,5) opinions)",
+            "config": config_dict(prob, args, {"method": args.method}),
+            "time_to_eps_s": solve_ms / 1e3,
+            "sweep_kernel_ms": sweep_ms,
+            "step_breakdown": {"solve_ms": solve_ms, "sweeps": st0.sweeps,
+                               "relaxations": st0.relaxations, "edge_updates": st0.edge_updates,
+                               "cert_ratio": st0.cert_ratio, "colors": st0.colors,
+                               "polarization": m0["P"], "disagreement": m0["D"]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
+                         "kernel": "k_sweep (persistent)",
+                         "algorithmic_bytes_per_launch": ab},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "e2e": e2e}
+    return line
+
+
+def run_e2e(args, prob, fj, torch, dev, stream, world):
+    """Same metric through the C-ABI with HOST buffers: the H2D copy of the
+    step's inputs (pinned) and the D2H read of z and the measures are inside
+    the timed region (the library stages host pointers itself)."""
+    rp = torch.from_numpy(prob.row_ptr).pin_memory()
+    col = torch.from_numpy(prob.col).pin_memory()
+    w = None if prob.w is None else torch.from_numpy(prob.w).pin_memory()
+    s = torch.from_numpy(prob.s).pin_memory()
+    z = torch.empty(prob.n, dtype=torch.float32).pin_memory()
+    sptr = ctypes_stream(stream)
+
+    def step():
+        g = fj.Graph(prob.n, rp, col, w, directed=prob.directed, stream=sptr)
+        st = fj.solve(g, s, z, args.eps, args.omega, method=args.method)
+        fj.measures(g, z)
+        g.close()
+        return st
+
+    step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eu = 0
+    k = max(1, min(args.steps, 3))
+    for _ in range(k):
+        eu += step().edge_updates
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    h2d = prob.row_ptr.nbytes + prob.col.nbytes + (0 if prob.w is None else prob.w.nbytes) + \
+        prob.s.nbytes
+    d2h = 4 * prob.n + 32
+    return {"value": eu * world / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": k,
+            "note": "wall clock around blocking C-ABI calls with pinned host buffers"}
+
+
+def ctypes_stream(stream):
+    import ctypes
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    import fjgen
+    prob = fjgen.config(args.config, shrink=args.shrink)
+    if args.impl == "reference":
+        line = run_reference(args, prob, world, rank)
+    else:
+        line = run_ours(args, prob, world, rank, local)
+        if rank == 0 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(prob, args)
+    if rank == 0 and line is not None:
+        txt = json.dumps(line)
+        print(txt, flush=True)
+        if args.out:
+            with open(args.out, "w") as f:
+                f.write(txt + "\n")
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

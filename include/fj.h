@@ -162,6 +162,11 @@ const char *fj_last_error(void);
 
 int fj_abi_version(void);
 
+/* Number of kernels this library has launched in this process (its own
+   kernels; the CUB sort/scan/reduce primitives used by graph build and the
+   opinion min/max are not counted).  Diagnostics for benchmarks. */
+int64_t fj_kernel_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

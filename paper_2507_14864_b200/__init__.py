@@ -24,7 +24,7 @@ METHODS = {"auto": 0, "async": 1, "colored": 2, "push": 3}
 #: every symbol include/fj.h declares
 EXPORTS = ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve", "fj_solve_ex",
            "fj_measures", "fj_measures_ex", "fj_opts_default", "fj_last_error",
-           "fj_abi_version")
+           "fj_abi_version", "fj_kernel_launches")
 
 
 class FJError(RuntimeError):
@@ -80,6 +80,7 @@ def lib():
         L.fj_opts_default.argtypes = [ctypes.POINTER(_Opts)]
         L.fj_opts_default.restype = None
         L.fj_last_error.restype = ctypes.c_char_p
+        L.fj_kernel_launches.restype = ctypes.c_int64
         for f in ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve",
                   "fj_solve_ex", "fj_measures", "fj_measures_ex"):
             getattr(L, f).restype = i

@@ -1,5 +1,7 @@
 // api.cu — error state, pointer classification, small C-ABI entry points.
 #include <stdarg.h>
+
+#include <atomic>
 #include <stdio.h>
 
 #include "fj_internal.cuh"
@@ -7,6 +9,9 @@
 namespace fj {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char *fmt, ...) {
   va_list ap;
@@ -33,15 +38,21 @@ void Layout::release() {
   cudaFree(w);
   cudaFree(d1);
   cudaFree(tasks);
+  cudaFree(wtasks);
   cudaFree(d_phase_begin);
+  cudaFree(d_wphase_begin);
   perm = iperm = nullptr;
   rp = nullptr;
   col = nullptr;
   w = nullptr;
   d1 = nullptr;
   tasks = nullptr;
+  wtasks = nullptr;
   d_phase_begin = nullptr;
+  d_wphase_begin = nullptr;
   ntasks = 0;
+  nwtasks = 0;
+  wphase_begin.clear();
   ncolors = 0;
   phase_begin.clear();
 }
@@ -53,6 +64,8 @@ extern "C" {
 const char *fj_last_error(void) { return fj::g_err; }
 
 int fj_abi_version(void) { return FJ_ABI_VERSION; }
+
+int64_t fj_kernel_launches(void) { return (int64_t)fj::g_launches.load(); }
 
 void fj_opts_default(fj_opts *o) {
   if (!o) return;
@@ -76,7 +89,7 @@ fj_status fj_graph_get_info(fj_graph_t g, fj_graph_info *info) {
   info->weighted = g->weighted;
   info->max_out_degree = g->async_layout.max_len;
   info->empty_rows = g->async_layout.empty_rows;
-  info->tasks = g->async_layout.ntasks;
+  info->tasks = g->async_layout.ntasks + g->async_layout.nwtasks;
   info->colors = g->ncolors;
   info->num_sms = g->num_sms;
   return FJ_OK;

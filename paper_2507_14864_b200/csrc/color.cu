@@ -96,6 +96,7 @@ fj_status build_coloring(fj_graph *g) {
   int rounds = 0;
   while (left > 0) {
     FJ_CUDA(cudaMemsetAsync(rem, 0, sizeof(unsigned long long), st));
+    fj::count_launch();
     k_jp_round<<<(unsigned)blocks, kBlock, 0, st>>>(n, g->in_rp, g->in_col, ort, ocol, c0, c1, rem,
                                                     maxc);
     FJ_CUDA(cudaMemcpyAsync(c0, c1, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));

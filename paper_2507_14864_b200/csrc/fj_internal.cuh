@@ -28,26 +28,33 @@ void set_error(const char *fmt, ...);
   } while (0)
 
 constexpr int kBlock = 256;           // threads per CTA of every task kernel
-constexpr int kPiece = 2048;          // arcs per piece of a long row (8 per thread)
+constexpr int kWarpPiece = 2048;      // arcs of one warp unit (whole row or piece)
+constexpr int kTileArcs = 2048;       // max arcs of one CTA tile task (smem products)
 constexpr int kNumClasses = 8;        // row-length classes of the layout
 
 // Row-length classes (out-degree L of the pull CSR).  Rows with L == 0 are
 // solved exactly at init (z_v = s_v, Eq. (1) with d_v = 0) and never enter a
-// sweep.  class k < 6 uses G = 1 << k lanes per row:
+// sweep.  Classes 0..5 are CTA "tile" tasks with G = 1 << k lanes per row:
 //   class 0: L in [1,4]   G = 1        class 3: L in (16,32]   G = 8
 //   class 1: L in (4,8]   G = 2        class 4: L in (32,64]   G = 16
 //   class 2: L in (8,16]  G = 4        class 5: L in (64,256]  G = 32
-//   class 6: L > 256      long row, split in pieces of kPiece arcs
+// Classes 6 and 7 are warp units (one warp, no block barrier):
+//   class 6: L in (256, kWarpPiece]  one warp per row
+//   class 7: L > kWarpPiece          pieces of kWarpPiece arcs, one warp each,
+//                                    combined by the last-arriving warp
 enum TaskKind : int32_t {
-  kG1 = 0, kG2 = 1, kG4 = 2, kG8 = 3, kG16 = 4, kG32 = 5,  // GROUP, G = 1 << kind
-  kLong = 7                                                   // one piece of a long row
+  kG1 = 0, kG2 = 1, kG4 = 2, kG8 = 3, kG16 = 4, kG32 = 5,  // CTA tile, G = 1 << kind
+  kWarp = 6                                                   // warp unit
 };
 
-// One unit of sweep work.  GROUP: rows [a, b) with G = 1 << (kind & 0xff).
-// LONG: row a, piece b of npieces = kind >> 8; slot = first partial slot of
-// the row (also its arrival counter index).
-struct Task {
+// One unit of sweep work.  Tile (kind 0..5): rows [a, b) with
+// G = 1 << kind lanes per row, one group per row (b - a <= kBlock / G).
+// Warp unit (kind & 0xff == kWarp): row a, piece b of npieces = kind >> 8;
+// slot = first partial slot of the row (also its arrival counter index).
+// [a0, a1) is the unit's arc range in the layout CSR.
+struct alignas(16) Task {
   int32_t a, b, kind, slot;
+  int64_t a0, a1;
 };
 
 // Sweep layout: the pull CSR (row u lists v with a_uv) with rows permuted to
@@ -61,10 +68,14 @@ struct Layout {
   int32_t *col = nullptr;    // [m]
   float *w = nullptr;        // [m] or null
   double *d1 = nullptr;      // 1 + d_u (weighted graphs only) [n]
-  Task *tasks = nullptr;
+  Task *tasks = nullptr;          // CTA tile tasks, grouped by phase (color)
   int ntasks = 0;
-  std::vector<int> phase_begin;   // host, ncolors + 1 entries
-  int *d_phase_begin = nullptr;   // device copy
+  Task *wtasks = nullptr;         // warp units, grouped by phase
+  int nwtasks = 0;
+  std::vector<int> phase_begin;   // host, ncolors + 1 entries (tile tasks)
+  std::vector<int> wphase_begin;  // host, ncolors + 1 entries (warp units)
+  int *d_phase_begin = nullptr;   // device copies
+  int *d_wphase_begin = nullptr;
   int npartials = 0;              // partial slots for long rows
   int64_t empty_rows = 0;
   int64_t active_rows = 0;        // rows with L > 0
@@ -102,4 +113,6 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
 fj_status build_coloring(fj_graph *g);
 // memory helpers (api.cu)
 bool is_device_ptr(const void *p);
+// every kernel launch issued by this library is counted (fj_kernel_launches)
+void count_launch();
 }  // namespace fj

@@ -169,14 +169,18 @@ fj_status transpose_in_csr(fj_graph *g, int64_t **ort, int32_t **ocol, float **o
   FJ_CUDA(cudaMalloc(ocol, sizeof(int32_t) * (m + 1)));
   *ow = nullptr;
   if (g->in_w) FJ_CUDA(cudaMalloc(ow, sizeof(float) * (m + 1)));
+  fj::count_launch();
   k_out_keys<<<grid_for(n * 32), kBlock, 0, st>>>(n, g->in_rp, g->in_col, nb, k0, cnt);
+  fj::count_launch();
   k_iota_u32<<<grid_for(m), kBlock, 0, st>>>(m, i0);
   FJ_TRY(sort_pairs(k0, k1, i0, i1, m, 2 * nb, st));
   int *err = nullptr;
   FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
   FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-  if (m > 0)
+  if (m > 0) {
+    fj::count_launch();
     k_unpack_sorted<<<grid_for(m), kBlock, 0, st>>>(m, nb, k0, i0, g->in_w, *ocol, *ow, err);
+  }
   FJ_TRY(exclusive_scan_i64(cnt, *ort, n + 1, st));
   FJ_CUDA(cudaFreeAsync(err, st));
   FJ_CUDA(cudaFreeAsync(k0, st));
@@ -219,6 +223,7 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
   int *err = nullptr;
   FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
   FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  fj::count_launch();
   k_validate_rowptr<<<grid_for(n + 1), kBlock, 0, st>>>(n, m, g->in_rp, err);
   int herr = 0;
   FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -238,11 +243,15 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
   FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint64_t) * (m + 1), st));
   FJ_CUDA(cudaMallocAsync(&i0, sizeof(uint32_t) * (m + 1), st));
   FJ_CUDA(cudaMallocAsync(&i1, sizeof(uint32_t) * (m + 1), st));
+  fj::count_launch();
   k_in_keys<<<grid_for(n * 32), kBlock, 0, st>>>(n, g->in_rp, col_raw, w_raw, nb, k0, err);
+  fj::count_launch();
   k_iota_u32<<<grid_for(m), kBlock, 0, st>>>(m, i0);
   FJ_TRY(sort_pairs(k0, k1, i0, i1, m, 2 * nb, st));
-  if (m > 0)
+  if (m > 0) {
+    fj::count_launch();
     k_unpack_sorted<<<grid_for(m), kBlock, 0, st>>>(m, nb, k0, i0, w_raw, g->in_col, g->in_w, err);
+  }
   FJ_CUDA(cudaFreeAsync(k0, st));
   FJ_CUDA(cudaFreeAsync(k1, st));
   FJ_CUDA(cudaFreeAsync(i0, st));
@@ -267,13 +276,19 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
   float *ow = nullptr;
   FJ_TRY(transpose_in_csr(g, &ort, &ocol, &ow));
   FJ_CUDA(cudaMalloc(&g->deg, sizeof(double) * n));
+  fj::count_launch();
   k_row_sums<<<grid_for(n * 32), kBlock, 0, st>>>(n, ort, ow, g->deg);
 
   // 5. symmetry of undirected input
   if (!g->directed && m > 0) {
+    fj::count_launch();
     k_neq<int64_t><<<grid_for(n + 1), kBlock, 0, st>>>(n + 1, ort, g->in_rp, err, 32);
+    fj::count_launch();
     k_neq<int32_t><<<grid_for(m), kBlock, 0, st>>>(m, ocol, g->in_col, err, 32);
-    if (ow) k_neq<float><<<grid_for(m), kBlock, 0, st>>>(m, ow, g->in_w, err, 32);
+    if (ow) {
+      fj::count_launch();
+      k_neq<float><<<grid_for(m), kBlock, 0, st>>>(m, ow, g->in_w, err, 32);
+    }
     FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
     FJ_CUDA(cudaStreamSynchronize(st));
     if (herr) {

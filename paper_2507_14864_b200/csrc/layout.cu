@@ -6,6 +6,9 @@
 // Permuted ids make the per-row state (s, ẑ, 1+d) streams coalesced; within
 // one class the original id order is kept (stable), so R-MAT hubs (low ids)
 // and lattice neighbours stay close in memory.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
 #include <cub/cub.cuh>
 
@@ -13,8 +16,7 @@
 
 namespace fj {
 
-static constexpr int kRowsPerGroupPerTask = 4;
-static constexpr int kClasses = 7;  // 0..5 GROUP (G = 1<<k), 6 long
+static constexpr int kClasses = kNumClasses;  // 0..5 tile (G = 1<<k), 6 warp row, 7 warp pieces
 
 __host__ __device__ static inline int row_class(int64_t L) {
   if (L <= 4) return 0;
@@ -23,7 +25,8 @@ __host__ __device__ static inline int row_class(int64_t L) {
   if (L <= 32) return 3;
   if (L <= 64) return 4;
   if (L <= 256) return 5;
-  return 6;
+  if (L <= kWarpPiece) return 6;
+  return 7;
 }
 
 static unsigned gridn(int64_t work) {
@@ -80,6 +83,21 @@ __global__ void k_copy_rows(int64_t n, const int32_t *__restrict__ perm,
   }
 }
 
+// arc range of every task (needs the device row pointers)
+__global__ void k_task_arcs(int ntasks, const int64_t *__restrict__ rp, Task *__restrict__ tasks) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntasks) return;
+  Task t = tasks[i];
+  if ((t.kind & 0xff) == kWarp) {
+    t.a0 = rp[t.a] + (int64_t)t.b * kWarpPiece;
+    t.a1 = min(rp[t.a + 1], t.a0 + (int64_t)kWarpPiece);
+  } else {
+    t.a0 = rp[t.a];
+    t.a1 = rp[t.b];
+  }
+  tasks[i] = t;
+}
+
 fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *ocol,
                                 const float *ow, const int32_t *color, int ncolors, Layout *L) {
   cudaStream_t st = g->stream;
@@ -99,6 +117,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   FJ_CUDA(cudaMemsetAsync(gcount, 0, sizeof(unsigned long long) * ngroups, st));
   FJ_CUDA(cudaMallocAsync(&len, sizeof(int64_t) * (n + 1), st));
   FJ_CUDA(cudaMemsetAsync(len + n, 0, sizeof(int64_t), st));
+  fj::count_launch();
   k_layout_keys<<<gridn(n), kBlock, 0, st>>>(n, ort, color, ncolors, k0, gcount);
 
   int gbits = 1;
@@ -119,6 +138,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   FJ_CUDA(cudaMalloc(&L->col, sizeof(int32_t) * (m + 1)));
   if (ow) FJ_CUDA(cudaMalloc(&L->w, sizeof(float) * (m + 1)));
   if (g->weighted) FJ_CUDA(cudaMalloc(&L->d1, sizeof(double) * n));
+  fj::count_launch();
   k_perm<<<gridn(n), kBlock, 0, st>>>(n, k0, ort, L->perm, L->iperm, len);
   {
     size_t tmp = 0;
@@ -128,6 +148,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     FJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, len, L->rp, n + 1, st));
     FJ_CUDA(cudaFreeAsync(t, st));
   }
+  fj::count_launch();
   k_copy_rows<<<gridn(n * 32), kBlock, 0, st>>>(n, L->perm, L->iperm, ort, ocol, ow, g->deg, L->rp,
                                                 L->col, L->w, L->d1);
 
@@ -155,45 +176,74 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   L->empty_rows = (int64_t)hcount[ngroups - 1];
   L->active_rows = n - L->empty_rows;
 
-  // lengths of long rows (class 6) for piece counts
-  std::vector<Task> tasks;
+  // work lists: tile tasks (classes 0..5) and warp units (classes 6, 7), each
+  // grouped by color; within a color, longest rows first
+  std::vector<Task> tasks, wtasks;
   L->phase_begin.assign(ncolors + 1, 0);
+  L->wphase_begin.assign(ncolors + 1, 0);
   int slot = 0;
   for (int c = 0; c < ncolors; c++) {
     L->phase_begin[c] = (int)tasks.size();
-    for (int cd = 0; cd < kClasses; cd++) {  // cd = 6 - class: long rows first
+    L->wphase_begin[c] = (int)wtasks.size();
+    for (int cd = 0; cd < kClasses; cd++) {  // cd = 7 - class
       int q = c * kClasses + cd;
       int cls = kClasses - 1 - cd;
       int64_t r0 = gstart[q], r1 = gstart[q + 1];
       if (r1 <= r0) continue;
-      if (cls == 6) {
+      if (cls == 7) {
         std::vector<int64_t> rph(r1 - r0 + 1);
         FJ_CUDA(cudaMemcpy(rph.data(), L->rp + r0, sizeof(int64_t) * (r1 - r0 + 1),
                            cudaMemcpyDeviceToHost));
         for (int64_t i = r0; i < r1; i++) {
           int64_t len_i = rph[i - r0 + 1] - rph[i - r0];
-          int np = (int)((len_i + kPiece - 1) / kPiece);
+          int np = (int)((len_i + kWarpPiece - 1) / kWarpPiece);
           for (int p = 0; p < np; p++)
-            tasks.push_back(Task{(int32_t)i, p, kLong | (np << 8), slot});
+            wtasks.push_back(Task{(int32_t)i, p, kWarp | (np << 8), slot, 0, 0});
           slot += np;
         }
+      } else if (cls == 6) {
+        for (int64_t i = r0; i < r1; i++)
+          wtasks.push_back(Task{(int32_t)i, 0, kWarp | (1 << 8), 0, 0, 0});
       } else {
         int G = 1 << cls;
-        int64_t per = (int64_t)(kBlock / G) * kRowsPerGroupPerTask;
+        int64_t per = kBlock / G;  // one G-lane group per row
         for (int64_t a = r0; a < r1; a += per)
-          tasks.push_back(Task{(int32_t)a, (int32_t)std::min(r1, a + per), cls, 0});
+          tasks.push_back(Task{(int32_t)a, (int32_t)std::min(r1, a + per), cls, 0, 0, 0});
       }
     }
   }
   L->phase_begin[ncolors] = (int)tasks.size();
+  L->wphase_begin[ncolors] = (int)wtasks.size();
+  if (getenv("FJ_DEBUG")) {  // per-color layout summary (diagnostics)
+    std::vector<int64_t> cut(ncolors + 1);
+    for (int c = 0; c <= ncolors; c++) cut[c] = gstart[c * kClasses];
+    std::vector<int64_t> arc(ncolors + 1);
+    for (int c = 0; c <= ncolors; c++)
+      FJ_CUDA(cudaMemcpy(&arc[c], L->rp + cut[c], sizeof(int64_t), cudaMemcpyDeviceToHost));
+    for (int c = 0; c < ncolors; c++)
+      fprintf(stderr, "fj layout color %d rows %lld arcs %lld tiles %d warp_units %d\n", c,
+              (long long)(cut[c + 1] - cut[c]), (long long)(arc[c + 1] - arc[c]),
+              L->phase_begin[c + 1] - L->phase_begin[c], L->wphase_begin[c + 1] - L->wphase_begin[c]);
+  }
   L->ntasks = (int)tasks.size();
+  L->nwtasks = (int)wtasks.size();
   L->npartials = slot;
   L->max_len = hmax;
-  FJ_CUDA(cudaMalloc(&L->tasks, sizeof(Task) * std::max<size_t>(1, tasks.size())));
-  if (!tasks.empty())
-    FJ_CUDA(cudaMemcpy(L->tasks, tasks.data(), sizeof(Task) * tasks.size(), cudaMemcpyHostToDevice));
+  for (int which = 0; which < 2; which++) {
+    std::vector<Task> &v = which ? wtasks : tasks;
+    Task **dst = which ? &L->wtasks : &L->tasks;
+    FJ_CUDA(cudaMalloc(dst, sizeof(Task) * std::max<size_t>(1, v.size())));
+    if (!v.empty()) {
+      FJ_CUDA(cudaMemcpy(*dst, v.data(), sizeof(Task) * v.size(), cudaMemcpyHostToDevice));
+      fj::count_launch();
+      k_task_arcs<<<gridn((int64_t)v.size()), kBlock, 0, st>>>((int)v.size(), L->rp, *dst);
+    }
+  }
   FJ_CUDA(cudaMalloc(&L->d_phase_begin, sizeof(int) * (ncolors + 1)));
   FJ_CUDA(cudaMemcpy(L->d_phase_begin, L->phase_begin.data(), sizeof(int) * (ncolors + 1),
+                     cudaMemcpyHostToDevice));
+  FJ_CUDA(cudaMalloc(&L->d_wphase_begin, sizeof(int) * (ncolors + 1)));
+  FJ_CUDA(cudaMemcpy(L->d_wphase_begin, L->wphase_begin.data(), sizeof(int) * (ncolors + 1),
                      cudaMemcpyHostToDevice));
   FJ_CUDA(cudaFreeAsync(k0, st));
   FJ_CUDA(cudaFreeAsync(k1, st));

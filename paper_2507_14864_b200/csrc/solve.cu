@@ -18,6 +18,7 @@
 // then evaluated on the final ẑ and is ≤ h — the paper's "Q = ∅".
 // A separate compensated fp64 pass (certificate) re-checks max |r_v|/h_v.
 #include <cuda/atomic>
+#include <type_traits>
 #include <cub/cub.cuh>
 
 #include "fj_internal.cuh"
@@ -48,15 +49,19 @@ struct KP {
   const float *__restrict__ w;
   const double *__restrict__ d1;
   const Task *__restrict__ tasks;
+  const Task *__restrict__ wtasks;
   const float *__restrict__ s;  // layout order
   double *z;                    // ẑ' (RELAX/CERT) or z (DIS), layout order
   const Scalars *sc;
   double omega;
+  double theta;  // sweep relaxes |r| > θ·h: θ = 1 first, < 1 on certificate resumes
   double2 *partial;
   int *arrive;
   const int *phase_begin;
+  const int *wphase_begin;
   int ncolors;
   int ntasks_all;
+  int nwtasks_all;
   int max_sweeps;
   unsigned *ctr;          // [3]
   SweepCounters *cnt;     // [3]
@@ -65,6 +70,25 @@ struct KP {
   unsigned long long *cert_max;  // double bits
   double *dis;
 };
+
+// CSR streams are read once per sweep: read-only path, no L1 allocation, so
+// L1 keeps the gathered ẑ values (hub rows are hit by many arcs)
+__device__ __forceinline__ int ld_stream(const int *q) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(q));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float *q) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(q));
+  return v;
+}
+// ẑ gathers: L1-cached.  ẑ is written during the sweep kernel, so an SM may
+// read a value another SM has since replaced; asynchronous relaxation allows
+// that (Lemma 3 holds for any order).  Every grid barrier executes a
+// gpu-scope fence, which invalidates L1, so the certifying zero-update sweep
+// and every color phase read current values.
+__device__ __forceinline__ double ld_z(const double *q) { return __ldca(q); }
 
 struct dd {
   double hi, lo;
@@ -119,16 +143,25 @@ __device__ __forceinline__ double threshold(const Scalars &S, double sp) {
   return S.floored ? S.heps * fmax(S.hs * sp, S.sigma) : S.hs * sp;
 }
 
+// residual r_i = s'_i − (1+d_i) ẑ_i + Σ_j a_ij ẑ_j combined in double-double:
+// at hub rows (d ~ 1e4–1e5) the two large terms cancel to ~h ≈ 5e-12, below
+// the rounding noise of a plain fp64 combination
+__device__ __forceinline__ double residual_dd(dd sum, double sp, double d1, double zi) {
+  dd_add(sum, sp);
+  dd_addprod(sum, -d1, zi);
+  return sum.hi + sum.lo;
+}
+
 template <bool W>
 __device__ __forceinline__ void relax_row(const KP &p, const Scalars &S, int row, int len,
-                                          double total, TAcc &t) {
+                                          dd total, TAcc &t) {
   const double sp = (double)p.s[row] + S.c;              // s' = s + c
   const double h = threshold(S, sp);
   const double zi = __ldcg(p.z + row);
   const double d1 = W ? p.d1[row] : (double)(len + 1);   // a_ii = 1 + d_i (Thm 3)
-  const double rho = (sp - d1 * zi) + total;              // r_i = s'_i − ((I+L)ẑ)_i
+  const double rho = residual_dd(total, sp, d1, zi);      // r_i = s'_i − ((I+L)ẑ)_i
   const double ar = fabs(rho);
-  if (ar > h) {                                           // |r_i| > h_i
+  if (ar > p.theta * h) {                                 // |r_i| > h_i
     __stcg(p.z + row, zi + p.omega * rho / d1);           // equ:sor1
     t.upd++;
     t.eu += (unsigned long long)len;
@@ -143,9 +176,7 @@ __device__ __forceinline__ void cert_row(const KP &p, const Scalars &S, int row,
   const double h = threshold(S, sp);
   const double zi = p.z[row];
   const double d1 = W ? p.d1[row] : (double)(len + 1);
-  dd_add(total, sp);
-  dd_addprod(total, -d1, zi);
-  const double ratio = fabs(total.hi + total.lo) / h;
+  const double ratio = fabs(residual_dd(total, sp, d1, zi)) / h;
   if (!(ratio <= t.certmax)) t.certmax = ratio;  // NaN sticks
 }
 
@@ -153,10 +184,10 @@ __device__ __forceinline__ void cert_row(const KP &p, const Scalars &S, int row,
 template <int MODE, bool W>
 __device__ __forceinline__ void arc_acc(typename AccT<MODE>::T &a, const KP &p, int64_t k,
                                         double zr) {
-  const int j = __ldg(p.col + k);
-  const double wk = W ? (double)__ldg(p.w + k) : 1.0;
+  const int j = ld_stream(p.col + k);
+  const double wk = W ? (double)ld_stream(p.w + k) : 1.0;
   if constexpr (MODE == RELAX) {
-    a = fma(wk, __ldcg(p.z + j), a);
+    a = fma(wk, ld_z(p.z + j), a);
   } else if constexpr (MODE == CERT) {
     if (W) dd_addprod(a, wk, p.z[j]);
     else dd_add(a, p.z[j]);
@@ -184,7 +215,7 @@ __device__ __forceinline__ void do_group(const KP &p, const Scalars &S, int rb, 
     for (int off = G / 2; off > 0; off >>= 1) acc_merge(a, acc_shfl(a, gmask, off));
     if (lane == 0) {
       const int len = (int)(end - beg);
-      if constexpr (MODE == RELAX) relax_row<W>(p, S, row, len, a, t);
+      if constexpr (MODE == RELAX) relax_row<W>(p, S, row, len, dd{a, 0.0}, t);
       else if constexpr (MODE == CERT) cert_row<W>(p, S, row, len, a, t);
       else t.dis += a;
     }
@@ -206,30 +237,54 @@ __device__ __forceinline__ A block_reduce(A a, A *sm) {
   return a;
 }
 
+// Warp unit (rows above 256 arcs): one warp accumulates a whole row or one
+// kWarpPiece-arc piece of it in registers — 8 independent col/w loads, then 8
+// ẑ gathers per lane per step — and reduces with shuffles (no block barrier).
+// Pieces of one row are combined by the last-arriving warp in piece order
+// (deterministic).
 template <int MODE, bool W>
-__device__ __forceinline__ void do_long(const KP &p, const Scalars &S, const Task &tk, TAcc &t,
-                                        void *smem) {
-  using A = typename AccT<MODE>::T;
+__device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Task &tk, TAcc &t) {
+  // rows above 256 arcs accumulate in double-double for RELAX and CERT
+  using A = typename std::conditional<MODE == DIS, double, dd>::type;
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
   const int row = tk.a, piece = tk.b, np = tk.kind >> 8, slot = tk.slot;
-  const int64_t beg = p.rp[row], end = p.rp[row + 1];
-  const int64_t a0 = beg + (int64_t)piece * kPiece;
-  const int64_t a1 = min(end, a0 + (int64_t)kPiece);
+  const int64_t a0 = tk.a0, a1 = tk.a1;
   const double zr = (MODE == DIS) ? p.z[row] : 0.0;
   A a;
   acc_zero(a);
-#pragma unroll 4
-  for (int64_t k = a0 + threadIdx.x; k < a1; k += kBlock) arc_acc<MODE, W>(a, p, k, zr);
-  a = block_reduce<A>(a, (A *)smem);
-  if (threadIdx.x != 0) return;
-  const int len = (int)(end - beg);
+  for (int64_t k0 = a0 + lane; k0 < a1; k0 += 32 * U) {
+    int j[U];
+    float wv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t k = k0 + 32 * u;
+      j[u] = k < a1 ? ld_stream(p.col + k) : -1;
+      wv[u] = (W && k < a1) ? ld_stream(p.w + k) : 1.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (j[u] < 0) continue;
+      double zj;
+      zj = ld_z(p.z + j[u]);
+      if constexpr (MODE != DIS) {
+        if (W) dd_addprod(a, (double)wv[u], zj);
+        else dd_add(a, zj);
+      } else {
+        const double dz = zr - zj;
+        a = fma((double)wv[u] * dz, dz, a);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc_merge(a, acc_shfl(a, 0xffffffffu, off));
+  if (lane != 0) return;
   if constexpr (MODE == DIS) {
     t.dis += a;
+    return;
   } else {
     if (np > 1) {
-      double2 v;
-      if constexpr (MODE == CERT) v = make_double2(a.hi, a.lo);
-      else v = make_double2(a, 0.0);
-      __stcg(p.partial + slot + piece, v);
+      __stcg(p.partial + slot + piece, make_double2(a.hi, a.lo));
       __threadfence();
       const int old = atomicAdd(p.arrive + slot, 1);
       if (old != np - 1) return;
@@ -237,27 +292,92 @@ __device__ __forceinline__ void do_long(const KP &p, const Scalars &S, const Tas
       acc_zero(a);
       for (int q = 0; q < np; q++) {  // fixed order ⇒ deterministic row sum
         const double2 x = __ldcg(p.partial + slot + q);
-        if constexpr (MODE == CERT) acc_merge(a, dd{x.x, x.y});
-        else a += x.x;
+        acc_merge(a, dd{x.x, x.y});
       }
       p.arrive[slot] = 0;
     }
+    const int len = (int)(__ldg(p.rp + row + 1) - __ldg(p.rp + row));
     if constexpr (MODE == RELAX) relax_row<W>(p, S, row, len, a, t);
     else cert_row<W>(p, S, row, len, a, t);
   }
 }
 
+// RELAX on a GROUP task, smem-staged (the hot loop).  All global loads of
+// the task are issued up front for memory-level parallelism:
+//   row state of the task's rows (rp pair, s, ẑ, 1+d) — one G-lane group per row;
+//   phase 1: the task's contiguous arc range, ≤ kTileArcs = 8 per thread:
+//            col + w loads, then the ẑ gathers, products a_ij ẑ_j → smem;
+//   phase 2: each group sums its row's products from smem, lane 0 relaxes.
+// One __syncthreads per task (smem double-buffered across tasks).
+template <bool W>
+__device__ __forceinline__ void relax_tile(const KP &p, const Scalars &S, const Task &tk, TAcc &t,
+                                           double *prod) {
+  const int cls = tk.kind & 0xff;
+  const int G = 1 << cls;
+  const int lane = threadIdx.x & (G - 1);
+  const int row = tk.a + (threadIdx.x >> cls);
+  const bool has = row < tk.b;
+  int64_t beg = 0, end = 0;
+  float sv = 0.f;
+  double zi = 0.0, d1 = 0.0;
+  if (has) {
+    beg = __ldg(p.rp + row);
+    end = __ldg(p.rp + row + 1);
+    if (lane == 0) {
+      sv = __ldg(p.s + row);
+      zi = __ldcg(p.z + row);
+      if (W) d1 = __ldg(p.d1 + row);
+    }
+  }
+  const int64_t a0 = tk.a0;
+  const int na = (int)(tk.a1 - a0);
+  int j[kTileArcs / kBlock];
+  float wv[kTileArcs / kBlock];
+#pragma unroll
+  for (int u = 0; u < kTileArcs / kBlock; u++) {
+    const int e = u * kBlock + threadIdx.x;
+    if (e < na) {
+      j[u] = ld_stream(p.col + a0 + e);
+      wv[u] = W ? ld_stream(p.w + a0 + e) : 1.0f;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kTileArcs / kBlock; u++) {
+    const int e = u * kBlock + threadIdx.x;
+    if (e < na) prod[e] = (double)wv[u] * ld_z(p.z + j[u]);
+  }
+  __syncthreads();
+  double a = 0.0;
+  if (has) {
+    const int kb = (int)(beg - a0), ke = (int)(end - a0);
+    for (int k = kb + lane; k < ke; k += G) a += prod[k];
+  }
+  for (int off = G >> 1; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+  if (has && lane == 0) {
+    const int len = (int)(end - beg);
+    const double sp = (double)sv + S.c;                       // s' = s + c
+    const double h = threshold(S, sp);
+    if (!W) d1 = (double)(len + 1);                           // a_ii = 1 + d_i
+    const double rho = residual_dd(dd{a, 0.0}, sp, d1, zi);  // r_i = s'_i − ((I+L)ẑ)_i
+    const double ar = fabs(rho);
+    if (ar > p.theta * h) {                                   // |r_i| > h_i
+      __stcg(p.z + row, zi + p.omega * rho / d1);             // equ:sor1
+      t.upd++;
+      t.eu += (unsigned long long)len;
+    }
+    if (!(ar <= S.sentinel)) t.bad = 1;
+  }
+}
+
 template <int MODE, bool W>
-__device__ __forceinline__ void dispatch(const KP &p, const Scalars &S, const Task &tk, TAcc &t,
-                                         void *smem) {
+__device__ __forceinline__ void dispatch_tile(const KP &p, const Scalars &S, const Task &tk, TAcc &t) {
   switch (tk.kind & 0xff) {
     case kG1: do_group<MODE, 1, W>(p, S, tk.a, tk.b, t); break;
     case kG2: do_group<MODE, 2, W>(p, S, tk.a, tk.b, t); break;
     case kG4: do_group<MODE, 4, W>(p, S, tk.a, tk.b, t); break;
     case kG8: do_group<MODE, 8, W>(p, S, tk.a, tk.b, t); break;
     case kG16: do_group<MODE, 16, W>(p, S, tk.a, tk.b, t); break;
-    case kG32: do_group<MODE, 32, W>(p, S, tk.a, tk.b, t); break;
-    default: do_long<MODE, W>(p, S, tk, t, smem); break;
+    default: do_group<MODE, 32, W>(p, S, tk.a, tk.b, t); break;
   }
 }
 
@@ -279,19 +399,11 @@ __device__ __forceinline__ void grid_sync(unsigned *bar) {
   __syncthreads();
 }
 
-__device__ __forceinline__ int claim(unsigned *ctr, int *s_task) {
-  if (threadIdx.x == 0) *s_task = (int)atomicAdd(ctr, 1u);
-  __syncthreads();
-  const int t = *s_task;
-  __syncthreads();
-  return t;
-}
-
 // ------------------------------------------------------ persistent sweeps
 template <bool W>
-__global__ void __launch_bounds__(kBlock) k_sweep(KP p) {
-  __shared__ int s_task;
-  __shared__ double s_red[kBlock / 32];
+__global__ void __launch_bounds__(kBlock, 4) k_sweep(KP p) {
+  extern __shared__ double s_prod[];  // 2 x kTileArcs products
+  int buf = 0;
   __shared__ unsigned long long s_dec[3];
   const Scalars S = *p.sc;
   TAcc t{};
@@ -300,13 +412,16 @@ __global__ void __launch_bounds__(kBlock) k_sweep(KP p) {
   int phase = 0;
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
     for (int k = 0; k < p.ncolors; ++k, ++phase) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[(phase + 2) % 3] = 0u;
       const int t0 = p.phase_begin[k], nt = p.phase_begin[k + 1] - t0;
-      for (;;) {
-        const int ti = claim(p.ctr + phase % 3, &s_task);
-        if (ti >= nt) break;
-        const Task tk = p.tasks[t0 + ti];
-        dispatch<RELAX, W>(p, S, tk, t, s_red);
+      // static round-robin (tasks are balanced by construction; no claim
+      // atomics on the hot loop): warp units first (hub rows), then tiles
+      const int w0 = p.wphase_begin[k], nw = p.wphase_begin[k + 1] - w0;
+      const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+      for (int wi = warp_id; wi < nw; wi += gridDim.x * (kBlock / 32))
+        do_warp<RELAX, W>(p, S, p.wtasks[w0 + wi], t);
+      for (int ti = blockIdx.x; ti < nt; ti += gridDim.x) {
+        relax_tile<W>(p, S, p.tasks[t0 + ti], t, s_prod + (buf & 1) * kTileArcs);
+        buf++;
       }
       if (k + 1 < p.ncolors) grid_sync(p.bar);
     }
@@ -354,18 +469,15 @@ __global__ void __launch_bounds__(kBlock) k_sweep(KP p) {
 
 // ------------------------------------------ one pass over all tasks (CERT/DIS)
 template <int MODE, bool W>
-__global__ void __launch_bounds__(kBlock) k_pass(KP p) {
-  __shared__ int s_task;
-  __shared__ dd s_red[kBlock / 32];
+__global__ void __launch_bounds__(kBlock, 4) k_pass(KP p) {
   Scalars S{};
   if (MODE == CERT) S = *p.sc;
   TAcc t{};
-  for (;;) {
-    const int ti = claim(p.ctr, &s_task);
-    if (ti >= p.ntasks_all) break;
-    const Task tk = p.tasks[ti];
-    dispatch<MODE, W>(p, S, tk, t, s_red);
-  }
+  const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+  for (int wi = warp_id; wi < p.nwtasks_all; wi += gridDim.x * (kBlock / 32))
+    do_warp<MODE, W>(p, S, p.wtasks[wi], t);
+  for (int ti = blockIdx.x; ti < p.ntasks_all; ti += gridDim.x)
+    dispatch_tile<MODE, W>(p, S, p.tasks[ti], t);
   if constexpr (MODE == CERT) {
     double m = t.certmax;
 #pragma unroll
@@ -400,11 +512,12 @@ __global__ void k_scalars(const float *__restrict__ smin, const float *__restric
 // s into layout order; ẑ' = 0 (Alg. 1 init) except rows with no arcs,
 // whose equation is (1 + 0) z_v = s'_v: solved exactly (ẑ'_v = s'_v)
 __global__ void k_init(int64_t n, const int32_t *__restrict__ perm, const int64_t *__restrict__ rp,
-                       const float *__restrict__ s, const Scalars *__restrict__ S,
+                       const float *__restrict__ s, Scalars *__restrict__ S,
                        float *__restrict__ s_l, double *__restrict__ z) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float si = s[perm[i]];
+  if (!isfinite(si)) atomicOr(&S->bad_input, 1);  // min/max reductions skip NaN
   s_l[i] = si;
   z[i] = (rp[i + 1] == rp[i]) ? (double)si + S->c : 0.0;
 }
@@ -463,9 +576,9 @@ static unsigned gridn(int64_t work) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 1 << 30));
 }
 
-static int persistent_grid(const void *fn, int num_sms) {
+static int persistent_grid(const void *fn, int num_sms, size_t smem = 0) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, smem);
   if (per_sm < 1) per_sm = 1;
   return per_sm * num_sms;
 }
@@ -493,9 +606,12 @@ static KP make_kp(const fj_graph *g, const Layout &L) {
   p.w = L.w;
   p.d1 = L.d1;
   p.tasks = L.tasks;
+  p.wtasks = L.wtasks;
   p.phase_begin = L.d_phase_begin;
+  p.wphase_begin = L.d_wphase_begin;
   p.ncolors = L.ncolors;
   p.ntasks_all = L.ntasks;
+  p.nwtasks_all = L.nwtasks;
   return p;
 }
 
@@ -565,7 +681,9 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     FJ_CUDA(cub::DeviceReduce::Max(t, tmp, s.dev, smax, n, st));
     FJ_CUDA(cudaFreeAsync(t, st));
   }
+  fj::count_launch();
   k_scalars<<<1, 1, 0, st>>>(smin, smax, eps, o->sigma, o->c, S);
+  fj::count_launch();
   k_init<<<gridn(n), kBlock, 0, st>>>(n, L.perm, L.rp, s.dev, S, s_l, z);
 
   KP p = make_kp(g, L);
@@ -573,6 +691,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   p.z = z;
   p.sc = S;
   p.omega = omega;
+  p.theta = 1.0;
   p.partial = partial;
   p.arrive = arrive;
   p.max_sweeps = o->max_sweeps;
@@ -583,7 +702,9 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   p.cert_max = certbits;
 
   const void *fn = W ? (const void *)k_sweep<true> : (const void *)k_sweep<false>;
-  const int grid = persistent_grid(fn, g->num_sms);
+  const size_t sweep_smem = 2 * kTileArcs * sizeof(double);
+  FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem));
+  const int grid = persistent_grid(fn, g->num_sms, sweep_smem);
   float ms_sweep = 0, ms_cert = 0;
   int rounds = 0;
   stats.colors = L.ncolors;
@@ -594,7 +715,8 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 8, st));
     void *args[] = {&p};
     FJ_CUDA(cudaEventRecord(es0, st));
-    FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, 0, st));
+    fj::count_launch();
+    FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, sweep_smem, st));
     FJ_CUDA(cudaEventRecord(es1, st));
     // fp64 compensated certificate over every non-empty row
     if (o->certify) {
@@ -603,6 +725,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
       FJ_CUDA(cudaEventRecord(ec0, st));
       const void *cf = W ? (const void *)k_pass<CERT, true> : (const void *)k_pass<CERT, false>;
       void *cargs[] = {&q};
+      fj::count_launch();
       FJ_CUDA(cudaLaunchKernel(cf, persistent_grid(cf, g->num_sms), kBlock, cargs, 0, st));
       FJ_CUDA(cudaEventRecord(ec1, st));
     }
@@ -624,6 +747,11 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     if (stats.reason != 0) break;
     if (!o->certify || stats.cert_ratio <= 1.0 || rounds >= o->cert_rounds) break;
     rounds++;  // resume from ẑ (Lemma 3: ẑ fully determines r)
+    p.max_sweeps = std::min(o->max_sweeps, 2000);  // a resume starts next to the fixed point
+    // the sweep's plain fp64 residual agreed with h where the compensated
+    // one did not: resume with a stricter sweep threshold so that every row
+    // the certificate rejects is relaxed again
+    p.theta *= 0.5;
   }
   stats.cert_rounds = rounds;
   stats.phases = stats.sweeps * L.ncolors;
@@ -632,6 +760,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   stats.relaxations += L.empty_rows;  // rows solved exactly at init
 
   // a6: unshift
+  fj::count_launch();
   k_finalize<<<gridn(n), kBlock, 0, st>>>(n, L.iperm, z, S, zdev ? z_out : zo,
                                           o->zprime_out ? (zpdev ? o->zprime_out : zp) : nullptr);
   if (!zdev) FJ_CUDA(cudaMemcpyAsync(z_out, zo, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
@@ -697,7 +826,9 @@ fj_status measures_impl(fj_graph *g, const float *z_in, const float *s_in, fj_me
   FJ_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * 5, st));
   FJ_CUDA(cudaMallocAsync(&ctr, sizeof(unsigned), st));
   FJ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), st));
+  fj::count_launch();
   k_meas_nodes1<<<gridn(n), kBlock, 0, st>>>(n, L.perm, z.dev, zl, sums);
+  fj::count_launch();
   k_meas_nodes2<<<gridn(n), kBlock, 0, st>>>(n, z.dev, s.dev, sums);
   KP p = make_kp(g, L);
   p.z = zl;
@@ -706,6 +837,7 @@ fj_status measures_impl(fj_graph *g, const float *z_in, const float *s_in, fj_me
   const bool W = g->weighted != 0;
   const void *fn = W ? (const void *)k_pass<DIS, true> : (const void *)k_pass<DIS, false>;
   void *args[] = {&p};
+  fj::count_launch();
   FJ_CUDA(cudaLaunchKernel(fn, persistent_grid(fn, g->num_sms), kBlock, args, 0, st));
   double h[5];
   FJ_CUDA(cudaMemcpyAsync(h, sums, sizeof(h), cudaMemcpyDeviceToHost, st));
