@@ -54,7 +54,7 @@ typedef enum {
    the same certified rule; they differ in the order of relaxations, which
    Lemma 3 allows to be arbitrary. */
 typedef enum {
-  FJ_METHOD_AUTO = 0,    /* ASYNC at ω = 1, COLORED otherwise                   */
+  FJ_METHOD_AUTO = 0,    /* ASYNC at ω = 1 or on directed graphs, else COLORED  */
   FJ_METHOD_ASYNC = 1,   /* in-place asynchronous sweeps (chaotic Gauss–Seidel) */
   FJ_METHOD_COLORED = 2, /* multicolor Gauss–Seidel/SOR: rows of one color are
                             mutually non-adjacent, colors run in sequence, so

@@ -30,31 +30,21 @@ bool is_device_ptr(const void *p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-void Layout::release() {
-  cudaFree(perm);
-  cudaFree(iperm);
-  cudaFree(rp);
-  cudaFree(col);
-  cudaFree(w);
-  cudaFree(d1);
-  cudaFree(tasks);
-  cudaFree(wtasks);
-  cudaFree(d_phase_begin);
-  cudaFree(d_wphase_begin);
+void Layout::release(cudaStream_t st) {
+  for (void *q : {(void *)perm, (void *)iperm, (void *)rp, (void *)col, (void *)w, (void *)d1,
+                  (void *)tasks, (void *)wtasks, (void *)d_phase_begin, (void *)d_wphase_begin})
+    if (q) cudaFreeAsync(q, st);
   perm = iperm = nullptr;
   rp = nullptr;
   col = nullptr;
   w = nullptr;
   d1 = nullptr;
-  tasks = nullptr;
-  wtasks = nullptr;
-  d_phase_begin = nullptr;
-  d_wphase_begin = nullptr;
-  ntasks = 0;
-  nwtasks = 0;
-  wphase_begin.clear();
+  tasks = wtasks = nullptr;
+  d_phase_begin = d_wphase_begin = nullptr;
+  ntasks = nwtasks = 0;
   ncolors = 0;
   phase_begin.clear();
+  wphase_begin.clear();
 }
 
 }  // namespace fj

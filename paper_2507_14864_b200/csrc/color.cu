@@ -84,8 +84,8 @@ fj_status build_coloring(fj_graph *g) {
   int32_t *c0 = nullptr, *c1 = nullptr;
   unsigned long long *rem = nullptr;
   int *maxc = nullptr;
-  FJ_CUDA(cudaMalloc(&c0, sizeof(int32_t) * n));
-  FJ_CUDA(cudaMalloc(&c1, sizeof(int32_t) * n));
+  FJ_CUDA(cudaMallocAsync(&c0, sizeof(int32_t) * n, st));
+  FJ_CUDA(cudaMallocAsync(&c1, sizeof(int32_t) * n, st));
   FJ_CUDA(cudaMallocAsync(&rem, sizeof(unsigned long long), st));
   FJ_CUDA(cudaMallocAsync(&maxc, sizeof(int), st));
   FJ_CUDA(cudaMemsetAsync(c0, 0xff, sizeof(int32_t) * n, st));
@@ -112,13 +112,13 @@ fj_status build_coloring(fj_graph *g) {
   FJ_CUDA(cudaStreamSynchronize(st));
   g->ncolors = hmax + 1;
   g->colors = c0;
-  cudaFree(c1);
+  cudaFreeAsync(c1, st);
   cudaFreeAsync(rem, st);
   cudaFreeAsync(maxc, st);
   fj_status s = build_layout_from_out(g, ort, ocol, ow, g->colors, g->ncolors, &g->color_layout);
-  cudaFree(ort);
-  cudaFree(ocol);
-  cudaFree(ow);
+  cudaFreeAsync(ort, st);
+  cudaFreeAsync(ocol, st);
+  if (ow) cudaFreeAsync(ow, st);
   FJ_CUDA(cudaStreamSynchronize(st));
   return s;
 }

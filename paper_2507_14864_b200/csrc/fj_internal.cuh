@@ -80,7 +80,7 @@ struct Layout {
   int64_t empty_rows = 0;
   int64_t active_rows = 0;        // rows with L > 0
   int64_t max_len = 0;
-  void release();
+  void release(cudaStream_t st);
 };
 
 }  // namespace fj

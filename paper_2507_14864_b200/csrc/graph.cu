@@ -11,6 +11,11 @@
 //   6. build the sweep layout (layout.cu).
 // Sorting and scans use CUB (toolkit library primitives); every kernel here
 // is a one-pass O(m) integer/fp64 kernel.
+#include <stdio.h>
+#include <stdlib.h>
+#include <time.h>
+
+#include <algorithm>
 #include <cub/cub.cuh>
 
 #include "fj_internal.cuh"
@@ -35,26 +40,40 @@ __global__ void k_validate_rowptr(int64_t n, int64_t m, const int64_t *__restric
   if (x < 0 || x > m) atomicOr(err, 1);
 }
 
-// one warp per row: keys[(v,u)] for the in-CSR arcs of row v, with column and
-// weight checks
-__global__ void k_in_keys(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                          const float *__restrict__ w, int nb, uint64_t *__restrict__ keys,
-                          int *__restrict__ err) {
+// One warp per row of the caller's in-CSR: column range, self-loops, weight
+// validity, and whether the row is already strictly increasing (bit 64: not
+// canonical, the rows must be sorted).
+__global__ void k_check_rows(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                             const float *__restrict__ w, int *__restrict__ err) {
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
   for (int64_t v = warp; v < n; v += nwarps) {
+    int bad = 0;
     for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) {
-      int32_t u = col[e];
-      if (u < 0 || u >= n) { atomicOr(err, 2); u = 0; }
-      if (u == v) atomicOr(err, 4);
+      const int32_t u = col[e];
+      if (u < 0 || u >= n) bad |= 2;
+      if (u == v) bad |= 4;
       if (w) {
-        float x = w[e];
-        if (!(x > 0.0f) || !isfinite(x)) atomicOr(err, 8);
+        const float x = w[e];
+        if (!(x > 0.0f) || !isfinite(x)) bad |= 8;
       }
-      keys[e] = ((uint64_t)v << nb) | (uint64_t)u;
+      if (e > rp[v] && col[e - 1] >= u) bad |= 64;
     }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0 && bad) atomicOr(err, bad);
   }
+}
+
+// (v, u) keys of the in-CSR arcs (only when rows must be sorted)
+__global__ void k_in_keys(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                          int nb, uint64_t *__restrict__ keys) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps)
+    for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32)
+      keys[e] = ((uint64_t)v << nb) | (uint64_t)col[e];
 }
 
 __global__ void k_iota_u32(int64_t m, uint32_t *__restrict__ x) {
@@ -75,18 +94,45 @@ __global__ void k_unpack_sorted(int64_t m, int nb, const uint64_t *__restrict__ 
   if (w_dst) w_dst[i] = w_src[idx[i]];
 }
 
-// out-CSR keys (u, v) from the canonical in-CSR: arc u→v sits in row v, col u
+// transpose inputs: key u, payload arc index; row of every arc
 __global__ void k_out_keys(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                           int nb, uint64_t *__restrict__ keys, int64_t *__restrict__ cnt) {
+                           uint32_t *__restrict__ key, uint32_t *__restrict__ idx,
+                           uint32_t *__restrict__ row) {
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
   for (int64_t v = warp; v < n; v += nwarps)
     for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) {
-      uint64_t u = (uint64_t)col[e];
-      keys[e] = (u << nb) | (uint64_t)v;
-      atomicAdd((unsigned long long *)&cnt[u], 1ull);
+      key[e] = (uint32_t)col[e];
+      idx[e] = (uint32_t)e;
+      row[e] = (uint32_t)v;
     }
+}
+
+// row pointers of the out-CSR from the sorted keys (no atomics): ort[u] is
+// the first position whose key is >= u (binary search)
+__global__ void k_bounds(int64_t n, int64_t m, const uint32_t *__restrict__ key,
+                         int64_t *__restrict__ ort) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u > n) return;
+  int64_t lo = 0, hi = m;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)key[mid] < u) lo = mid + 1;
+    else hi = mid;
+  }
+  ort[u] = lo;
+}
+
+// out-CSR entries from the stably sorted arc indices (v ascending within u)
+__global__ void k_out_fill(int64_t m, const uint32_t *__restrict__ idx, const uint32_t *__restrict__ row,
+                           const float *__restrict__ w, int32_t *__restrict__ ocol,
+                           float *__restrict__ ow) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const uint32_t e = idx[k];
+  ocol[k] = (int32_t)row[e];
+  if (ow) ow[k] = w[e];
 }
 
 // d_u = Σ_v a_uv over the out-row u (warp per row, fixed lane order + fixed
@@ -123,12 +169,17 @@ static unsigned grid_for(int64_t work, int per_block = kBlock) {
   return (unsigned)b;
 }
 
-// Sort `m` keys (and a 32-bit index payload) on bits [0, nbits).
-static fj_status sort_pairs(uint64_t *&keys, uint64_t *&keys_alt, uint32_t *&idx,
-                            uint32_t *&idx_alt, int64_t m, int nbits, cudaStream_t st) {
+static unsigned grid_warps(int64_t rows) {  // warp-per-row kernels: grid-stride
+  int64_t b = (rows * 32 + kBlock - 1) / kBlock;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 64));
+}
+
+template <class K, class V>
+static fj_status sort_pairs(K *&keys, K *&keys_alt, V *&val, V *&val_alt, int64_t m, int nbits,
+                            cudaStream_t st) {
   if (m == 0) return FJ_OK;
-  cub::DoubleBuffer<uint64_t> dk(keys, keys_alt);
-  cub::DoubleBuffer<uint32_t> dv(idx, idx_alt);
+  cub::DoubleBuffer<K> dk(keys, keys_alt);
+  cub::DoubleBuffer<V> dv(val, val_alt);
   size_t tmp = 0;
   FJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, m, 0, nbits, st));
   void *t = nullptr;
@@ -136,64 +187,61 @@ static fj_status sort_pairs(uint64_t *&keys, uint64_t *&keys_alt, uint32_t *&idx
   FJ_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, m, 0, nbits, st));
   FJ_CUDA(cudaFreeAsync(t, st));
   if (dk.Current() != keys) std::swap(keys, keys_alt);
-  if (dv.Current() != idx) std::swap(idx, idx_alt);
-  return FJ_OK;
-}
-
-static fj_status exclusive_scan_i64(int64_t *in, int64_t *out, int64_t count, cudaStream_t st) {
-  size_t tmp = 0;
-  FJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, count, st));
-  void *t = nullptr;
-  FJ_CUDA(cudaMallocAsync(&t, tmp, st));
-  FJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, count, st));
-  FJ_CUDA(cudaFreeAsync(t, st));
+  if (dv.Current() != val) std::swap(val, val_alt);
   return FJ_OK;
 }
 
 // Transpose the canonical in-CSR into the pull CSR (row u lists v with a_uv),
-// rows sorted.  Caller frees *ort, *ocol, *ow (cudaFree).
+// rows sorted: a stable radix sort on u alone keeps the v order of the
+// canonical input.  Caller frees *ort, *ocol, *ow (cudaFreeAsync on g->stream).
 fj_status transpose_in_csr(fj_graph *g, int64_t **ort, int32_t **ocol, float **ow) {
   cudaStream_t st = g->stream;
   const int64_t n = g->n, m = g->m;
-  const int nb = bits_for(n);
-  uint64_t *k0 = nullptr, *k1 = nullptr;
-  uint32_t *i0 = nullptr, *i1 = nullptr;
-  int64_t *cnt = nullptr;
-  FJ_CUDA(cudaMallocAsync(&k0, sizeof(uint64_t) * (m + 1), st));
-  FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint64_t) * (m + 1), st));
+  uint32_t *k0 = nullptr, *k1 = nullptr, *i0 = nullptr, *i1 = nullptr, *row = nullptr;
+  FJ_CUDA(cudaMallocAsync(&k0, sizeof(uint32_t) * (m + 1), st));
+  FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint32_t) * (m + 1), st));
   FJ_CUDA(cudaMallocAsync(&i0, sizeof(uint32_t) * (m + 1), st));
   FJ_CUDA(cudaMallocAsync(&i1, sizeof(uint32_t) * (m + 1), st));
-  FJ_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * (n + 1), st));
-  FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (n + 1), st));
-  FJ_CUDA(cudaMalloc(ort, sizeof(int64_t) * (n + 1)));
-  FJ_CUDA(cudaMalloc(ocol, sizeof(int32_t) * (m + 1)));
+  FJ_CUDA(cudaMallocAsync(&row, sizeof(uint32_t) * (m + 1), st));
+  FJ_CUDA(cudaMallocAsync(ort, sizeof(int64_t) * (n + 1), st));
+  FJ_CUDA(cudaMallocAsync(ocol, sizeof(int32_t) * (m + 8), st));
   *ow = nullptr;
-  if (g->in_w) FJ_CUDA(cudaMalloc(ow, sizeof(float) * (m + 1)));
+  if (g->in_w) FJ_CUDA(cudaMallocAsync(ow, sizeof(float) * (m + 8), st));
   fj::count_launch();
-  k_out_keys<<<grid_for(n * 32), kBlock, 0, st>>>(n, g->in_rp, g->in_col, nb, k0, cnt);
-  fj::count_launch();
-  k_iota_u32<<<grid_for(m), kBlock, 0, st>>>(m, i0);
-  FJ_TRY(sort_pairs(k0, k1, i0, i1, m, 2 * nb, st));
-  int *err = nullptr;
-  FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
-  FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  k_out_keys<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, k0, i0, row);
+  FJ_TRY(sort_pairs(k0, k1, i0, i1, m, bits_for(n), st));
   if (m > 0) {
     fj::count_launch();
-    k_unpack_sorted<<<grid_for(m), kBlock, 0, st>>>(m, nb, k0, i0, g->in_w, *ocol, *ow, err);
+    k_out_fill<<<grid_for(m), kBlock, 0, st>>>(m, i0, row, g->in_w, *ocol, *ow);
   }
-  FJ_TRY(exclusive_scan_i64(cnt, *ort, n + 1, st));
-  FJ_CUDA(cudaFreeAsync(err, st));
+  fj::count_launch();
+  k_bounds<<<grid_for(n + 1), kBlock, 0, st>>>(n, m, k0, *ort);
   FJ_CUDA(cudaFreeAsync(k0, st));
   FJ_CUDA(cudaFreeAsync(k1, st));
   FJ_CUDA(cudaFreeAsync(i0, st));
   FJ_CUDA(cudaFreeAsync(i1, st));
-  FJ_CUDA(cudaFreeAsync(cnt, st));
+  FJ_CUDA(cudaFreeAsync(row, st));
   FJ_CUDA(cudaGetLastError());
   return FJ_OK;
 }
 
+static double wall() {
+  timespec t;
+  clock_gettime(CLOCK_MONOTONIC, &t);
+  return t.tv_sec + 1e-9 * t.tv_nsec;
+}
+
 static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const int32_t *col_in,
                              const float *w_in, int directed, cudaStream_t st, fj_graph *g) {
+  const bool dbg = getenv("FJ_DEBUG") != nullptr;
+  double t0 = wall();
+  auto mark = [&](const char *what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(st);
+    double t1 = wall();
+    fprintf(stderr, "fj create %-28s %8.2f ms\n", what, 1e3 * (t1 - t0));
+    t0 = t1;
+  };
   g->n = n;
   g->m = nnz;
   g->directed = directed ? 1 : 0;
@@ -202,66 +250,80 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
   int dev = 0;
   FJ_CUDA(cudaGetDevice(&dev));
   FJ_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  {
+    // keep stream-ordered allocations in the pool between calls (graphs and
+    // solve workspaces are re-created per call; re-mapping GBs is slow)
+    cudaMemPool_t pool;
+    FJ_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = ~0ull;
+    FJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   const int64_t m = nnz;
   const int nb = bits_for(n);
 
-  // 1. stage
-  FJ_CUDA(cudaMalloc(&g->in_rp, sizeof(int64_t) * (n + 1)));
-  FJ_CUDA(cudaMalloc(&g->in_col, sizeof(int32_t) * (m + 1)));
-  if (w_in) FJ_CUDA(cudaMalloc(&g->in_w, sizeof(float) * (m + 1)));
-  int32_t *col_raw = nullptr;
-  float *w_raw = nullptr;
-  FJ_CUDA(cudaMallocAsync(&col_raw, sizeof(int32_t) * (m + 1), st));
-  if (w_in) FJ_CUDA(cudaMallocAsync(&w_raw, sizeof(float) * (m + 1), st));
+  // 1. stage into library-owned memory (padded: the sweep reads in 16-byte units)
+  FJ_CUDA(cudaMallocAsync(&g->in_rp, sizeof(int64_t) * (n + 1), st));
+  FJ_CUDA(cudaMallocAsync(&g->in_col, sizeof(int32_t) * (m + 8), st));
+  if (w_in) FJ_CUDA(cudaMallocAsync(&g->in_w, sizeof(float) * (m + 8), st));
   FJ_CUDA(cudaMemcpyAsync(g->in_rp, rp_in, sizeof(int64_t) * (n + 1), cudaMemcpyDefault, st));
   if (m > 0) {
-    FJ_CUDA(cudaMemcpyAsync(col_raw, col_in, sizeof(int32_t) * m, cudaMemcpyDefault, st));
-    if (w_in) FJ_CUDA(cudaMemcpyAsync(w_raw, w_in, sizeof(float) * m, cudaMemcpyDefault, st));
+    FJ_CUDA(cudaMemcpyAsync(g->in_col, col_in, sizeof(int32_t) * m, cudaMemcpyDefault, st));
+    if (w_in) FJ_CUDA(cudaMemcpyAsync(g->in_w, w_in, sizeof(float) * m, cudaMemcpyDefault, st));
   }
+  mark("stage");
 
-  // 2. validate row_ptr before anything indexes with it
+  // 2. validate
   int *err = nullptr;
+  int herr = 0;
   FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
   FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
   fj::count_launch();
   k_validate_rowptr<<<grid_for(n + 1), kBlock, 0, st>>>(n, m, g->in_rp, err);
-  int herr = 0;
   FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
   if (herr) {
     cudaFreeAsync(err, st);
-    cudaFreeAsync(col_raw, st);
-    cudaFreeAsync(w_raw, st);
     set_error("fj_graph_create: in_row_ptr must start at 0, be non-decreasing and end at nnz");
     return FJ_ERR_INVALID;
   }
-
-  // 3. canonical in-CSR
-  uint64_t *k0 = nullptr, *k1 = nullptr;
-  uint32_t *i0 = nullptr, *i1 = nullptr;
-  FJ_CUDA(cudaMallocAsync(&k0, sizeof(uint64_t) * (m + 1), st));
-  FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint64_t) * (m + 1), st));
-  FJ_CUDA(cudaMallocAsync(&i0, sizeof(uint32_t) * (m + 1), st));
-  FJ_CUDA(cudaMallocAsync(&i1, sizeof(uint32_t) * (m + 1), st));
   fj::count_launch();
-  k_in_keys<<<grid_for(n * 32), kBlock, 0, st>>>(n, g->in_rp, col_raw, w_raw, nb, k0, err);
-  fj::count_launch();
-  k_iota_u32<<<grid_for(m), kBlock, 0, st>>>(m, i0);
-  FJ_TRY(sort_pairs(k0, k1, i0, i1, m, 2 * nb, st));
-  if (m > 0) {
-    fj::count_launch();
-    k_unpack_sorted<<<grid_for(m), kBlock, 0, st>>>(m, nb, k0, i0, w_raw, g->in_col, g->in_w, err);
-  }
-  FJ_CUDA(cudaFreeAsync(k0, st));
-  FJ_CUDA(cudaFreeAsync(k1, st));
-  FJ_CUDA(cudaFreeAsync(i0, st));
-  FJ_CUDA(cudaFreeAsync(i1, st));
-  FJ_CUDA(cudaFreeAsync(col_raw, st));
-  if (w_raw) FJ_CUDA(cudaFreeAsync(w_raw, st));
+  k_check_rows<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, g->in_w, err);
   FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
+  mark("validate");
+
+  // 3. canonical in-CSR: sort rows only if some row is not strictly increasing
+  if ((herr & ~64) == 0 && (herr & 64)) {
+    uint64_t *k0 = nullptr, *k1 = nullptr;
+    uint32_t *i0 = nullptr, *i1 = nullptr;
+    int32_t *col_raw = nullptr;
+    float *w_raw = nullptr;
+    FJ_CUDA(cudaMallocAsync(&k0, sizeof(uint64_t) * (m + 1), st));
+    FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint64_t) * (m + 1), st));
+    FJ_CUDA(cudaMallocAsync(&i0, sizeof(uint32_t) * (m + 1), st));
+    FJ_CUDA(cudaMallocAsync(&i1, sizeof(uint32_t) * (m + 1), st));
+    FJ_CUDA(cudaMallocAsync(&col_raw, sizeof(int32_t) * (m + 1), st));
+    FJ_CUDA(cudaMemcpyAsync(col_raw, g->in_col, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, st));
+    if (w_in) {
+      FJ_CUDA(cudaMallocAsync(&w_raw, sizeof(float) * (m + 1), st));
+      FJ_CUDA(cudaMemcpyAsync(w_raw, g->in_w, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+    }
+    fj::count_launch();
+    k_in_keys<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, col_raw, nb, k0);
+    fj::count_launch();
+    k_iota_u32<<<grid_for(m), kBlock, 0, st>>>(m, i0);
+    FJ_TRY(sort_pairs(k0, k1, i0, i1, m, 2 * nb, st));
+    FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+    fj::count_launch();
+    k_unpack_sorted<<<grid_for(m), kBlock, 0, st>>>(m, nb, k0, i0, w_raw, g->in_col, g->in_w, err);
+    FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    for (void *q : {(void *)k0, (void *)k1, (void *)i0, (void *)i1, (void *)col_raw, (void *)w_raw})
+      if (q) FJ_CUDA(cudaFreeAsync(q, st));
+    FJ_CUDA(cudaStreamSynchronize(st));
+    mark("canonicalise (sort)");
+  }
   FJ_CUDA(cudaGetLastError());
-  if (herr) {
+  if (herr & ~64) {
     cudaFreeAsync(err, st);
     set_error("fj_graph_create: %s%s%s%s",
               herr & 2 ? "column index out of range; " : "", herr & 4 ? "self-loop; " : "",
@@ -275,9 +337,10 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
   int32_t *ocol = nullptr;
   float *ow = nullptr;
   FJ_TRY(transpose_in_csr(g, &ort, &ocol, &ow));
-  FJ_CUDA(cudaMalloc(&g->deg, sizeof(double) * n));
+  FJ_CUDA(cudaMallocAsync(&g->deg, sizeof(double) * n, st));
   fj::count_launch();
-  k_row_sums<<<grid_for(n * 32), kBlock, 0, st>>>(n, ort, ow, g->deg);
+  k_row_sums<<<grid_warps(n), kBlock, 0, st>>>(n, ort, ow, g->deg);
+  mark("transpose + degrees");
 
   // 5. symmetry of undirected input
   if (!g->directed && m > 0) {
@@ -292,24 +355,26 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
     FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
     FJ_CUDA(cudaStreamSynchronize(st));
     if (herr) {
-      cudaFree(ort);
-      cudaFree(ocol);
-      cudaFree(ow);
+      cudaFreeAsync(ort, st);
+      cudaFreeAsync(ocol, st);
+      if (ow) cudaFreeAsync(ow, st);
       cudaFreeAsync(err, st);
       set_error("fj_graph_create: directed = 0 but the arc set is not symmetric with equal weights");
       return FJ_ERR_INVALID;
     }
+    mark("symmetry check");
   }
   FJ_CUDA(cudaFreeAsync(err, st));
 
   // 6. sweep layout (1 color)
   fj_status s = build_layout_from_out(g, ort, ocol, ow, nullptr, 1, &g->async_layout);
-  cudaFree(ort);
-  cudaFree(ocol);
-  cudaFree(ow);
+  cudaFreeAsync(ort, st);
+  cudaFreeAsync(ocol, st);
+  if (ow) cudaFreeAsync(ow, st);
   if (s != FJ_OK) return s;
   FJ_CUDA(cudaStreamSynchronize(st));
   FJ_CUDA(cudaGetLastError());
+  mark("layout");
   return FJ_OK;
 }
 
@@ -343,13 +408,12 @@ fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t *in_row_ptr, con
 fj_status fj_graph_destroy(fj_graph_t g) {
   if (!g) return FJ_OK;
   cudaStreamSynchronize(g->stream);
-  cudaFree(g->in_rp);
-  cudaFree(g->in_col);
-  cudaFree(g->in_w);
-  cudaFree(g->deg);
-  cudaFree(g->colors);
-  g->async_layout.release();
-  g->color_layout.release();
+  for (void *q : {(void *)g->in_rp, (void *)g->in_col, (void *)g->in_w, (void *)g->deg,
+                  (void *)g->colors})
+    if (q) cudaFreeAsync(q, g->stream);
+  g->async_layout.release(g->stream);
+  g->color_layout.release(g->stream);
+  cudaStreamSynchronize(g->stream);
   delete g;
   return FJ_OK;
 }

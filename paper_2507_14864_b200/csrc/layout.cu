@@ -102,7 +102,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
                                 const float *ow, const int32_t *color, int ncolors, Layout *L) {
   cudaStream_t st = g->stream;
   const int64_t n = g->n, m = g->m;
-  L->release();
+  L->release(st);
   L->n = n;
   L->m = m;
   L->ncolors = ncolors;
@@ -132,12 +132,12 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     FJ_CUDA(cudaFreeAsync(t, st));
     if (dk.Current() != k0) std::swap(k0, k1);
   }
-  FJ_CUDA(cudaMalloc(&L->perm, sizeof(int32_t) * n));
-  FJ_CUDA(cudaMalloc(&L->iperm, sizeof(int32_t) * n));
-  FJ_CUDA(cudaMalloc(&L->rp, sizeof(int64_t) * (n + 1)));
-  FJ_CUDA(cudaMalloc(&L->col, sizeof(int32_t) * (m + 1)));
-  if (ow) FJ_CUDA(cudaMalloc(&L->w, sizeof(float) * (m + 1)));
-  if (g->weighted) FJ_CUDA(cudaMalloc(&L->d1, sizeof(double) * n));
+  FJ_CUDA(cudaMallocAsync(&L->perm, sizeof(int32_t) * n, st));
+  FJ_CUDA(cudaMallocAsync(&L->iperm, sizeof(int32_t) * n, st));
+  FJ_CUDA(cudaMallocAsync(&L->rp, sizeof(int64_t) * (n + 2), st));
+  FJ_CUDA(cudaMallocAsync(&L->col, sizeof(int32_t) * (m + 8), st));
+  if (ow) FJ_CUDA(cudaMallocAsync(&L->w, sizeof(float) * (m + 8), st));
+  if (g->weighted) FJ_CUDA(cudaMallocAsync(&L->d1, sizeof(double) * n, st));
   fj::count_launch();
   k_perm<<<gridn(n), kBlock, 0, st>>>(n, k0, ort, L->perm, L->iperm, len);
   {
@@ -192,8 +192,9 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
       if (r1 <= r0) continue;
       if (cls == 7) {
         std::vector<int64_t> rph(r1 - r0 + 1);
-        FJ_CUDA(cudaMemcpy(rph.data(), L->rp + r0, sizeof(int64_t) * (r1 - r0 + 1),
-                           cudaMemcpyDeviceToHost));
+        FJ_CUDA(cudaMemcpyAsync(rph.data(), L->rp + r0, sizeof(int64_t) * (r1 - r0 + 1),
+                                cudaMemcpyDeviceToHost, st));
+        FJ_CUDA(cudaStreamSynchronize(st));
         for (int64_t i = r0; i < r1; i++) {
           int64_t len_i = rph[i - r0 + 1] - rph[i - r0];
           int np = (int)((len_i + kWarpPiece - 1) / kWarpPiece);
@@ -219,7 +220,8 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     for (int c = 0; c <= ncolors; c++) cut[c] = gstart[c * kClasses];
     std::vector<int64_t> arc(ncolors + 1);
     for (int c = 0; c <= ncolors; c++)
-      FJ_CUDA(cudaMemcpy(&arc[c], L->rp + cut[c], sizeof(int64_t), cudaMemcpyDeviceToHost));
+      FJ_CUDA(cudaMemcpyAsync(&arc[c], L->rp + cut[c], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FJ_CUDA(cudaStreamSynchronize(st));
     for (int c = 0; c < ncolors; c++)
       fprintf(stderr, "fj layout color %d rows %lld arcs %lld tiles %d warp_units %d\n", c,
               (long long)(cut[c + 1] - cut[c]), (long long)(arc[c + 1] - arc[c]),
@@ -232,19 +234,20 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   for (int which = 0; which < 2; which++) {
     std::vector<Task> &v = which ? wtasks : tasks;
     Task **dst = which ? &L->wtasks : &L->tasks;
-    FJ_CUDA(cudaMalloc(dst, sizeof(Task) * std::max<size_t>(1, v.size())));
+    FJ_CUDA(cudaMallocAsync(dst, sizeof(Task) * std::max<size_t>(1, v.size()), st));
     if (!v.empty()) {
-      FJ_CUDA(cudaMemcpy(*dst, v.data(), sizeof(Task) * v.size(), cudaMemcpyHostToDevice));
+      FJ_CUDA(cudaMemcpyAsync(*dst, v.data(), sizeof(Task) * v.size(), cudaMemcpyHostToDevice, st));
       fj::count_launch();
       k_task_arcs<<<gridn((int64_t)v.size()), kBlock, 0, st>>>((int)v.size(), L->rp, *dst);
     }
   }
-  FJ_CUDA(cudaMalloc(&L->d_phase_begin, sizeof(int) * (ncolors + 1)));
-  FJ_CUDA(cudaMemcpy(L->d_phase_begin, L->phase_begin.data(), sizeof(int) * (ncolors + 1),
-                     cudaMemcpyHostToDevice));
-  FJ_CUDA(cudaMalloc(&L->d_wphase_begin, sizeof(int) * (ncolors + 1)));
-  FJ_CUDA(cudaMemcpy(L->d_wphase_begin, L->wphase_begin.data(), sizeof(int) * (ncolors + 1),
-                     cudaMemcpyHostToDevice));
+  FJ_CUDA(cudaMallocAsync(&L->d_phase_begin, sizeof(int) * (ncolors + 1), st));
+  FJ_CUDA(cudaMemcpyAsync(L->d_phase_begin, L->phase_begin.data(), sizeof(int) * (ncolors + 1),
+                          cudaMemcpyHostToDevice, st));
+  FJ_CUDA(cudaMallocAsync(&L->d_wphase_begin, sizeof(int) * (ncolors + 1), st));
+  FJ_CUDA(cudaMemcpyAsync(L->d_wphase_begin, L->wphase_begin.data(), sizeof(int) * (ncolors + 1),
+                          cudaMemcpyHostToDevice, st));
+  FJ_CUDA(cudaStreamSynchronize(st));  // host vectors above are stack-owned
   FJ_CUDA(cudaFreeAsync(k0, st));
   FJ_CUDA(cudaFreeAsync(k1, st));
   FJ_CUDA(cudaFreeAsync(gcount, st));

@@ -621,7 +621,14 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   const int64_t n = g->n;
   fj_stats stats{};
   int method = o->method;
-  if (method == FJ_METHOD_AUTO) method = (omega == 1.0) ? FJ_METHOD_ASYNC : FJ_METHOD_COLORED;
+  // AUTO: BLI (ω = 1) runs asynchronous sweeps, provably convergent for the
+  // M-matrix I + L in any order.  BLISOR (ω ≠ 1) on an undirected graph runs
+  // multicolor sweeps (sequential SOR on an SPD matrix converges for every
+  // ω ∈ (0,2)); on a directed graph, where no ordering carries a
+  // guarantee, asynchronous sweeps (the certificate and the divergence
+  // sentinel still decide the outcome).
+  if (method == FJ_METHOD_AUTO)
+    method = (omega == 1.0 || g->directed) ? FJ_METHOD_ASYNC : FJ_METHOD_COLORED;
   if (method == FJ_METHOD_COLORED && !g->colors) FJ_TRY(build_coloring(g));
   if (method == FJ_METHOD_PUSH) {
     set_error("fj_solve: FJ_METHOD_PUSH is not available in this build");
