@@ -88,7 +88,8 @@ __device__ __forceinline__ float ld_stream(const float *q) {
 // that (Lemma 3 holds for any order).  Every grid barrier executes a
 // gpu-scope fence, which invalidates L1, so the certifying zero-update sweep
 // and every color phase read current values.
-__device__ __forceinline__ double ld_z(const double *q) { return __ldca(q); }
+// (weak loads: the compiler may batch them; __ldca compiles to a strong load)
+__device__ __forceinline__ double ld_z(const double *q) { return *q; }
 
 struct dd {
   double hi, lo;
@@ -254,24 +255,29 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
   A a;
   acc_zero(a);
   for (int64_t k0 = a0 + lane; k0 < a1; k0 += 32 * U) {
+    // stage 1: all column / weight loads of this step (out-of-range lanes
+    // read a valid dummy slot and contribute weight 0)
     int j[U];
     float wv[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int64_t k = k0 + 32 * u;
-      j[u] = k < a1 ? ld_stream(p.col + k) : -1;
-      wv[u] = (W && k < a1) ? ld_stream(p.w + k) : 1.0f;
+      const bool ok = k < a1;
+      j[u] = ld_stream(p.col + (ok ? k : a0));
+      wv[u] = W ? ld_stream(p.w + (ok ? k : a0)) : 1.0f;
+      if (!ok) wv[u] = 0.0f;
     }
+    // stage 2: all gathers
+    double zj[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
+    // stage 3: accumulate
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      if (j[u] < 0) continue;
-      double zj;
-      zj = ld_z(p.z + j[u]);
       if constexpr (MODE != DIS) {
-        if (W) dd_addprod(a, (double)wv[u], zj);
-        else dd_add(a, zj);
+        dd_addprod(a, (double)wv[u], zj[u]);
       } else {
-        const double dz = zr - zj;
+        const double dz = zr - zj[u];
         a = fma((double)wv[u] * dz, dz, a);
       }
     }
@@ -331,20 +337,23 @@ __device__ __forceinline__ void relax_tile(const KP &p, const Scalars &S, const 
   }
   const int64_t a0 = tk.a0;
   const int na = (int)(tk.a1 - a0);
-  int j[kTileArcs / kBlock];
-  float wv[kTileArcs / kBlock];
+  constexpr int U = kTileArcs / kBlock;
+  int j[U];
+  float wv[U];
 #pragma unroll
-  for (int u = 0; u < kTileArcs / kBlock; u++) {
+  for (int u = 0; u < U; u++) {
     const int e = u * kBlock + threadIdx.x;
-    if (e < na) {
-      j[u] = ld_stream(p.col + a0 + e);
-      wv[u] = W ? ld_stream(p.w + a0 + e) : 1.0f;
-    }
+    const bool ok = e < na;
+    j[u] = ld_stream(p.col + a0 + (ok ? e : 0));
+    wv[u] = W ? ld_stream(p.w + a0 + (ok ? e : 0)) : 1.0f;
   }
+  double zj[U];
 #pragma unroll
-  for (int u = 0; u < kTileArcs / kBlock; u++) {
+  for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
+#pragma unroll
+  for (int u = 0; u < U; u++) {
     const int e = u * kBlock + threadIdx.x;
-    if (e < na) prod[e] = (double)wv[u] * ld_z(p.z + j[u]);
+    if (e < na) prod[e] = (double)wv[u] * zj[u];
   }
   __syncthreads();
   double a = 0.0;
