@@ -32,7 +32,8 @@ bool is_device_ptr(const void *p) {
 
 void Layout::release(cudaStream_t st) {
   for (void *q : {(void *)perm, (void *)iperm, (void *)rp, (void *)col, (void *)w, (void *)d1,
-                  (void *)tasks, (void *)wtasks, (void *)d_phase_begin, (void *)d_wphase_begin})
+                  (void *)tasks, (void *)wtasks, (void *)d_phase_begin, (void *)d_wphase_begin,
+                  (void *)d_crow})
     if (q) cudaFreeAsync(q, st);
   perm = iperm = nullptr;
   rp = nullptr;
@@ -41,6 +42,8 @@ void Layout::release(cudaStream_t st) {
   d1 = nullptr;
   tasks = wtasks = nullptr;
   d_phase_begin = d_wphase_begin = nullptr;
+  d_crow = nullptr;
+  crow.clear();
   ntasks = nwtasks = 0;
   ncolors = 0;
   phase_begin.clear();

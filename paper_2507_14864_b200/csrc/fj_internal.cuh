@@ -76,6 +76,9 @@ struct Layout {
   std::vector<int> wphase_begin;  // host, ncolors + 1 entries (warp units)
   int *d_phase_begin = nullptr;   // device copies
   int *d_wphase_begin = nullptr;
+  std::vector<int64_t> crow;      // host: first row of each color; [ncolors] = first
+                                  // empty row; [ncolors + 1] = n
+  int64_t *d_crow = nullptr;      // device copy
   int npartials = 0;              // partial slots for long rows
   int64_t empty_rows = 0;
   int64_t active_rows = 0;        // rows with L > 0
@@ -98,6 +101,8 @@ struct fj_graph {
   double *deg = nullptr;
   fj::Layout async_layout;   // 1 color, rows grouped by class
   fj::Layout color_layout;   // lazily built for COLORED solves
+  fj::Layout push_layout;    // lazily built for PUSH (in-rows: scatter lists)
+  fj::Layout push_color_layout;
   int32_t *colors = nullptr; // color per original node (lazy)
   int ncolors = 0;
 };
@@ -108,7 +113,7 @@ fj_status transpose_in_csr(fj_graph *g, int64_t **ort, int32_t **ocol, float **o
 // layout.cu: sweep layout from the pull CSR (original ids)
 fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *ocol,
                                 const float *ow, const int32_t *color /* nullable */,
-                                int ncolors, Layout *L);
+                                int ncolors, Layout *L, bool need_d1 = false);
 // color.cu
 fj_status build_coloring(fj_graph *g);
 // memory helpers (api.cu)

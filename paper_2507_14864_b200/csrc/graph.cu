@@ -413,6 +413,8 @@ fj_status fj_graph_destroy(fj_graph_t g) {
     if (q) cudaFreeAsync(q, g->stream);
   g->async_layout.release(g->stream);
   g->color_layout.release(g->stream);
+  g->push_layout.release(g->stream);
+  g->push_color_layout.release(g->stream);
   cudaStreamSynchronize(g->stream);
   delete g;
   return FJ_OK;

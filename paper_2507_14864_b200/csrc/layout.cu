@@ -99,7 +99,8 @@ __global__ void k_task_arcs(int ntasks, const int64_t *__restrict__ rp, Task *__
 }
 
 fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *ocol,
-                                const float *ow, const int32_t *color, int ncolors, Layout *L) {
+                                const float *ow, const int32_t *color, int ncolors, Layout *L,
+                                bool need_d1) {
   cudaStream_t st = g->stream;
   const int64_t n = g->n, m = g->m;
   L->release(st);
@@ -137,7 +138,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   FJ_CUDA(cudaMallocAsync(&L->rp, sizeof(int64_t) * (n + 2), st));
   FJ_CUDA(cudaMallocAsync(&L->col, sizeof(int32_t) * (m + 8), st));
   if (ow) FJ_CUDA(cudaMallocAsync(&L->w, sizeof(float) * (m + 8), st));
-  if (g->weighted) FJ_CUDA(cudaMallocAsync(&L->d1, sizeof(double) * n, st));
+  if (g->weighted || need_d1) FJ_CUDA(cudaMallocAsync(&L->d1, sizeof(double) * n, st));
   fj::count_launch();
   k_perm<<<gridn(n), kBlock, 0, st>>>(n, k0, ort, L->perm, L->iperm, len);
   {
@@ -174,6 +175,9 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   std::vector<int64_t> gstart(ngroups + 1, 0);
   for (int q = 0; q < ngroups; q++) gstart[q + 1] = gstart[q] + (int64_t)hcount[q];
   L->empty_rows = (int64_t)hcount[ngroups - 1];
+  L->crow.assign(ncolors + 2, 0);
+  for (int c = 0; c <= ncolors; c++) L->crow[c] = gstart[c * kClasses];
+  L->crow[ncolors + 1] = n;
   L->active_rows = n - L->empty_rows;
 
   // work lists: tile tasks (classes 0..5) and warp units (classes 6, 7), each
@@ -246,6 +250,9 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
                           cudaMemcpyHostToDevice, st));
   FJ_CUDA(cudaMallocAsync(&L->d_wphase_begin, sizeof(int) * (ncolors + 1), st));
   FJ_CUDA(cudaMemcpyAsync(L->d_wphase_begin, L->wphase_begin.data(), sizeof(int) * (ncolors + 1),
+                          cudaMemcpyHostToDevice, st));
+  FJ_CUDA(cudaMallocAsync(&L->d_crow, sizeof(int64_t) * (ncolors + 2), st));
+  FJ_CUDA(cudaMemcpyAsync(L->d_crow, L->crow.data(), sizeof(int64_t) * (ncolors + 2),
                           cudaMemcpyHostToDevice, st));
   FJ_CUDA(cudaStreamSynchronize(st));  // host vectors above are stack-owned
   FJ_CUDA(cudaFreeAsync(k0, st));

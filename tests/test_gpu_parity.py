@@ -295,3 +295,26 @@ def test_full_lattice_step_1d(dev):
                                  omega, False)
         assert np.all(np.abs(z - zt) <= eps * np.maximum(np.abs(zt), SIG) + 6e-8 * np.abs(zt))
         g.close()
+
+
+# --------------------------------------------------- frontier push (row a3)
+@pytest.mark.parametrize("name", sorted(TINY))
+def test_tiny_push(dev, name):
+    """FJ_METHOD_PUSH (Alg. 1 data-parallel: pop phase + atomic scatter)."""
+    rp, col, w, s, directed = TINY[name]()
+    st, _, _ = check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="push")
+    assert st.relaxations > 0 and st.edge_updates > 0
+
+
+@pytest.mark.parametrize("name", ["er2000", "lattice64", "chunglu4k"])
+def test_tiny_push_sor_colored(dev, name):
+    """FJ_METHOD_PUSH with ω ≠ 1: Alg. 3 per color (pushes of one color commute)."""
+    rp, col, w, s, directed = TINY[name]()
+    check_parity(dev, rp, col, w, s, 1e-6, 1.5, directed, method="push")
+
+
+@pytest.mark.parametrize("hub_deg", [3000, 20000])
+def test_push_long_scatter_lists(dev, hub_deg):
+    n = hub_deg + 1
+    rp, col, w = G.in_csr_from_edges(n, [(0, i) for i in range(1, n)])
+    check_parity(dev, rp, col, w, fjgen.uniform(n, 9), 1e-6, 1.0, False, method="push")
