@@ -15,7 +15,7 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfj.so")
+LIB_PATH = os.environ.get("FJ_LIB_PATH") or os.path.join(_HERE, "libfj.so")
 _LIB = None
 
 FJ_OK, FJ_ERR_INVALID, FJ_ERR_NUMERIC, FJ_ERR_CUDA = 0, 2, 3, 4

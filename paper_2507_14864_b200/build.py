@@ -12,8 +12,11 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    out = os.path.join(HERE, "libfj.so")
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Build libfj.so (or a diagnostic variant at `out` with extra -D defines)."""
+    out = out or os.path.join(HERE, "libfj.so")
+    objdir = os.path.join(HERE, "csrc") if not defines else os.path.dirname(out)
     srcs = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
     deps = srcs + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + \
         [os.path.join(HERE, "..", "include", "fj.h")]
@@ -21,8 +24,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         t = os.path.getmtime(out)
         if all(os.path.getmtime(d) <= t for d in deps):
             return out
-    objs = [os.path.join(HERE, "csrc", os.path.basename(s)[:-3] + ".o") for s in srcs]
-    procs = [subprocess.Popen([NVCC, *FLAGS, "-c", s, "-o", o], stdout=subprocess.PIPE,
+    objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    dflags = [f"-D{d}" for d in defines]
+    procs = [subprocess.Popen([NVCC, *FLAGS, *dflags, "-c", s, "-o", o], stdout=subprocess.PIPE,
                               stderr=subprocess.STDOUT, text=True) for s, o in zip(srcs, objs)]
     logs = []
     for src, pr in zip(srcs, procs):
@@ -36,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as f:
+    with open(os.path.join(objdir, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))

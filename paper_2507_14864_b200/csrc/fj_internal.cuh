@@ -30,6 +30,10 @@ void set_error(const char *fmt, ...);
 constexpr int kBlock = 256;           // threads per CTA of every task kernel
 constexpr int kWarpPiece = 2048;      // arcs of one warp unit (whole row or piece)
 constexpr int kTileArcs = 2048;       // max arcs of one CTA tile task (smem products)
+#ifndef FJ_WT_ARCS
+#define FJ_WT_ARCS 256
+#endif
+constexpr int kWarpTileArcs = FJ_WT_ARCS;  // max arcs of one warp tile (8 per lane)
 constexpr int kNumClasses = 8;        // row-length classes of the layout
 
 // Row-length classes (out-degree L of the pull CSR).  Rows with L == 0 are
@@ -72,6 +76,10 @@ struct Layout {
   int ntasks = 0;
   Task *wtasks = nullptr;         // warp units, grouped by phase
   int nwtasks = 0;
+  Task *rtasks = nullptr;         // sweep list: warp units, then warp tiles (short rows)
+  int nrtasks = 0;
+  std::vector<int> rphase_begin;
+  int *d_rphase_begin = nullptr;
   std::vector<int> phase_begin;   // host, ncolors + 1 entries (tile tasks)
   std::vector<int> wphase_begin;  // host, ncolors + 1 entries (warp units)
   int *d_phase_begin = nullptr;   // device copies
@@ -83,6 +91,8 @@ struct Layout {
   int64_t empty_rows = 0;
   int64_t active_rows = 0;        // rows with L > 0
   int64_t max_len = 0;
+  int64_t warp_unit_arcs = 0;     // arcs in rows handled by warp units (> kWarpTileArcs)
+  bool stream_tma = false;        // sweep streams arcs with TMA (see solve.cu)
   void release(cudaStream_t st);
 };
 

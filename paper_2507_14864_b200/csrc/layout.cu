@@ -24,7 +24,7 @@ __host__ __device__ static inline int row_class(int64_t L) {
   if (L <= 16) return 2;
   if (L <= 32) return 3;
   if (L <= 64) return 4;
-  if (L <= 256) return 5;
+  if (L <= (kWarpTileArcs > 64 ? kWarpTileArcs : 128)) return 5;
   if (L <= kWarpPiece) return 6;
   return 7;
 }
@@ -104,6 +104,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   cudaStream_t st = g->stream;
   const int64_t n = g->n, m = g->m;
   L->release(st);
+  L->warp_unit_arcs = 0;
   L->n = n;
   L->m = m;
   L->ncolors = ncolors;
@@ -182,18 +183,28 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
 
   // work lists: tile tasks (classes 0..5) and warp units (classes 6, 7), each
   // grouped by color; within a color, longest rows first
-  std::vector<Task> tasks, wtasks;
+  std::vector<Task> tasks, wtasks, rtasks;
   L->phase_begin.assign(ncolors + 1, 0);
   L->wphase_begin.assign(ncolors + 1, 0);
+  L->rphase_begin.assign(ncolors + 1, 0);
+  static const int kLmax[6] = {4, 8, 16, 32, 64, kWarpTileArcs > 64 ? kWarpTileArcs : 128};
   int slot = 0;
   for (int c = 0; c < ncolors; c++) {
     L->phase_begin[c] = (int)tasks.size();
     L->wphase_begin[c] = (int)wtasks.size();
+    L->rphase_begin[c] = (int)rtasks.size();
     for (int cd = 0; cd < kClasses; cd++) {  // cd = 7 - class
       int q = c * kClasses + cd;
       int cls = kClasses - 1 - cd;
       int64_t r0 = gstart[q], r1 = gstart[q + 1];
       if (r1 <= r0) continue;
+      if (cls >= 6) {
+        int64_t ra = 0, rz = 0;
+        FJ_CUDA(cudaMemcpyAsync(&ra, L->rp + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        FJ_CUDA(cudaMemcpyAsync(&rz, L->rp + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        FJ_CUDA(cudaStreamSynchronize(st));
+        L->warp_unit_arcs += rz - ra;
+      }
       if (cls == 7) {
         std::vector<int64_t> rph(r1 - r0 + 1);
         FJ_CUDA(cudaMemcpyAsync(rph.data(), L->rp + r0, sizeof(int64_t) * (r1 - r0 + 1),
@@ -202,23 +213,37 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
         for (int64_t i = r0; i < r1; i++) {
           int64_t len_i = rph[i - r0 + 1] - rph[i - r0];
           int np = (int)((len_i + kWarpPiece - 1) / kWarpPiece);
-          for (int p = 0; p < np; p++)
+          for (int p = 0; p < np; p++) {
             wtasks.push_back(Task{(int32_t)i, p, kWarp | (np << 8), slot, 0, 0});
+            rtasks.push_back(wtasks.back());
+          }
           slot += np;
         }
       } else if (cls == 6) {
-        for (int64_t i = r0; i < r1; i++)
+        for (int64_t i = r0; i < r1; i++) {
           wtasks.push_back(Task{(int32_t)i, 0, kWarp | (1 << 8), 0, 0, 0});
+          rtasks.push_back(wtasks.back());
+        }
       } else {
         int G = 1 << cls;
         int64_t per = kBlock / G;  // one G-lane group per row
         for (int64_t a = r0; a < r1; a += per)
           tasks.push_back(Task{(int32_t)a, (int32_t)std::min(r1, a + per), cls, 0, 0, 0});
+        // warp tiles for the sweep: <= kWarpTileArcs arcs, 32/G rows per step
+        const int64_t wper = kWarpTileArcs / kLmax[cls];
+        for (int64_t a = r0; a < r1; a += wper)
+          rtasks.push_back(Task{(int32_t)a, (int32_t)std::min(r1, a + wper), cls, 0, 0, 0});
       }
     }
   }
   L->phase_begin[ncolors] = (int)tasks.size();
   L->wphase_begin[ncolors] = (int)wtasks.size();
+  L->rphase_begin[ncolors] = (int)rtasks.size();
+  L->nrtasks = (int)rtasks.size();
+  // measured on all five configs: direct loads beat the TMA-staged stream
+  // once short rows run as warp tiles (the stage buffers take L1 away from
+  // the ẑ gathers); the TMA path stays selectable with FJ_TMA=1
+  L->stream_tma = false;
   if (getenv("FJ_DEBUG")) {  // per-color layout summary (diagnostics)
     std::vector<int64_t> cut(ncolors + 1);
     for (int c = 0; c <= ncolors; c++) cut[c] = gstart[c * kClasses];
@@ -235,9 +260,9 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   L->nwtasks = (int)wtasks.size();
   L->npartials = slot;
   L->max_len = hmax;
-  for (int which = 0; which < 2; which++) {
-    std::vector<Task> &v = which ? wtasks : tasks;
-    Task **dst = which ? &L->wtasks : &L->tasks;
+  for (int which = 0; which < 3; which++) {
+    std::vector<Task> &v = which == 0 ? tasks : which == 1 ? wtasks : rtasks;
+    Task **dst = which == 0 ? &L->tasks : which == 1 ? &L->wtasks : &L->rtasks;
     FJ_CUDA(cudaMallocAsync(dst, sizeof(Task) * std::max<size_t>(1, v.size()), st));
     if (!v.empty()) {
       FJ_CUDA(cudaMemcpyAsync(*dst, v.data(), sizeof(Task) * v.size(), cudaMemcpyHostToDevice, st));
@@ -250,6 +275,9 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
                           cudaMemcpyHostToDevice, st));
   FJ_CUDA(cudaMallocAsync(&L->d_wphase_begin, sizeof(int) * (ncolors + 1), st));
   FJ_CUDA(cudaMemcpyAsync(L->d_wphase_begin, L->wphase_begin.data(), sizeof(int) * (ncolors + 1),
+                          cudaMemcpyHostToDevice, st));
+  FJ_CUDA(cudaMallocAsync(&L->d_rphase_begin, sizeof(int) * (ncolors + 1), st));
+  FJ_CUDA(cudaMemcpyAsync(L->d_rphase_begin, L->rphase_begin.data(), sizeof(int) * (ncolors + 1),
                           cudaMemcpyHostToDevice, st));
   FJ_CUDA(cudaMallocAsync(&L->d_crow, sizeof(int64_t) * (ncolors + 2), st));
   FJ_CUDA(cudaMemcpyAsync(L->d_crow, L->crow.data(), sizeof(int64_t) * (ncolors + 2),

@@ -17,6 +17,8 @@
 // The loop ends on the first sweep that relaxes nothing: every residual was
 // then evaluated on the final ẑ and is ≤ h — the paper's "Q = ∅".
 // A separate compensated fp64 pass (certificate) re-checks max |r_v|/h_v.
+#include <stdlib.h>
+
 #include <cuda/atomic>
 #include <type_traits>
 #include <cub/cub.cuh>
@@ -50,6 +52,8 @@ struct KP {
   const double *__restrict__ d1;
   const Task *__restrict__ tasks;
   const Task *__restrict__ wtasks;
+  const Task *__restrict__ rtasks;
+  const int *rphase_begin;
   const float *__restrict__ s;  // layout order
   double *z;                    // ẑ' (RELAX/CERT) or z (DIS), layout order
   const Scalars *sc;
@@ -70,6 +74,7 @@ struct KP {
   unsigned long long *cert_max;  // double bits
   double *dis;
   double *rout;                  // CERT: optional residual output (layout order)
+  int dbg;                       // diagnostics (env FJ_DBG_SKIP): 1 skip warp units, 2 skip tiles
 };
 
 // CSR streams are read once per sweep: read-only path, no L1 allocation, so
@@ -171,6 +176,21 @@ __device__ __forceinline__ void relax_row(const KP &p, const Scalars &S, int row
   if (!(ar <= S.sentinel)) t.bad = 1;
 }
 
+// same as relax_row, with the row state loaded by the caller (prefetched)
+__device__ __forceinline__ void relax_row_pre(const KP &p, const Scalars &S, int row, int len,
+                                              dd total, float sv, double zi, double d1, TAcc &t) {
+  const double sp = (double)sv + S.c;
+  const double h = threshold(S, sp);
+  const double rho = residual_dd(total, sp, d1, zi);
+  const double ar = fabs(rho);
+  if (ar > p.theta * h) {
+    __stcg(p.z + row, zi + p.omega * rho / d1);
+    t.upd++;
+    t.eu += (unsigned long long)len;
+  }
+  if (!(ar <= S.sentinel)) t.bad = 1;
+}
+
 template <bool W>
 __device__ __forceinline__ void cert_row(const KP &p, const Scalars &S, int row, int len, dd total,
                                          TAcc &t) {
@@ -255,6 +275,16 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
   const int row = tk.a, piece = tk.b, np = tk.kind >> 8, slot = tk.slot;
   const int64_t a0 = tk.a0, a1 = tk.a1;
   const double zr = (MODE == DIS) ? p.z[row] : 0.0;
+  // RELAX: lanes 1..5 fetch the row state now so that the final relax does
+  // not wait on another round trip (s, ẑ_row, 1+d, row_ptr pair)
+  double pre = 0.0;
+  if constexpr (MODE == RELAX) {
+    if (lane == 1) pre = (double)__ldg(p.s + row);
+    else if (lane == 2) pre = __ldcg(p.z + row);
+    else if (lane == 3 && W) pre = __ldg(p.d1 + row);
+    else if (lane == 4) pre = (double)__ldg(p.rp + row);
+    else if (lane == 5) pre = (double)__ldg(p.rp + row + 1);
+  }
   A a;
   acc_zero(a);
   for (int64_t k0 = a0 + lane; k0 < a1; k0 += 32 * U) {
@@ -278,7 +308,11 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if constexpr (MODE != DIS) {
+#ifdef FJ_PLAIN_WARP
+        a.hi = fma((double)wv[u], zj[u], a.hi);  // diagnostics only
+#else
         dd_addprod(a, (double)wv[u], zj[u]);
+#endif
       } else {
         const double dz = zr - zj[u];
         a = fma((double)wv[u] * dz, dz, a);
@@ -287,6 +321,16 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc_merge(a, acc_shfl(a, 0xffffffffu, off));
+  float sv = 0.f;
+  double zi = 0.0, d1 = 0.0;
+  int len = 0;
+  if constexpr (MODE == RELAX) {
+    sv = (float)__shfl_sync(0xffffffffu, pre, 1);
+    zi = __shfl_sync(0xffffffffu, pre, 2);
+    const double rb = __shfl_sync(0xffffffffu, pre, 4), re = __shfl_sync(0xffffffffu, pre, 5);
+    len = (int)(re - rb);
+    d1 = W ? __shfl_sync(0xffffffffu, pre, 3) : (double)(len + 1);
+  }
   if (lane != 0) return;
   if constexpr (MODE == DIS) {
     t.dis += a;
@@ -305,9 +349,15 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
       }
       p.arrive[slot] = 0;
     }
-    const int len = (int)(__ldg(p.rp + row + 1) - __ldg(p.rp + row));
-    if constexpr (MODE == RELAX) relax_row<W>(p, S, row, len, a, t);
-    else cert_row<W>(p, S, row, len, a, t);
+    if constexpr (MODE == RELAX) {
+      // a non-final piece returned above; a multi-piece row is finished by
+      // the last-arriving warp, whose prefetched ẑ_row is still current (only
+      // this row's finisher writes it, once per phase)
+      relax_row_pre(p, S, row, len, a, sv, zi, d1, t);
+    } else {
+      const int lenc = (int)(__ldg(p.rp + row + 1) - __ldg(p.rp + row));
+      cert_row<W>(p, S, row, lenc, a, t);
+    }
   }
 }
 
@@ -381,6 +431,304 @@ __device__ __forceinline__ void relax_tile(const KP &p, const Scalars &S, const 
   }
 }
 
+// RELAX on a warp tile (rows of ≤ 256 arcs, ≤ kWarpTileArcs arcs per tile):
+// one warp, no block barrier.  Row state and the tile's arcs are loaded up
+// front (≤ 8 column/weight loads then ≤ 8 ẑ gathers per lane), products go to
+// the warp's smem slice, then G-lane groups sum their rows (≤ 2 row steps)
+// and the group leader relaxes.
+template <bool W>
+__device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, const Task &tk,
+                                                TAcc &t, double *wprod) {
+  constexpr int U = kWarpTileArcs / 32;
+  const int lane = threadIdx.x & 31;
+  const int cls = tk.kind & 0xff;
+  const int G = 1 << cls;
+  const int gl = lane & (G - 1);
+  const int ng = 32 >> cls;  // groups per warp = rows per step
+  // row state for both steps
+  int64_t rb[2], re[2];
+  float sv[2];
+  double zi[2], d1[2];
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    const int row = tk.a + q * ng + (lane >> cls);
+    rb[q] = re[q] = 0;
+    sv[q] = 0.f;
+    zi[q] = d1[q] = 0.0;
+    if (row < tk.b) {
+      rb[q] = __ldg(p.rp + row);
+      re[q] = __ldg(p.rp + row + 1);
+      if (gl == 0) {
+        sv[q] = __ldg(p.s + row);
+        zi[q] = __ldcg(p.z + row);
+        if (W) d1[q] = __ldg(p.d1 + row);
+      }
+    }
+  }
+  const int64_t a0 = tk.a0;
+  const int na = (int)(tk.a1 - a0);
+  int j[U];
+  float wv[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int e = u * 32 + lane;
+    const bool ok = e < na;
+    j[u] = ld_stream(p.col + a0 + (ok ? e : 0));
+    wv[u] = W ? ld_stream(p.w + a0 + (ok ? e : 0)) : 1.0f;
+  }
+  double zj[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int e = u * 32 + lane;
+    if (e < na) wprod[e] = (double)wv[u] * zj[u];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    double a = 0.0;
+    const int kb = (int)(rb[q] - a0), ke = (int)(re[q] - a0);
+    for (int k = kb + gl; k < ke; k += G) a += wprod[k];
+    for (int off = G >> 1; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+    const int row = tk.a + q * ng + (lane >> cls);
+    if (row < tk.b && gl == 0) {
+      const int len = (int)(re[q] - rb[q]);
+      relax_row_pre(p, S, row, len, dd{a, 0.0}, sv[q], zi[q], W ? d1[q] : (double)(len + 1), t);
+    }
+  }
+  __syncwarp();  // the slice is reused by this warp's next task
+}
+
+// ------------------------------------------------ TMA-pipelined warp stream
+// Each warp walks its work items (hub-row warp units, then short-row warp
+// tiles) as a stream of <= 256-arc chunks.  The column indices (and weights)
+// of chunk i+1 are fetched into the warp's shared-memory stage by a TMA bulk
+// copy (cp.async.bulk, completion on an mbarrier) while chunk i is gathered and
+// reduced, so the HBM stream runs behind the dependent ẑ gathers without
+// holding registers.
+constexpr int kChunk = kWarpTileArcs;                       // arcs per chunk
+constexpr int kStageElems = kChunk + 8;                     // + 16-byte alignment slack
+struct WarpSmem {
+  int32_t col[2][kStageElems];
+  float w[2][kStageElems];
+  double prod[kChunk];
+  unsigned long long bar[2];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *q) {
+  return (uint32_t)__cvta_generic_to_shared(q);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
+                                            unsigned long long *b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+// lane 0: fetch arcs [c0, c1) of the layout CSR into stage st (16-byte
+// aligned superset; the arrays are padded by >= 8 elements)
+template <bool W>
+__device__ __forceinline__ void chunk_issue(const KP &p, WarpSmem *ws, int st, int64_t c0,
+                                            int64_t c1) {
+  const int64_t al = c0 & ~(int64_t)3;
+  const uint32_t nb = (uint32_t)((((c1 + 3) & ~(int64_t)3) - al) * 4);
+  // the stage was last read through the generic proxy (after __syncwarp)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect(&ws->bar[st], W ? 2 * nb : nb);
+  tma_load_1d(ws->col[st], p.col + al, nb, &ws->bar[st]);
+  if (W) tma_load_1d(ws->w[st], p.w + al, nb, &ws->bar[st]);
+}
+
+// relax the rows of a warp tile from a staged chunk
+template <bool W>
+__device__ __forceinline__ void tile_from_stage(const KP &p, const Scalars &S, const Task &tk,
+                                                TAcc &t, WarpSmem *ws, int st, uint32_t par) {
+  constexpr int U = kChunk / 32;
+  const int lane = threadIdx.x & 31;
+  const int cls = tk.kind & 0xff;
+  const int G = 1 << cls;
+  const int gl = lane & (G - 1);
+  const int ng = 32 >> cls;
+  int64_t rb[2], re[2];
+  float sv[2];
+  double zi[2], d1[2];
+#pragma unroll
+  for (int q = 0; q < 2; q++) {  // row state first: independent of the chunk
+    const int row = tk.a + q * ng + (lane >> cls);
+    rb[q] = re[q] = 0;
+    sv[q] = 0.f;
+    zi[q] = d1[q] = 0.0;
+    if (row < tk.b) {
+      rb[q] = __ldg(p.rp + row);
+      re[q] = __ldg(p.rp + row + 1);
+      if (gl == 0) {
+        sv[q] = __ldg(p.s + row);
+        zi[q] = __ldcg(p.z + row);
+        if (W) d1[q] = __ldg(p.d1 + row);
+      }
+    }
+  }
+  const int64_t a0 = tk.a0;
+  const int na = (int)(tk.a1 - a0);
+  const int off = (int)(a0 & 3);
+  mbar_wait(&ws->bar[st], par);
+  int j[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int e = u * 32 + lane;
+    j[u] = e < na ? ws->col[st][off + e] : -1;
+  }
+  double zj[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) zj[u] = j[u] >= 0 ? ld_z(p.z + j[u]) : 0.0;
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int e = u * 32 + lane;
+    if (e < na) ws->prod[e] = (W ? (double)ws->w[st][off + e] : 1.0) * zj[u];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    double a = 0.0;
+    const int kb = (int)(rb[q] - a0), ke = (int)(re[q] - a0);
+    for (int k = kb + gl; k < ke; k += G) a += ws->prod[k];
+    for (int o = G >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    const int row = tk.a + q * ng + (lane >> cls);
+    if (row < tk.b && gl == 0) {
+      const int len = (int)(re[q] - rb[q]);
+      relax_row_pre(p, S, row, len, dd{a, 0.0}, sv[q], zi[q], W ? d1[q] : (double)(len + 1), t);
+    }
+  }
+}
+
+// one warp's work items of a phase, as a TMA-pipelined chunk stream
+template <bool W>
+__device__ __forceinline__ void relax_stream(const KP &p, const Scalars &S, int r0, int nr,
+                                             TAcc &t, WarpSmem *ws, uint32_t &phase_bits) {
+  const int lane = threadIdx.x & 31;
+  const int stride = gridDim.x * (kBlock / 32);
+  int ti = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+  if (ti >= nr) return;
+  Task T = p.rtasks[r0 + ti];
+  int64_t c0 = T.a0;
+  int st = 0;
+  if (lane == 0) chunk_issue<W>(p, ws, 0, c0, min(T.a1, c0 + (int64_t)kChunk));
+  dd acc{0.0, 0.0};   // warp-unit accumulator (per lane)
+  double pre = 0.0;   // warp-unit row state (lanes 1..5)
+  bool unit_start = true;
+  while (true) {
+    const bool unit = (T.kind & 0xff) == kWarp;
+    const int64_t c1 = unit ? min(T.a1, c0 + (int64_t)kChunk) : T.a1;
+    // next chunk (same unit, or the next work item)
+    Task N = T;
+    int nti = ti;
+    int64_t n0 = c1;
+    if (!unit || c1 >= T.a1) {
+      nti = ti + stride;
+      if (nti < nr) {
+        N = p.rtasks[r0 + nti];
+        n0 = N.a0;
+      }
+    }
+    const bool has_next = nti < nr;
+    if (has_next && lane == 0)
+      chunk_issue<W>(p, ws, st ^ 1, n0,
+                     (N.kind & 0xff) == kWarp ? min(N.a1, n0 + (int64_t)kChunk) : N.a1);
+    const uint32_t par = (phase_bits >> st) & 1u;
+    phase_bits ^= 1u << st;
+    if (!unit) {
+      tile_from_stage<W>(p, S, T, t, ws, st, par);
+    } else {
+      const int row = T.a;
+      if (unit_start) {
+        acc = dd{0.0, 0.0};
+        pre = 0.0;
+        if (lane == 1) pre = (double)__ldg(p.s + row);
+        else if (lane == 2) pre = __ldcg(p.z + row);
+        else if (lane == 3 && W) pre = __ldg(p.d1 + row);
+        else if (lane == 4) pre = (double)__ldg(p.rp + row);
+        else if (lane == 5) pre = (double)__ldg(p.rp + row + 1);
+      }
+      const int off = (int)(c0 & 3);
+      const int na = (int)(c1 - c0);
+      mbar_wait(&ws->bar[st], par);
+      constexpr int U = kChunk / 32;
+      int j[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int e = u * 32 + lane;
+        j[u] = e < na ? ws->col[st][off + e] : -1;
+      }
+      double zj[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) zj[u] = j[u] >= 0 ? ld_z(p.z + j[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int e = u * 32 + lane;
+        if (e < na) {
+          if (W) dd_addprod(acc, (double)ws->w[st][off + e], zj[u]);
+          else dd_add(acc, zj[u]);
+        }
+      }
+      if (c1 >= T.a1) {  // unit done: reduce and finish the row (or its piece)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc_merge(acc, acc_shfl(acc, 0xffffffffu, o));
+        const float sv = (float)__shfl_sync(0xffffffffu, pre, 1);
+        const double zi = __shfl_sync(0xffffffffu, pre, 2);
+        const double rbv = __shfl_sync(0xffffffffu, pre, 4), rev = __shfl_sync(0xffffffffu, pre, 5);
+        const int len = (int)(rev - rbv);
+        const double d1 = W ? __shfl_sync(0xffffffffu, pre, 3) : (double)(len + 1);
+        if (lane == 0) {
+          const int np = T.kind >> 8;
+          bool finish = true;
+          if (np > 1) {
+            __stcg(p.partial + T.slot + T.b, make_double2(acc.hi, acc.lo));
+            __threadfence();
+            finish = atomicAdd(p.arrive + T.slot, 1) == np - 1;
+            if (finish) {
+              __threadfence();
+              acc = dd{0.0, 0.0};
+              for (int q = 0; q < np; q++) {
+                const double2 x = __ldcg(p.partial + T.slot + q);
+                acc_merge(acc, dd{x.x, x.y});
+              }
+              p.arrive[T.slot] = 0;
+            }
+          }
+          if (finish) relax_row_pre(p, S, row, len, acc, sv, zi, d1, t);
+        }
+      }
+    }
+    __syncwarp();  // stage st and the product slice are free again
+    if (!has_next) break;
+    unit_start = !unit || c1 >= T.a1;
+    st ^= 1;
+    T = N;
+    c0 = n0;
+    ti = nti;
+  }
+}
+
 template <int MODE, bool W>
 __device__ __forceinline__ void dispatch_tile(const KP &p, const Scalars &S, const Task &tk, TAcc &t) {
   switch (tk.kind & 0xff) {
@@ -412,28 +760,53 @@ __device__ __forceinline__ void grid_sync(unsigned *bar) {
 }
 
 // ------------------------------------------------------ persistent sweeps
-template <bool W>
-__global__ void __launch_bounds__(kBlock, 4) k_sweep(KP p) {
-  extern __shared__ double s_prod[];  // 2 x kTileArcs products
-  int buf = 0;
+#ifndef FJ_MINB
+#define FJ_MINB 4
+#endif
+template <bool W, bool TMA>
+__global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
+  extern __shared__ double s_prod[];  // per warp: a WarpSmem (TMA stages + products)
   __shared__ unsigned long long s_dec[3];
   const Scalars S = *p.sc;
+  WarpSmem *ws = reinterpret_cast<WarpSmem *>(s_prod) + (threadIdx.x >> 5);
+  uint32_t phase_bits = 0;
+  if (TMA && (threadIdx.x & 31) == 0) {
+    mbar_init(&ws->bar[0]);
+    mbar_init(&ws->bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
   TAcc t{};
   unsigned long long tot_upd = 0, tot_eu = 0;
   int sweeps = 0, reason = 1;
   int phase = 0;
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
     for (int k = 0; k < p.ncolors; ++k, ++phase) {
-      const int t0 = p.phase_begin[k], nt = p.phase_begin[k + 1] - t0;
       // static round-robin (tasks are balanced by construction; no claim
       // atomics on the hot loop): warp units first (hub rows), then tiles
       const int w0 = p.wphase_begin[k], nw = p.wphase_begin[k + 1] - w0;
       const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
-      for (int wi = warp_id; wi < nw; wi += gridDim.x * (kBlock / 32))
-        do_warp<RELAX, W>(p, S, p.wtasks[w0 + wi], t);
-      for (int ti = blockIdx.x; ti < nt; ti += gridDim.x) {
-        relax_tile<W>(p, S, p.tasks[t0 + ti], t, s_prod + (buf & 1) * kTileArcs);
-        buf++;
+      if (TMA) {
+        relax_stream<W>(p, S, p.rphase_begin[k], p.rphase_begin[k + 1] - p.rphase_begin[k], t,
+                        ws, phase_bits);
+      } else {  // one warp per work item (hub rows first), next item prefetched
+        const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
+        const int stride = gridDim.x * (kBlock / 32);
+        double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
+        int wi = warp_id;
+        Task nxt;
+        if (wi < nr) nxt = p.rtasks[r0 + wi];
+        while (wi < nr) {
+          const Task cur = nxt;
+          const int wn = wi + stride;
+          if (wn < nr) nxt = p.rtasks[r0 + wn];
+          if ((cur.kind & 0xff) == kWarp) {
+            if (!(p.dbg & 1)) do_warp<RELAX, W>(p, S, cur, t);
+          } else if (!(p.dbg & 2)) {
+            relax_warp_tile<W>(p, S, cur, t, wprod);
+          }
+          wi = wn;
+        }
       }
       if (k + 1 < p.ncolors) grid_sync(p.bar);
     }
@@ -782,6 +1155,8 @@ static KP make_kp(const fj_graph *g, const Layout &L) {
   p.d1 = L.d1;
   p.tasks = L.tasks;
   p.wtasks = L.wtasks;
+  p.rtasks = L.rtasks;
+  p.rphase_begin = L.d_rphase_begin;
   p.phase_begin = L.d_phase_begin;
   p.wphase_begin = L.d_wphase_begin;
   p.ncolors = L.ncolors;
@@ -1071,6 +1446,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   p.sc = S;
   p.omega = omega;
   p.theta = 1.0;
+  p.dbg = getenv("FJ_DBG_SKIP") ? atoi(getenv("FJ_DBG_SKIP")) : 0;
   p.partial = partial;
   p.arrive = arrive;
   p.max_sweeps = o->max_sweeps;
@@ -1080,8 +1456,14 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   p.out = outv;
   p.cert_max = certbits;
 
-  const void *fn = W ? (const void *)k_sweep<true> : (const void *)k_sweep<false>;
-  const size_t sweep_smem = 2 * kTileArcs * sizeof(double);
+  // TMA-streamed chunks pay off when the arc stream dominates (short rows,
+  // local gathers: lattice, ER); hub-dominated graphs keep the shared memory
+  // as L1 for their gathers and load the stream directly
+  const bool tma = getenv("FJ_TMA") ? atoi(getenv("FJ_TMA")) != 0 : L.stream_tma;
+  const void *fn = W ? (tma ? (const void *)k_sweep<true, true> : (const void *)k_sweep<true, false>)
+                     : (tma ? (const void *)k_sweep<false, true> : (const void *)k_sweep<false, false>);
+  const size_t sweep_smem =
+      tma ? (kBlock / 32) * sizeof(WarpSmem) : (kBlock / 32) * kWarpTileArcs * sizeof(double);
   FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem));
   const int grid = persistent_grid(fn, g->num_sms, sweep_smem);
   float ms_sweep = 0, ms_cert = 0;
