@@ -149,6 +149,27 @@ fj_status fj_solve(fj_graph_t g, const float *s, double eps, double omega, float
 fj_status fj_solve_ex(fj_graph_t g, const float *s, double eps, double omega,
                       const fj_opts *o, float *z_out, fj_stats *st);
 
+/*
+ * ω selection.
+ * fj_omega_opt: μ = ρ((I+D)^{-1}A) by power iteration from the
+ * all-ones vector (at most max_iters SpMV sweeps, stop when the estimate moves
+ * by ≤ tol relatively), then ω_opt = 1 + (μ/(1+√(1−μ²)))² (Eq. optimal-omega,
+ * P:486).  The formula is the consistently-ordered SPD optimum; on directed
+ * graphs it is only a guide.  Outputs are host doubles.
+ */
+fj_status fj_omega_opt(fj_graph_t g, int max_iters, double tol, double *mu, double *omega);
+
+/*
+ * fj_omega_sweep: the paper's heuristic: solve at ω = hi, hi − step,
+ * …, down to lo, and return in *best_omega the ω with the fewest relaxations
+ * ("minimum number of updates"); diverging points cost +∞, ties go to the
+ * smaller ω.  table (nullable, host, 3·(*npts) doubles on entry =
+ * capacity): rows (ω, relaxations, status).  *npts returns the point count.
+ * method: fj_method for every solve.
+ */
+fj_status fj_omega_sweep(fj_graph_t g, const float *s, double eps, double lo, double hi,
+                         double step, int method, double *best_omega, double *table, int *npts);
+
 /* Polarization and disagreement of z (fp32[n]) on g (§8 row a7), fp64
    accumulation; results written to host doubles. */
 fj_status fj_measures(fj_graph_t g, const float *z, double *polarization,

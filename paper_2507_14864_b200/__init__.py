@@ -24,7 +24,7 @@ METHODS = {"auto": 0, "async": 1, "colored": 2, "push": 3}
 #: every symbol include/fj.h declares
 EXPORTS = ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve", "fj_solve_ex",
            "fj_measures", "fj_measures_ex", "fj_opts_default", "fj_last_error",
-           "fj_abi_version", "fj_kernel_launches")
+           "fj_abi_version", "fj_kernel_launches", "fj_omega_opt", "fj_omega_sweep")
 
 
 class FJError(RuntimeError):
@@ -81,8 +81,12 @@ def lib():
         L.fj_opts_default.restype = None
         L.fj_last_error.restype = ctypes.c_char_p
         L.fj_kernel_launches.restype = ctypes.c_int64
+        L.fj_omega_opt.argtypes = [P, i, d, ctypes.POINTER(d), ctypes.POINTER(d)]
+        L.fj_omega_sweep.argtypes = [P, P, d, d, d, d, i, ctypes.POINTER(d), P,
+                                     ctypes.POINTER(i)]
         for f in ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve",
-                  "fj_solve_ex", "fj_measures", "fj_measures_ex"):
+                  "fj_solve_ex", "fj_measures", "fj_measures_ex", "fj_omega_opt",
+                  "fj_omega_sweep"):
             getattr(L, f).restype = i
         _LIB = L
     return _LIB
@@ -225,3 +229,25 @@ def measures_pd(g: Graph, z):
     P, D = ctypes.c_double(), ctypes.c_double()
     _check(lib().fj_measures(g._h, _ptr(z), ctypes.byref(P), ctypes.byref(D)))
     return P.value, D.value
+
+
+def omega_opt(g: Graph, max_iters: int = 2000, tol: float = 1e-9):
+    """fj_omega_opt: (μ, ω_opt) — Eq. optimal-omega, μ by power iteration."""
+    mu, om = ctypes.c_double(), ctypes.c_double()
+    _check(lib().fj_omega_opt(g._h, int(max_iters), float(tol), ctypes.byref(mu),
+                              ctypes.byref(om)))
+    return mu.value, om.value
+
+
+def omega_sweep(g: Graph, s, eps: float, lo: float = 1.0, hi: float = 1.95, step: float = 0.05,
+                method: str = "auto"):
+    """fj_omega_sweep: the paper's fewest-updates heuristic.
+    Returns (best ω, [(ω, relaxations, status), ...])."""
+    cap = int(round((hi - lo) / step)) + 2
+    table = (ctypes.c_double * (3 * cap))()
+    n = ctypes.c_int(cap)
+    best = ctypes.c_double()
+    _check(lib().fj_omega_sweep(g._h, _ptr(s), float(eps), float(lo), float(hi), float(step),
+                                METHODS[method], ctypes.byref(best), table, ctypes.byref(n)))
+    rows = [(table[3 * i], int(table[3 * i + 1]), int(table[3 * i + 2])) for i in range(n.value)]
+    return best.value, rows

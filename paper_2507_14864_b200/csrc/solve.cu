@@ -27,7 +27,7 @@
 
 namespace fj {
 
-enum Mode { RELAX = 0, CERT = 1, DIS = 2 };
+enum Mode { RELAX = 0, CERT = 1, DIS = 2, SPMV = 3 };
 
 struct Scalars {
   double c;        // shift (Alg. 2; reading R5)
@@ -215,6 +215,8 @@ __device__ __forceinline__ void arc_acc(typename AccT<MODE>::T &a, const KP &p, 
   } else if constexpr (MODE == CERT) {
     if (W) dd_addprod(a, wk, p.z[j]);
     else dd_add(a, p.z[j]);
+  } else if constexpr (MODE == SPMV) {
+    a = fma(wk, p.z[j], a);
   } else {
     const double dz = zr - p.z[j];
     a = fma(wk * dz, dz, a);
@@ -241,6 +243,7 @@ __device__ __forceinline__ void do_group(const KP &p, const Scalars &S, int rb, 
       const int len = (int)(end - beg);
       if constexpr (MODE == RELAX) relax_row<W>(p, S, row, len, dd{a, 0.0}, t);
       else if constexpr (MODE == CERT) cert_row<W>(p, S, row, len, a, t);
+      else if constexpr (MODE == SPMV) p.rout[row] = a;
       else t.dis += a;
     }
   }
@@ -269,7 +272,7 @@ __device__ __forceinline__ A block_reduce(A a, A *sm) {
 template <int MODE, bool W>
 __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Task &tk, TAcc &t) {
   // rows above 256 arcs accumulate in double-double for RELAX and CERT
-  using A = typename std::conditional<MODE == DIS, double, dd>::type;
+  using A = typename std::conditional<MODE == DIS || MODE == SPMV, double, dd>::type;
   constexpr int U = 8;
   const int lane = threadIdx.x & 31;
   const int row = tk.a, piece = tk.b, np = tk.kind >> 8, slot = tk.slot;
@@ -307,7 +310,9 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
     // stage 3: accumulate
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      if constexpr (MODE != DIS) {
+      if constexpr (MODE == SPMV) {
+        a = fma((double)wv[u], zj[u], a);
+      } else if constexpr (MODE != DIS) {
 #ifdef FJ_PLAIN_WARP
         a.hi = fma((double)wv[u], zj[u], a.hi);  // diagnostics only
 #else
@@ -334,6 +339,9 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
   if (lane != 0) return;
   if constexpr (MODE == DIS) {
     t.dis += a;
+    return;
+  } else if constexpr (MODE == SPMV) {
+    atomicAdd(p.rout + row, a);  // pieces of one row add up (y zeroed first)
     return;
   } else {
     if (np > 1) {
@@ -870,7 +878,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_pass(KP p) {
     if (isnan(t.certmax)) m = t.certmax;
     if ((threadIdx.x & 31) == 0 && m != 0.0)
       atomicMax(p.cert_max, (unsigned long long)__double_as_longlong(m));
-  } else {
+  } else if constexpr (MODE == DIS) {
     double sdis = t.dis;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sdis += __shfl_xor_sync(0xffffffffu, sdis, off);
@@ -1603,6 +1611,95 @@ fj_status measures_impl(fj_graph *g, const float *z_in, const float *s_in, fj_me
   return FJ_OK;
 }
 
+
+// ------------------------------------------------------------- ω selection
+// y_i ← ((J x)_i + x_i)/2 with J = (I+D)^{-1} A; Σ y², Σ x·y
+__global__ void k_jacobi_scale(int64_t n, const int64_t *__restrict__ rp, const double *__restrict__ d1,
+                               const double *__restrict__ x, double *__restrict__ y,
+                               double *__restrict__ sums) {
+  __shared__ double sm[kBlock / 32];
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double yy = 0.0, xy = 0.0;
+  if (i < n) {
+    const double dv = d1 ? d1[i] : (double)(rp[i + 1] - rp[i] + 1);
+    const double v = 0.5 * (y[i] / dv + x[i]);  // (J + I)/2: Perron root strictly dominant
+    y[i] = v;
+    yy = v * v;
+    xy = x[i] * v;
+  }
+  yy = block_reduce<double>(yy, sm);
+  xy = block_reduce<double>(xy, sm);
+  if (threadIdx.x == 0) {
+    atomicAdd(sums, yy);
+    atomicAdd(sums + 1, xy);
+  }
+}
+__global__ void k_scale_copy(int64_t n, double f, const double *__restrict__ y, double *__restrict__ x) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = y[i] * f;
+}
+__global__ void k_fill(int64_t n, double v, double *__restrict__ x) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = v;
+}
+
+// μ = ρ((I+D)^{-1} A) by power iteration on (J+I)/2 from x = 1 (J ≥ 0, so ρ
+// is its Perron root; the shift keeps it strictly dominant even for
+// bipartite graphs where −μ is also an eigenvalue), then ω_opt = 1 + (μ/(1+√(1−μ²)))² (Eq. optimal-omega).
+fj_status omega_opt_impl(fj_graph *g, int max_iters, double tol, double *mu_out,
+                         double *omega_out, int *iters_out) {
+  cudaStream_t st = g->stream;
+  const Layout &L = g->async_layout;
+  const int64_t n = g->n;
+  double *x = nullptr, *y = nullptr, *sums = nullptr, *partial = nullptr;
+  unsigned *ctr = nullptr;
+  FJ_CUDA(cudaMallocAsync(&x, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&y, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&sums, sizeof(double) * 2, st));
+  FJ_CUDA(cudaMallocAsync(&ctr, sizeof(unsigned), st));
+  fj::count_launch();
+  k_fill<<<gridn(n), kBlock, 0, st>>>(n, 1.0 / sqrt((double)n), x);
+  KP p = make_kp(g, L);
+  p.ctr = ctr;
+  const bool W = g->weighted != 0;
+  const void *fn = W ? (const void *)k_pass<SPMV, true> : (const void *)k_pass<SPMV, false>;
+  const int grid = persistent_grid(fn, g->num_sms);
+  double mu = 0.0, prev = -1.0;
+  int it = 0;
+  for (; it < max_iters; it++) {
+    FJ_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * n, st));
+    FJ_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * 2, st));
+    p.z = x;
+    p.rout = y;
+    void *args[] = {&p};
+    fj::count_launch();
+    FJ_CUDA(cudaLaunchKernel(fn, grid, kBlock, args, 0, st));
+    fj::count_launch();
+    k_jacobi_scale<<<gridn(n), kBlock, 0, st>>>(n, L.rp, L.d1, x, y, sums);
+    double h[2];
+    FJ_CUDA(cudaMemcpyAsync(h, sums, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FJ_CUDA(cudaStreamSynchronize(st));
+    const double ny = sqrt(h[0]);
+    mu = 2.0 * ny - 1.0;  // ||(J+I)x/2|| → (μ+1)/2 with ||x|| = 1
+    if (ny == 0.0) break;
+    fj::count_launch();
+    k_scale_copy<<<gridn(n), kBlock, 0, st>>>(n, 1.0 / ny, y, x);
+    if (fabs(mu - prev) <= tol * mu) break;
+    prev = mu;
+  }
+  cudaFreeAsync(x, st);
+  cudaFreeAsync(y, st);
+  cudaFreeAsync(sums, st);
+  cudaFreeAsync(ctr, st);
+  (void)partial;
+  FJ_CUDA(cudaStreamSynchronize(st));
+  if (mu > 1.0) mu = 1.0;
+  *mu_out = mu;
+  const double r = mu / (1.0 + sqrt(fmax(0.0, 1.0 - mu * mu)));
+  *omega_out = 1.0 + r * r;
+  if (iters_out) *iters_out = it + 1;
+  return FJ_OK;
+}
 }  // namespace fj
 
 extern "C" {
@@ -1634,6 +1731,62 @@ fj_status fj_solve_ex(fj_graph_t g, const float *s, double eps, double omega, co
     return FJ_ERR_INVALID;
   }
   return fj::solve_impl(g, s, eps, omega, &d, z_out, st);
+}
+
+fj_status fj_omega_opt(fj_graph_t g, int max_iters, double tol, double *mu, double *omega) {
+  if (!g || !mu || !omega || max_iters < 1 || !(tol > 0)) {
+    fj::set_error("fj_omega_opt: bad argument");
+    return FJ_ERR_INVALID;
+  }
+  return fj::omega_opt_impl(g, max_iters, tol, mu, omega, nullptr);
+}
+
+fj_status fj_omega_sweep(fj_graph_t g, const float *s, double eps, double lo, double hi, double step,
+                         int method, double *best_omega, double *table, int *npts) {
+  if (!g || !s || !best_omega || !npts || !(step > 0) || !(lo > 0) || !(hi < 2) || hi < lo) {
+    fj::set_error("fj_omega_sweep: bad argument");
+    return FJ_ERR_INVALID;
+  }
+  const int cap = *npts;
+  int k = 0;
+  double best = 1.0;
+  int64_t best_cost = -1;
+  float *z = nullptr;
+  FJ_CUDA(cudaMallocAsync(&z, sizeof(float) * g->n, g->stream));
+  fj_opts o;
+  fj_opts_default(&o);
+  o.method = method;
+  // the paper's heuristic: start near 2, lower ω by a fixed step to 1,
+  // keep the ω with the fewest updates; diverging ω cost +inf
+  for (int i = 0;; i++) {
+    const double om = hi - i * step;
+    if (om < lo - 1e-12) break;
+    fj_stats st;
+    fj_status rc = fj_solve_ex(g, s, eps, om, &o, z, &st);
+    if (rc != FJ_OK && rc != FJ_ERR_NUMERIC) {
+      cudaFreeAsync(z, g->stream);
+      return rc;
+    }
+    if (table && k < cap) {
+      table[3 * k] = om;
+      table[3 * k + 1] = (double)st.relaxations;
+      table[3 * k + 2] = (double)rc;
+    }
+    k++;
+    if (rc == FJ_OK && (best_cost < 0 || st.relaxations <= best_cost)) {
+      best_cost = st.relaxations;  // ties go to the smaller ω
+      best = om;
+    }
+  }
+  cudaFreeAsync(z, g->stream);
+  cudaStreamSynchronize(g->stream);
+  *npts = k;
+  *best_omega = best;
+  if (best_cost < 0) {
+    fj::set_error("fj_omega_sweep: no ω in the grid converged");
+    return FJ_ERR_NUMERIC;
+  }
+  return FJ_OK;
 }
 
 fj_status fj_solve(fj_graph_t g, const float *s, double eps, double omega, float *z_out) {

@@ -318,3 +318,49 @@ def test_push_long_scatter_lists(dev, hub_deg):
     n = hub_deg + 1
     rp, col, w = G.in_csr_from_edges(n, [(0, i) for i in range(1, n)])
     check_parity(dev, rp, col, w, fjgen.uniform(n, 9), 1e-6, 1.0, False, method="push")
+
+
+# ------------------------------------------------------- ω selection (f1)
+def test_omega_opt_small_closed_forms(dev):
+    """Eq. optimal-omega with μ by power iteration: P2 → μ = 1/2,
+    ω = 1.0718; K3 → μ = 2/3, ω = 1.1459 (S:360–361)."""
+    for edges, n, mu_t, om_t in [([(0, 1)], 2, 0.5, 1.0718), ([(0, 1), (1, 2), (0, 2)], 3, 2 / 3, 1.1459)]:
+        rp, col, w = G.in_csr_from_edges(n, edges)
+        g = fj.Graph(n, rp, col, None, directed=False)
+        mu, om = fj.omega_opt(g)
+        assert mu == pytest.approx(mu_t, abs=1e-6) and om == pytest.approx(om_t, abs=1e-4)
+        g.close()
+
+
+SMALL = {
+    "er2000": lambda: TINY["er2000"]()[:3] + (False,),
+    "lattice32": lambda: (*fjgen.lattice_graph(32, 0.01, 15), None, False),
+    "rmat10w": lambda: (lambda rp, col: (rp, col, fjgen.arc_weights(rp, col, 13), True))(
+        *fjgen.rmat_graph(10, 16, 13)),
+    "dirw-dense": lambda: TINY["dirw-dense"]()[:3] + (True,),
+}
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_omega_opt_vs_dense(dev, name):
+    rp, col, w, directed = SMALL[name]()
+    g = fj.Graph(len(rp) - 1, rp, col, w, directed=directed)
+    mu, om = fj.omega_opt(g, max_iters=20000, tol=1e-12)
+    mu_d = oracle.jacobi_mu_dense(rp, col, w)
+    assert mu == pytest.approx(mu_d, rel=1e-4)
+    assert om == pytest.approx(oracle.omega_opt(mu_d), rel=1e-4)
+    g.close()
+
+
+def test_omega_sweep_heuristic(dev):
+    """P:488 heuristic: the returned ω has the fewest relaxations among the
+    converged grid points (ties to the smaller ω); undirected ER favours ω > 1."""
+    rp, col, w, s, directed = TINY["er2000"]()
+    g = fj.Graph(2000, rp, col, None, directed=False)
+    best, rows = fj.omega_sweep(g, s, 1e-6, lo=1.0, hi=1.9, step=0.1)
+    assert len(rows) == 10
+    ok = [r for r in rows if r[2] == 0]
+    mincost = min(r[1] for r in ok)
+    assert best == pytest.approx(min(r[0] for r in ok if r[1] == mincost))
+    assert best > 1.0
+    g.close()
