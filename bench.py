@@ -113,6 +113,18 @@ def dist_setup(args):
     return world, rank, local
 
 
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    """Max of `value` over all ranks (device time is the max over ranks)."""
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64,
+                     device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def config_dict(prob, args, extra=None):
     d = {"workload": f"config{args.config}:{prob.name}", "n": prob.n, "m": prob.m,
          "eps": args.eps, "omega": args.omega, "directed": prob.directed,
@@ -132,13 +144,10 @@ def run_reference(args, prob, world, rank):
     `pushes` pops of Alg. 2+1 on the full graph."""
     import oracle
     if rank != 0:
-        return None
+        return None  # rank 0 alone runs the CPU reference
     total = args.steps + args.warmup
     budget_s = max(2.0, min(15.0, 150.0 / max(1, total)))
-    # calibrate pushes/second on a short bounded run
-    cal = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0, max_pushes=200_000)
-    rate = cal.pushes / max(cal.seconds, 1e-6)
-    pushes = int(rate * budget_s)
+    pushes = _calibrated_pushes(prob, args, budget_s)
     times, eus = [], []
     for i in range(total):
         r = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0, max_pushes=pushes)
@@ -160,11 +169,22 @@ def run_reference(args, prob, world, rank):
     return line
 
 
+def _calibrated_pushes(prob, args, seconds):
+    """Pops of the oracle's FIFO that take about `seconds` on this host (the
+    first pops are the hubs, so probe twice)."""
+    import oracle
+    pushes = 200_000
+    for _ in range(2):
+        cal = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0,
+                           max_pushes=pushes)
+        rate = cal.pushes / max(cal.seconds, 1e-6)
+        pushes = max(pushes, int(rate * min(seconds, 4.0)))
+    return max(1, int(rate * seconds))
+
+
 def cpu_baseline(prob, args):
     import oracle
-    cal = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0, max_pushes=200_000)
-    rate = cal.pushes / max(cal.seconds, 1e-6)
-    pushes = int(rate * 15.0)
+    pushes = _calibrated_pushes(prob, args, 15.0)
     r = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0, max_pushes=pushes)
     return {"value": r.touched / r.seconds, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"first {r.pushes} pops ({r.touched} edge updates, {r.seconds:.1f} s) of "
@@ -221,12 +241,7 @@ def run_ours(args, prob, world, rank, local):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = fj.lib().fj_kernel_launches() - launches0
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world, dev)
     eu_rank = sum(st.edge_updates for st, _ in stats)
     value = eu_rank * world / (ms / 1e3)
     st0, m0 = stats[-1]

@@ -38,17 +38,23 @@ __global__ void k_layout_keys(int64_t n, const int64_t *__restrict__ ort,
                               const int32_t *__restrict__ color, int ncolors,
                               uint64_t *__restrict__ keys, unsigned long long *__restrict__ gcount) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (u >= n) return;
-  int64_t L = ort[u + 1] - ort[u];
-  uint64_t grp;
-  if (L == 0) {
-    grp = (uint64_t)ncolors * kClasses;  // empty rows last, never swept
-  } else {
-    int c = color ? color[u] : 0;
-    grp = (uint64_t)c * kClasses + (uint64_t)(kClasses - 1 - row_class(L));
+  uint64_t grp = ~0ull;
+  if (u < n) {
+    int64_t L = ort[u + 1] - ort[u];
+    if (L == 0) {
+      grp = (uint64_t)ncolors * kClasses;  // empty rows last, never swept
+    } else {
+      int c = color ? color[u] : 0;
+      grp = (uint64_t)c * kClasses + (uint64_t)(kClasses - 1 - row_class(L));
+    }
+    keys[u] = (grp << 31) | (uint64_t)u;
   }
-  atomicAdd(&gcount[grp], 1ull);
-  keys[u] = (grp << 31) | (uint64_t)u;
+  // warp-aggregated histogram: one atomic per distinct group in the warp
+  const unsigned act = __ballot_sync(0xffffffffu, u < n);
+  if (u < n) {
+    const unsigned same = __match_any_sync(act, grp);
+    if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&gcount[grp], (unsigned long long)__popc(same));
+  }
 }
 
 __global__ void k_perm(int64_t n, const uint64_t *__restrict__ keys, const int64_t *__restrict__ ort,

@@ -347,15 +347,18 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
     if (np > 1) {
       __stcg(p.partial + slot + piece, make_double2(a.hi, a.lo));
       __threadfence();
+      // cumulative arrival count: the np-th, 2np-th, ... arrival finishes the
+      // row (no reset, so overlapping sweeps of the barrier-free kernel can
+      // never lose an arrival; mixing partials of two sweeps is still a
+      // valid relaxation amount by Lemma 3 and the certificate decides)
       const int old = atomicAdd(p.arrive + slot, 1);
-      if (old != np - 1) return;
+      if ((old + 1) % np != 0) return;
       __threadfence();
       acc_zero(a);
       for (int q = 0; q < np; q++) {  // fixed order ⇒ deterministic row sum
         const double2 x = __ldcg(p.partial + slot + q);
         acc_merge(a, dd{x.x, x.y});
       }
-      p.arrive[slot] = 0;
     }
     if constexpr (MODE == RELAX) {
       // a non-final piece returned above; a multi-piece row is finished by
@@ -712,7 +715,7 @@ __device__ __forceinline__ void relax_stream(const KP &p, const Scalars &S, int 
           if (np > 1) {
             __stcg(p.partial + T.slot + T.b, make_double2(acc.hi, acc.lo));
             __threadfence();
-            finish = atomicAdd(p.arrive + T.slot, 1) == np - 1;
+            finish = (atomicAdd(p.arrive + T.slot, 1) + 1) % np == 0;
             if (finish) {
               __threadfence();
               acc = dd{0.0, 0.0};
@@ -720,7 +723,6 @@ __device__ __forceinline__ void relax_stream(const KP &p, const Scalars &S, int 
                 const double2 x = __ldcg(p.partial + T.slot + q);
                 acc_merge(acc, dd{x.x, x.y});
               }
-              p.arrive[T.slot] = 0;
             }
           }
           if (finish) relax_row_pre(p, S, row, len, acc, sv, zi, d1, t);
@@ -857,6 +859,102 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
     p.out[1] = tot_upd;
     p.out[2] = tot_eu;
     p.out[3] = (unsigned long long)reason;
+  }
+}
+
+// ------------------------------------------- barrier-free asynchronous sweeps
+// ASYNC with one phase: warps claim batches of work items from one monotonic
+// counter; item c belongs to epoch (sweep) c / nr.  Epochs therefore run back
+// to back without a grid barrier, and the claim order balances the load.  The
+// warp that completes an epoch checks its update count: zero updates (no row
+// had |r| > h when evaluated) stops the loop — the paper's Q = ∅ — and the
+// host-side compensated certificate decides (resuming if a row slipped).
+constexpr int kClaim = 16;   // items per claim
+constexpr int kRing = 8;     // per-epoch counter slots
+struct AsyncCtl {
+  unsigned long long next;                 // claim counter (items)
+  unsigned long long upd[kRing], eu[kRing], done[kRing];
+  unsigned long long tot_upd, tot_eu;
+  unsigned int stop, bad, epochs, pad;
+};
+
+// settle one warp's counts for an epoch part: warp-reduce, then lane 0 adds
+// them; the warp that completes the epoch decides whether to stop
+__device__ __forceinline__ void async_settle(AsyncCtl *c, unsigned long long ep,
+                                             unsigned long long nr, TAcc &t,
+                                             unsigned long long cnt) {
+  unsigned long long u = t.upd, e2 = t.eu, b = t.bad;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    u += __shfl_xor_sync(0xffffffffu, u, off);
+    e2 += __shfl_xor_sync(0xffffffffu, e2, off);
+    b |= __shfl_xor_sync(0xffffffffu, b, off);
+  }
+  t = TAcc{};
+  if ((threadIdx.x & 31) != 0 || cnt == 0) return;
+  const int slot = (int)(ep % kRing);
+  if (u) atomicAdd(&c->upd[slot], u);
+  atomicAdd(&c->tot_upd, u);
+  atomicAdd(&c->tot_eu, e2);
+  if (b) atomicOr(&c->bad, 1u);
+  __threadfence();
+  if (atomicAdd(&c->done[slot], cnt) + cnt == nr) {  // epoch ep complete
+    __threadfence();
+    const unsigned long long uu = atomicAdd(&c->upd[slot], 0ull);
+    atomicMax(&c->epochs, (unsigned int)(ep + 1));
+    if (uu == 0 || atomicAdd(&c->bad, 0u)) atomicExch(&c->stop, 1u);
+    const int z = (int)((ep + kRing / 2) % kRing);  // recycle a slot well ahead
+    c->upd[z] = 0;
+    c->done[z] = 0;
+  }
+}
+
+// out[0..3] = sweeps, relaxations, edge updates, reason (as k_sweep writes)
+__global__ void k_async_result(const AsyncCtl *c, unsigned long long *out,
+                               unsigned long long max_sweeps) {
+  out[0] = c->epochs;
+  out[1] = c->tot_upd;
+  out[2] = c->tot_eu;
+  out[3] = c->bad ? 2ull : (c->stop ? 0ull : 1ull);
+}
+
+template <bool W>
+__global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_async(KP p, AsyncCtl *c) {
+  extern __shared__ double s_prod[];
+  const Scalars S = *p.sc;
+  const int lane = threadIdx.x & 31;
+  double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
+  const unsigned long long nr = (unsigned long long)(p.rphase_begin[1] - p.rphase_begin[0]);
+  const Task *items = p.rtasks + p.rphase_begin[0];
+  const unsigned long long limit = nr * (unsigned long long)p.max_sweeps;
+  unsigned long long my_epoch = ~0ull;
+  TAcc t{};
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&c->next, (unsigned long long)kClaim);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const unsigned int stop = *(volatile unsigned int *)&c->stop;
+    if (stop || base >= limit || nr == 0) break;
+    unsigned long long ep = base / nr, cnt = 0;
+    for (int q = 0; q < kClaim; q++) {
+      const unsigned long long it = base + q;
+      if (it >= limit) break;
+      const unsigned long long e = it / nr;
+      if (e != ep) {  // the batch straddles two epochs: settle the first part
+        async_settle(c, ep, nr, t, cnt);
+        cnt = 0;
+        ep = e;
+      }
+      if (e != my_epoch) {  // a new sweep for this warp: drop stale L1 lines of ẑ
+        __threadfence();
+        my_epoch = e;
+      }
+      const Task tk = items[it - e * nr];
+      if ((tk.kind & 0xff) == kWarp) do_warp<RELAX, W>(p, S, tk, t);
+      else relax_warp_tile<W>(p, S, tk, t, wprod);
+      cnt++;
+    }
+    async_settle(c, ep, nr, t, cnt);
   }
 }
 
@@ -1477,15 +1575,34 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   float ms_sweep = 0, ms_cert = 0;
   int rounds = 0;
   stats.colors = L.ncolors;
+  // one-phase ASYNC runs barrier-free (k_sweep_async) unless FJ_BARRIER=1
+  const bool barrier_free = L.ncolors == 1 && !tma && !(getenv("FJ_BARRIER") && atoi(getenv("FJ_BARRIER")));
+  const void *fa = W ? (const void *)k_sweep_async<true> : (const void *)k_sweep_async<false>;
+  const size_t async_smem = (kBlock / 32) * kWarpTileArcs * sizeof(double);
+  AsyncCtl *actl = nullptr;
+  if (barrier_free) {
+    FJ_CUDA(cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)async_smem));
+    FJ_CUDA(cudaMallocAsync(&actl, sizeof(AsyncCtl), st));
+  }
+  const int agrid = barrier_free ? persistent_grid(fa, g->num_sms, async_smem) : 0;
   for (;;) {
     // a3–a5: persistent sweeps with on-device loop control
     FJ_CUDA(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * 8, st));
     FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(SweepCounters) * 3, st));
     FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 8, st));
-    void *args[] = {&p};
     FJ_CUDA(cudaEventRecord(es0, st));
-    fj::count_launch();
-    FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, sweep_smem, st));
+    if (barrier_free) {
+      FJ_CUDA(cudaMemsetAsync(actl, 0, sizeof(AsyncCtl), st));
+      void *args[] = {&p, &actl};
+      fj::count_launch();
+      FJ_CUDA(cudaLaunchKernel(fa, agrid, kBlock, args, async_smem, st));
+      fj::count_launch();
+      k_async_result<<<1, 1, 0, st>>>(actl, outv, (unsigned long long)p.max_sweeps);
+    } else {
+      void *args[] = {&p};
+      fj::count_launch();
+      FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, sweep_smem, st));
+    }
     FJ_CUDA(cudaEventRecord(es1, st));
     // fp64 compensated certificate over every non-empty row
     if (o->certify) {
@@ -1522,6 +1639,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     // the certificate rejects is relaxed again
     p.theta *= 0.5;
   }
+  if (actl) cudaFreeAsync(actl, st);
   stats.cert_rounds = rounds;
   stats.phases = stats.sweeps * L.ncolors;
   stats.rows_read = stats.sweeps * L.active_rows;

@@ -5,7 +5,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import fjgen
 so = os.path.join(ROOT, "tools", "libprobe.so")
-if not os.path.exists(so):
+if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(os.path.join(ROOT, "tools", "microbench.cu")):
     subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a",
                            "-O3", "-shared", "-Xcompiler", "-fPIC", "-o", so,
                            os.path.join(ROOT, "tools", "microbench.cu")])
@@ -52,3 +52,10 @@ for name, perm in orders.items():
     ms = L.fj_probe(2, m, oc2.data_ptr(), 0 if w is None else w.data_ptr(), z.data_ptr(),
                     zf.data_ptr(), 5, 4)
     print(f"{p.name} relabel {name:24s} spmv fp64 {ms:7.3f} ms  arcs/s {m/ms/1e6:7.1f} G", flush=True)
+
+L.fj_probe_k.restype = ctypes.c_float
+L.fj_probe_k.argtypes = [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 3 + [ctypes.c_int]
+for K in (2, 4, 8):
+    zk = torch.rand(p.n * K, dtype=torch.float64, device=dev)
+    ms = L.fj_probe_k(K, m, ocol.data_ptr(), 0 if w is None else w.data_ptr(), zk.data_ptr(), 5)
+    print(f"{p.name} K={K} spmv fp64 {ms:7.3f} ms  arcs/s {m/ms/1e6:7.1f} G  EU/s {K*m/ms/1e6:7.1f} G", flush=True)
