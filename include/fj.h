@@ -150,6 +150,19 @@ fj_status fj_solve_ex(fj_graph_t g, const float *s, double eps, double omega,
                       const fj_opts *o, float *z_out, fj_stats *st);
 
 /*
+ * Batched solve: k ∈ [1, 4] opinion vectors on one graph
+ * in one set of sweeps; ẑ is kept node-major so every gathered cache line and
+ * every CSR stream serves all k right-hand sides.  S and Z_out: fp32[n·k],
+ * node-major (S[v·k + r]).  Every right-hand side r gets its own Alg. 2 shift
+ * c_r and thresholds (reading R5), its own relax decisions, and its own fp64
+ * certificate; st (nullable) reports the worst certificate ratio, the sum of
+ * relaxations / edge updates over the right-hand sides, and the c of r = 0.
+ * Schedule: ASYNC only (o->method AUTO or ASYNC).
+ */
+fj_status fj_solve_batch(fj_graph_t g, const float *S, int k, double eps, double omega,
+                         const fj_opts *o, float *Z_out, fj_stats *st);
+
+/*
  * ω selection.
  * fj_omega_opt: μ = ρ((I+D)^{-1}A) by power iteration from the
  * all-ones vector (at most max_iters SpMV sweeps, stop when the estimate moves

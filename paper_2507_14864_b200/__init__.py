@@ -24,7 +24,8 @@ METHODS = {"auto": 0, "async": 1, "colored": 2, "push": 3}
 #: every symbol include/fj.h declares
 EXPORTS = ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve", "fj_solve_ex",
            "fj_measures", "fj_measures_ex", "fj_opts_default", "fj_last_error",
-           "fj_abi_version", "fj_kernel_launches", "fj_omega_opt", "fj_omega_sweep")
+           "fj_abi_version", "fj_kernel_launches", "fj_omega_opt", "fj_omega_sweep",
+           "fj_solve_batch")
 
 
 class FJError(RuntimeError):
@@ -81,12 +82,14 @@ def lib():
         L.fj_opts_default.restype = None
         L.fj_last_error.restype = ctypes.c_char_p
         L.fj_kernel_launches.restype = ctypes.c_int64
+        L.fj_solve_batch.argtypes = [P, P, i, d, d, ctypes.POINTER(_Opts), P,
+                                     ctypes.POINTER(_Stats)]
         L.fj_omega_opt.argtypes = [P, i, d, ctypes.POINTER(d), ctypes.POINTER(d)]
         L.fj_omega_sweep.argtypes = [P, P, d, d, d, d, i, ctypes.POINTER(d), P,
                                      ctypes.POINTER(i)]
         for f in ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve",
                   "fj_solve_ex", "fj_measures", "fj_measures_ex", "fj_omega_opt",
-                  "fj_omega_sweep"):
+                  "fj_omega_sweep", "fj_solve_batch"):
             getattr(L, f).restype = i
         _LIB = L
     return _LIB
@@ -204,6 +207,24 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
     rc = lib().fj_solve_ex(g._h, _ptr(s), float(eps), float(omega), ctypes.byref(o),
                            _ptr(z_out), ctypes.byref(st))
     stats = SolveStats(**{k: getattr(st, k) for k, _ in _Stats._fields_})
+    if rc == FJ_ERR_NUMERIC and not raise_on_numeric:
+        return stats
+    _check(rc)
+    return stats
+
+
+def solve_batch(g: Graph, S, Z_out, k: int, eps: float, omega: float = 1.0,
+                sigma: float = 1e-5, max_sweeps: int = 0, raise_on_numeric: bool = True) -> SolveStats:
+    """fj_solve_batch: k opinion vectors (node-major fp32[n*k]) in one solve."""
+    _dtype_ok(S, "S", "float32")
+    _dtype_ok(Z_out, "Z_out", "float32")
+    o = _Opts()
+    lib().fj_opts_default(ctypes.byref(o))
+    o.sigma, o.max_sweeps = sigma, max_sweeps
+    st = _Stats()
+    rc = lib().fj_solve_batch(g._h, _ptr(S), int(k), float(eps), float(omega), ctypes.byref(o),
+                              _ptr(Z_out), ctypes.byref(st))
+    stats = SolveStats(**{kk: getattr(st, kk) for kk, _ in _Stats._fields_})
     if rc == FJ_ERR_NUMERIC and not raise_on_numeric:
         return stats
     _check(rc)

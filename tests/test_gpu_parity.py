@@ -364,3 +364,26 @@ def test_omega_sweep_heuristic(dev):
     assert best == pytest.approx(min(r[0] for r in ok if r[1] == mincost))
     assert best > 1.0
     g.close()
+
+
+# ----------------------------------------------------- batched RHS (f2)
+@pytest.mark.parametrize("name", ["er2000", "rmat12w", "chunglu4k", "lattice64"])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_batch_solve(dev, name, k):
+    """fj_solve_batch: k opinion vectors (Unif / Exp / Pareto / signed, the
+    paper's three distributions P:618 plus a signed one) solved together; each
+    column matches the oracle and passes the oracle's certificate."""
+    rp, col, w, s0, directed = TINY[name]()
+    n = len(rp) - 1
+    cols = [s0, fjgen.exponential(n, 21), fjgen.pareto(n, 22), fjgen.uniform(n, 23, -1.0, 1.0)][:k]
+    S = np.ascontiguousarray(np.stack(cols, axis=1).astype(np.float32))
+    g = fj.Graph(n, _t(rp, dev), _t(col, dev), _t(w, dev), directed=directed)
+    Z = torch.empty(n * k, dtype=torch.float32, device=dev)
+    st = fj.solve_batch(g, _t(S.ravel(), dev), Z, k, 1e-6)
+    torch.cuda.synchronize()
+    Zh = Z.cpu().numpy().reshape(n, k).astype(np.float64)
+    assert st.status == 0 and st.cert_ratio <= 1.0
+    for r in range(k):
+        ref = oracle.solve(rp, col, w, S[:, r], 1e-6, 1.0)
+        assert rel_err(Zh[:, r], ref.z) <= 1e-4, r
+    g.close()
