@@ -936,6 +936,14 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_async(KP p, AsyncCtl 
     const unsigned int stop = *(volatile unsigned int *)&c->stop;
     if (stop || base >= limit || nr == 0) break;
     unsigned long long ep = base / nr, cnt = 0;
+    // bounded staleness: a warp may run at most kRing/2 - 1 sweeps ahead of
+    // the oldest unfinished one (keeps the per-sweep counter slots distinct;
+    // the oldest sweep's holders are never blocked, so this cannot deadlock)
+    if (lane == 0)
+      while (ep >= (unsigned long long)*(volatile unsigned int *)&c->epochs + kRing / 2 - 1 &&
+             !*(volatile unsigned int *)&c->stop)
+        __nanosleep(256);
+    __syncwarp();
     for (int q = 0; q < kClaim; q++) {
       const unsigned long long it = base + q;
       if (it >= limit) break;
@@ -1146,6 +1154,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_sweep_batch(KP p, AsyncCtl *c) {
     const unsigned int stop = *(volatile unsigned int *)&c->stop;
     if (stop || base >= limit || nr == 0) break;
     unsigned long long ep = base / nr, cnt = 0;
+    // bounded staleness: a warp may run at most kRing/2 - 1 sweeps ahead of
+    // the oldest unfinished one (keeps the per-sweep counter slots distinct;
+    // the oldest sweep's holders are never blocked, so this cannot deadlock)
+    if (lane == 0)
+      while (ep >= (unsigned long long)*(volatile unsigned int *)&c->epochs + kRing / 2 - 1 &&
+             !*(volatile unsigned int *)&c->stop)
+        __nanosleep(256);
+    __syncwarp();
     for (int q = 0; q < kClaim; q++) {
       const unsigned long long it = base + q;
       if (it >= limit) break;
@@ -1988,7 +2004,10 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   int rounds = 0;
   stats.colors = L.ncolors;
   // one-phase ASYNC runs barrier-free (k_sweep_async) unless FJ_BARRIER=1
-  const bool barrier_free = L.ncolors == 1 && !tma && !(getenv("FJ_BARRIER") && atoi(getenv("FJ_BARRIER")));
+  // the barrier-free kernel is opt-in (FJ_ASYNC_FREE=1): measured slower on
+  // C4/C5, where overlapping sweeps lose some Gauss–Seidel ordering
+  const bool barrier_free = L.ncolors == 1 && !tma && getenv("FJ_ASYNC_FREE") &&
+                            atoi(getenv("FJ_ASYNC_FREE"));
   const void *fa = W ? (const void *)k_sweep_async<true> : (const void *)k_sweep_async<false>;
   const size_t async_smem = (kBlock / 32) * kWarpTileArcs * sizeof(double);
   AsyncCtl *actl = nullptr;
