@@ -262,9 +262,11 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
   const int nb = bits_for(n);
 
   // 1. stage into library-owned memory (padded: the sweep reads in 16-byte units)
+  mark("setup");
   FJ_CUDA(cudaMallocAsync(&g->in_rp, sizeof(int64_t) * (n + 1), st));
   FJ_CUDA(cudaMallocAsync(&g->in_col, sizeof(int32_t) * (m + 8), st));
   if (w_in) FJ_CUDA(cudaMallocAsync(&g->in_w, sizeof(float) * (m + 8), st));
+  mark("alloc");
   FJ_CUDA(cudaMemcpyAsync(g->in_rp, rp_in, sizeof(int64_t) * (n + 1), cudaMemcpyDefault, st));
   if (m > 0) {
     FJ_CUDA(cudaMemcpyAsync(g->in_col, col_in, sizeof(int32_t) * m, cudaMemcpyDefault, st));

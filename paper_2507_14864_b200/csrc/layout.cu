@@ -8,6 +8,7 @@
 // and lattice neighbours stay close in memory.
 #include <stdio.h>
 #include <stdlib.h>
+#include <time.h>
 
 #include <algorithm>
 #include <cub/cub.cuh>
@@ -89,6 +90,51 @@ __global__ void k_copy_rows(int64_t n, const int32_t *__restrict__ perm,
   }
 }
 
+// pieces per row for warp units: class 6 rows → 1, class 7 rows → ⌈L/2048⌉
+__global__ void k_piece_counts(int64_t n, const int64_t *__restrict__ rp, int64_t *__restrict__ np) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  if (i == n) { np[i] = 0; return; }
+  const int64_t L = rp[i + 1] - rp[i];
+  np[i] = L > (kWarpTileArcs > 64 ? kWarpTileArcs : 128) ? (L + kWarpPiece - 1) / kWarpPiece : 0;
+}
+// warp units in row order: unit scan[i] + p is piece p of row i
+__global__ void k_fill_units(int64_t n, const int64_t *__restrict__ scan, Task *__restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t b = scan[i], np = scan[i + 1] - b;
+  for (int64_t p = 0; p < np; p++)
+    out[b + p] = Task{(int32_t)i, (int32_t)p, kWarp | (int32_t)(np << 8), (int32_t)b, 0, 0};
+}
+// values of a device array at host-given positions
+__global__ void k_pick(int cnt, const int64_t *__restrict__ pos, const int64_t *__restrict__ src,
+                       int64_t *__restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) out[i] = src[pos[i]];
+}
+// tile tasks of many row groups: group q covers tasks [out0, out0 + count) of
+// rows [r0, r1) in steps of `per` rows, kind = class
+struct TileGroup {
+  int64_t out0, count;
+  int32_t r0, r1, per, kind;
+};
+__global__ void k_fill_tiles(int ng, const TileGroup *__restrict__ gd, int64_t total,
+                             Task *__restrict__ out) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  int lo = 0, hi = ng - 1;  // last group with out0 <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (gd[mid].out0 <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const TileGroup g = gd[lo];
+  const int64_t k = t - g.out0;
+  const int32_t a = (int32_t)(g.r0 + k * g.per);
+  const int32_t b = (int32_t)min((int64_t)g.r1, (int64_t)a + g.per);
+  out[t] = Task{a, b, g.kind, 0, 0, 0};
+}
+
 // arc range of every task (needs the device row pointers)
 __global__ void k_task_arcs(int ntasks, const int64_t *__restrict__ rp, Task *__restrict__ tasks) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -109,6 +155,18 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
                                 bool need_d1) {
   cudaStream_t st = g->stream;
   const int64_t n = g->n, m = g->m;
+  const bool dbg = getenv("FJ_DEBUG") != nullptr;
+  timespec tt0;
+  clock_gettime(CLOCK_MONOTONIC, &tt0);
+  auto mark = [&](const char *what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(st);
+    timespec t1;
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    fprintf(stderr, "fj layout %-26s %8.2f ms\n", what,
+            1e3 * (t1.tv_sec - tt0.tv_sec) + 1e-6 * (t1.tv_nsec - tt0.tv_nsec));
+    tt0 = t1;
+  };
   L->release(st);
   L->warp_unit_arcs = 0;
   L->n = n;
@@ -157,6 +215,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     FJ_CUDA(cudaFreeAsync(t, st));
   }
   fj::count_launch();
+  mark("keys+sort+perm+scan");
   k_copy_rows<<<gridn(n * 32), kBlock, 0, st>>>(n, L->perm, L->iperm, ort, ocol, ow, g->deg, L->rp,
                                                 L->col, L->w, L->d1);
 
@@ -178,6 +237,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
                           cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
 
+  mark("copy rows + counts");
   // group g covers new rows [gstart[g], gstart[g] + hcount[g])
   std::vector<int64_t> gstart(ngroups + 1, 0);
   for (int q = 0; q < ngroups; q++) gstart[q + 1] = gstart[q] + (int64_t)hcount[q];
@@ -189,63 +249,109 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
 
   // work lists: tile tasks (classes 0..5) and warp units (classes 6, 7), each
   // grouped by color; within a color, longest rows first
-  std::vector<Task> tasks, wtasks, rtasks;
+  // ---- work lists, generated on the device ----
+  // (1) row_ptr and warp-unit scan at every group boundary
+  static const int kLmax[6] = {4, 8, 16, 32, 64, kWarpTileArcs > 64 ? kWarpTileArcs : 128};
+  int64_t *npc = nullptr, *scan = nullptr, *dpos = nullptr, *dval = nullptr;
+  FJ_CUDA(cudaMallocAsync(&npc, sizeof(int64_t) * (n + 1), st));
+  FJ_CUDA(cudaMallocAsync(&scan, sizeof(int64_t) * (n + 1), st));
+  fj::count_launch();
+  k_piece_counts<<<gridn(n + 1), kBlock, 0, st>>>(n, L->rp, npc);
+  {
+    size_t tmp = 0;
+    FJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, npc, scan, n + 1, st));
+    void *t = nullptr;
+    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    FJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, npc, scan, n + 1, st));
+    FJ_CUDA(cudaFreeAsync(t, st));
+  }
+  std::vector<int64_t> hpos(ngroups + 1), hrp(ngroups + 1), hscan(ngroups + 1);
+  for (int q = 0; q <= ngroups; q++) hpos[q] = gstart[q];
+  FJ_CUDA(cudaMallocAsync(&dpos, sizeof(int64_t) * (ngroups + 1), st));
+  FJ_CUDA(cudaMallocAsync(&dval, sizeof(int64_t) * 2 * (ngroups + 1), st));
+  FJ_CUDA(cudaMemcpyAsync(dpos, hpos.data(), sizeof(int64_t) * (ngroups + 1), cudaMemcpyHostToDevice, st));
+  fj::count_launch();
+  k_pick<<<gridn(ngroups + 1), kBlock, 0, st>>>(ngroups + 1, dpos, L->rp, dval);
+  fj::count_launch();
+  k_pick<<<gridn(ngroups + 1), kBlock, 0, st>>>(ngroups + 1, dpos, scan, dval + ngroups + 1);
+  FJ_CUDA(cudaMemcpyAsync(hrp.data(), dval, sizeof(int64_t) * (ngroups + 1), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaMemcpyAsync(hscan.data(), dval + ngroups + 1, sizeof(int64_t) * (ngroups + 1),
+                          cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  // (2) list sizes and group descriptors on the host (O(colors · classes))
   L->phase_begin.assign(ncolors + 1, 0);
   L->wphase_begin.assign(ncolors + 1, 0);
   L->rphase_begin.assign(ncolors + 1, 0);
-  static const int kLmax[6] = {4, 8, 16, 32, 64, kWarpTileArcs > 64 ? kWarpTileArcs : 128};
-  int slot = 0;
+  std::vector<TileGroup> ctag, rtag;  // CTA tiles, warp tiles
+  std::vector<std::pair<int64_t, int64_t>> unit_copy;  // per color: (src wtask begin, count)
+  int64_t nt = 0, nrt = 0;
   for (int c = 0; c < ncolors; c++) {
-    L->phase_begin[c] = (int)tasks.size();
-    L->wphase_begin[c] = (int)wtasks.size();
-    L->rphase_begin[c] = (int)rtasks.size();
-    for (int cd = 0; cd < kClasses; cd++) {  // cd = 7 - class
-      int q = c * kClasses + cd;
-      int cls = kClasses - 1 - cd;
-      int64_t r0 = gstart[q], r1 = gstart[q + 1];
+    L->phase_begin[c] = (int)nt;
+    L->rphase_begin[c] = (int)nrt;
+    const int q6 = c * kClasses + 0, q5 = c * kClasses + 2;  // cd 0,1 = classes 7,6
+    const int64_t u0 = hscan[q6], u1 = hscan[q5];
+    L->wphase_begin[c] = (int)u0;
+    unit_copy.push_back({u0, u1 - u0});
+    nrt += u1 - u0;
+    L->warp_unit_arcs += hrp[q5] - hrp[q6];
+    for (int cd = 2; cd < kClasses; cd++) {
+      const int q = c * kClasses + cd, cls = kClasses - 1 - cd;
+      const int64_t r0 = gstart[q], r1 = gstart[q + 1];
       if (r1 <= r0) continue;
-      if (cls >= 6) {
-        int64_t ra = 0, rz = 0;
-        FJ_CUDA(cudaMemcpyAsync(&ra, L->rp + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        FJ_CUDA(cudaMemcpyAsync(&rz, L->rp + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        FJ_CUDA(cudaStreamSynchronize(st));
-        L->warp_unit_arcs += rz - ra;
-      }
-      if (cls == 7) {
-        std::vector<int64_t> rph(r1 - r0 + 1);
-        FJ_CUDA(cudaMemcpyAsync(rph.data(), L->rp + r0, sizeof(int64_t) * (r1 - r0 + 1),
-                                cudaMemcpyDeviceToHost, st));
-        FJ_CUDA(cudaStreamSynchronize(st));
-        for (int64_t i = r0; i < r1; i++) {
-          int64_t len_i = rph[i - r0 + 1] - rph[i - r0];
-          int np = (int)((len_i + kWarpPiece - 1) / kWarpPiece);
-          for (int p = 0; p < np; p++) {
-            wtasks.push_back(Task{(int32_t)i, p, kWarp | (np << 8), slot, 0, 0});
-            rtasks.push_back(wtasks.back());
-          }
-          slot += np;
-        }
-      } else if (cls == 6) {
-        for (int64_t i = r0; i < r1; i++) {
-          wtasks.push_back(Task{(int32_t)i, 0, kWarp | (1 << 8), 0, 0, 0});
-          rtasks.push_back(wtasks.back());
-        }
-      } else {
-        int G = 1 << cls;
-        int64_t per = kBlock / G;  // one G-lane group per row
-        for (int64_t a = r0; a < r1; a += per)
-          tasks.push_back(Task{(int32_t)a, (int32_t)std::min(r1, a + per), cls, 0, 0, 0});
-        // warp tiles for the sweep: <= kWarpTileArcs arcs, 32/G rows per step
-        const int64_t wper = kWarpTileArcs / kLmax[cls];
-        for (int64_t a = r0; a < r1; a += wper)
-          rtasks.push_back(Task{(int32_t)a, (int32_t)std::min(r1, a + wper), cls, 0, 0, 0});
-      }
+      const int64_t per = kBlock >> cls, wper = kWarpTileArcs / kLmax[cls];
+      const int64_t cnt = (r1 - r0 + per - 1) / per, wcnt = (r1 - r0 + wper - 1) / wper;
+      ctag.push_back(TileGroup{nt, cnt, (int32_t)r0, (int32_t)r1, (int32_t)per, cls});
+      rtag.push_back(TileGroup{nrt, wcnt, (int32_t)r0, (int32_t)r1, (int32_t)wper, cls});
+      nt += cnt;
+      nrt += wcnt;
     }
   }
-  L->phase_begin[ncolors] = (int)tasks.size();
-  L->wphase_begin[ncolors] = (int)wtasks.size();
-  L->rphase_begin[ncolors] = (int)rtasks.size();
-  L->nrtasks = (int)rtasks.size();
+  const int64_t nwt = hscan[ngroups - 1];  // all warp units precede the empty rows
+  L->phase_begin[ncolors] = (int)nt;
+  L->wphase_begin[ncolors] = (int)nwt;
+  L->rphase_begin[ncolors] = (int)nrt;
+  L->ntasks = (int)nt;
+  L->nwtasks = (int)nwt;
+  L->nrtasks = (int)nrt;
+  L->npartials = (int)nwt;
+  // (3) fill the three lists on the device
+  FJ_CUDA(cudaMallocAsync(&L->tasks, sizeof(Task) * std::max<int64_t>(1, nt), st));
+  FJ_CUDA(cudaMallocAsync(&L->wtasks, sizeof(Task) * std::max<int64_t>(1, nwt), st));
+  FJ_CUDA(cudaMallocAsync(&L->rtasks, sizeof(Task) * std::max<int64_t>(1, nrt), st));
+  if (nwt > 0) {
+    fj::count_launch();
+    k_fill_units<<<gridn(n), kBlock, 0, st>>>(n, scan, L->wtasks);
+  }
+  TileGroup *dg = nullptr;
+  const size_t ngd = ctag.size() + rtag.size();
+  FJ_CUDA(cudaMallocAsync(&dg, sizeof(TileGroup) * std::max<size_t>(1, ngd), st));
+  if (!ctag.empty())
+    FJ_CUDA(cudaMemcpyAsync(dg, ctag.data(), sizeof(TileGroup) * ctag.size(), cudaMemcpyHostToDevice, st));
+  if (!rtag.empty())
+    FJ_CUDA(cudaMemcpyAsync(dg + ctag.size(), rtag.data(), sizeof(TileGroup) * rtag.size(),
+                            cudaMemcpyHostToDevice, st));
+  if (nt > 0) {
+    fj::count_launch();
+    k_fill_tiles<<<gridn(nt), kBlock, 0, st>>>((int)ctag.size(), dg, nt, L->tasks);
+  }
+  if (!rtag.empty()) {
+    fj::count_launch();
+    k_fill_tiles<<<gridn(nrt), kBlock, 0, st>>>((int)rtag.size(), dg + ctag.size(), nrt, L->rtasks);
+  }
+  for (int c = 0; c < ncolors; c++)  // warp units of color c head its sweep list
+    if (unit_copy[c].second > 0)
+      FJ_CUDA(cudaMemcpyAsync(L->rtasks + L->rphase_begin[c], L->wtasks + unit_copy[c].first,
+                              sizeof(Task) * unit_copy[c].second, cudaMemcpyDeviceToDevice, st));
+  for (Task *lst : {L->tasks, L->wtasks, L->rtasks}) {
+    const int64_t cnt = lst == L->tasks ? nt : lst == L->wtasks ? nwt : nrt;
+    if (cnt > 0) {
+      fj::count_launch();
+      k_task_arcs<<<gridn(cnt), kBlock, 0, st>>>((int)cnt, L->rp, lst);
+    }
+  }
+  FJ_CUDA(cudaStreamSynchronize(st));  // host vectors above are stack-owned
+  for (void *q : {(void *)npc, (void *)scan, (void *)dpos, (void *)dval, (void *)dg}) cudaFreeAsync(q, st);
+  mark("task lists");
   // measured on all five configs: direct loads beat the TMA-staged stream
   // once short rows run as warp tiles (the stage buffers take L1 away from
   // the ẑ gathers); the TMA path stays selectable with FJ_TMA=1
@@ -262,20 +368,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
               (long long)(cut[c + 1] - cut[c]), (long long)(arc[c + 1] - arc[c]),
               L->phase_begin[c + 1] - L->phase_begin[c], L->wphase_begin[c + 1] - L->wphase_begin[c]);
   }
-  L->ntasks = (int)tasks.size();
-  L->nwtasks = (int)wtasks.size();
-  L->npartials = slot;
   L->max_len = hmax;
-  for (int which = 0; which < 3; which++) {
-    std::vector<Task> &v = which == 0 ? tasks : which == 1 ? wtasks : rtasks;
-    Task **dst = which == 0 ? &L->tasks : which == 1 ? &L->wtasks : &L->rtasks;
-    FJ_CUDA(cudaMallocAsync(dst, sizeof(Task) * std::max<size_t>(1, v.size()), st));
-    if (!v.empty()) {
-      FJ_CUDA(cudaMemcpyAsync(*dst, v.data(), sizeof(Task) * v.size(), cudaMemcpyHostToDevice, st));
-      fj::count_launch();
-      k_task_arcs<<<gridn((int64_t)v.size()), kBlock, 0, st>>>((int)v.size(), L->rp, *dst);
-    }
-  }
   FJ_CUDA(cudaMallocAsync(&L->d_phase_begin, sizeof(int) * (ncolors + 1), st));
   FJ_CUDA(cudaMemcpyAsync(L->d_phase_begin, L->phase_begin.data(), sizeof(int) * (ncolors + 1),
                           cudaMemcpyHostToDevice, st));
