@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--method", default="auto")
     ap.add_argument("--eps", type=float, default=1e-6)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the per-omega time-to-eps table of the config (untimed)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     return ap.parse_args()
@@ -170,16 +172,20 @@ def run_reference(args, prob, world, rank):
 
 
 def _calibrated_pushes(prob, args, seconds):
-    """Pops of the oracle's FIFO that take about `seconds` on this host (the
-    first pops are the hubs, so probe twice)."""
+    """Pops of the oracle's FIFO that take about `seconds` on this host: grow a
+    bounded run until it lasts >= seconds/4, then scale (the first pops are the
+    hubs and cost more than later ones)."""
     import oracle
-    pushes = 200_000
-    for _ in range(2):
+    pushes = 100_000
+    while True:
         cal = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0,
                            max_pushes=pushes)
-        rate = cal.pushes / max(cal.seconds, 1e-6)
-        pushes = max(pushes, int(rate * min(seconds, 4.0)))
-    return max(1, int(rate * seconds))
+        if cal.status == 0 or cal.seconds >= seconds / 4:
+            break
+        pushes *= 4
+    if cal.status == 0:
+        return pushes  # the whole solve fits the budget
+    return max(1, int(pushes * seconds / max(cal.seconds, 1e-6)))
 
 
 def cpu_baseline(prob, args):
@@ -264,6 +270,9 @@ def run_ours(args, prob, world, rank, local):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, prob, fj, torch, dev, stream, world)
+    omega_table = None
+    if not args.no_sweep:
+        omega_table = run_omega_table(args, prob, fj, torch, rp, col, w, s, z)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -281,10 +290,33 @@ def run_ours(args, prob, world, rank, local):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
                          "kernel": "k_sweep (persistent)",
                          "algorithmic_bytes_per_launch": ab},
+            "omega_sweep": omega_table,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "e2e": e2e}
     return line
+
+
+def run_omega_table(args, prob, fj, torch, rp, col, w, s, z):
+    """Time-to-ε per ω of the config's list (BASELINE config 4: SOR ω swept
+    over {1.0, 1.2, 1.4, 1.6, 1.8}); outside the timed steps, graph built once,
+    median of 3 solves, diverging ω reported as such."""
+    import fjgen
+    omegas = fjgen.CONFIG_SOLVE.get(args.config, {}).get("omegas", [args.omega])
+    g = fj.Graph(prob.n, rp, col, w, directed=prob.directed)
+    rows = []
+    for om in omegas:
+        runs = [fj.solve(g, s, z, args.eps, om, method=args.method, raise_on_numeric=False)
+                for _ in range(3)]
+        st = sorted(runs, key=lambda r: r.solve_ms)[1]
+        rows.append({"omega": om, "status": "ok" if st.status == 0 else "diverged/numeric",
+                     "time_to_eps_s": st.solve_ms / 1e3 if st.status == 0 else None,
+                     "sweeps": st.sweeps, "edge_updates": st.edge_updates,
+                     "edge_updates_per_s": st.edge_updates / (st.solve_ms / 1e3),
+                     "cert_ratio": st.cert_ratio})
+    g.close()
+    torch.cuda.synchronize()
+    return rows
 
 
 def run_e2e(args, prob, fj, torch, dev, stream, world):

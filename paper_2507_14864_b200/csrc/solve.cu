@@ -456,26 +456,11 @@ __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, c
   const int G = 1 << cls;
   const int gl = lane & (G - 1);
   const int ng = 32 >> cls;  // groups per warp = rows per step
-  // row state for both steps
+  // row state is loaded per step in phase 2: loading both steps up front
+  // spilled (148 B/thread) and was 9 % slower on C4, 16 % on C5
   int64_t rb[2], re[2];
   float sv[2];
   double zi[2], d1[2];
-#pragma unroll
-  for (int q = 0; q < 2; q++) {
-    const int row = tk.a + q * ng + (lane >> cls);
-    rb[q] = re[q] = 0;
-    sv[q] = 0.f;
-    zi[q] = d1[q] = 0.0;
-    if (row < tk.b) {
-      rb[q] = __ldg(p.rp + row);
-      re[q] = __ldg(p.rp + row + 1);
-      if (gl == 0) {
-        sv[q] = __ldg(p.s + row);
-        zi[q] = __ldcg(p.z + row);
-        if (W) d1[q] = __ldg(p.d1 + row);
-      }
-    }
-  }
   const int64_t a0 = tk.a0;
   const int na = (int)(tk.a1 - a0);
   int j[U];
@@ -498,6 +483,21 @@ __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, c
   __syncwarp();
 #pragma unroll
   for (int q = 0; q < 2; q++) {
+    {
+      const int row = tk.a + q * ng + (lane >> cls);
+      rb[q] = re[q] = 0;
+      sv[q] = 0.f;
+      zi[q] = d1[q] = 0.0;
+      if (row < tk.b) {
+        rb[q] = __ldg(p.rp + row);
+        re[q] = __ldg(p.rp + row + 1);
+        if (gl == 0) {
+          sv[q] = __ldg(p.s + row);
+          zi[q] = __ldcg(p.z + row);
+          if (W) d1[q] = __ldg(p.d1 + row);
+        }
+      }
+    }
     double a = 0.0;
     const int kb = (int)(rb[q] - a0), ke = (int)(re[q] - a0);
     for (int k = kb + gl; k < ke; k += G) a += wprod[k];
