@@ -93,6 +93,7 @@ struct Layout {
   int64_t max_len = 0;
   int64_t warp_unit_arcs = 0;     // arcs in rows handled by warp units (> kWarpTileArcs)
   bool stream_tma = false;        // sweep streams arcs with TMA (see solve.cu)
+  int piece = kWarpPiece;         // arcs per warp piece of a hub row
   void release(cudaStream_t st);
 };
 

@@ -91,12 +91,13 @@ __global__ void k_copy_rows(int64_t n, const int32_t *__restrict__ perm,
 }
 
 // pieces per row for warp units: class 6 rows → 1, class 7 rows → ⌈L/2048⌉
-__global__ void k_piece_counts(int64_t n, const int64_t *__restrict__ rp, int64_t *__restrict__ np) {
+__global__ void k_piece_counts(int64_t n, const int64_t *__restrict__ rp, int piece,
+                               int64_t *__restrict__ np) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
   if (i == n) { np[i] = 0; return; }
   const int64_t L = rp[i + 1] - rp[i];
-  np[i] = L > (kWarpTileArcs > 64 ? kWarpTileArcs : 128) ? (L + kWarpPiece - 1) / kWarpPiece : 0;
+  np[i] = L > (kWarpTileArcs > 64 ? kWarpTileArcs : 128) ? (L + piece - 1) / piece : 0;
 }
 // warp units in row order: unit scan[i] + p is piece p of row i
 __global__ void k_fill_units(int64_t n, const int64_t *__restrict__ scan, Task *__restrict__ out) {
@@ -136,13 +137,14 @@ __global__ void k_fill_tiles(int ng, const TileGroup *__restrict__ gd, int64_t t
 }
 
 // arc range of every task (needs the device row pointers)
-__global__ void k_task_arcs(int ntasks, const int64_t *__restrict__ rp, Task *__restrict__ tasks) {
+__global__ void k_task_arcs(int ntasks, const int64_t *__restrict__ rp, int piece,
+                            Task *__restrict__ tasks) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ntasks) return;
   Task t = tasks[i];
   if ((t.kind & 0xff) == kWarp) {
-    t.a0 = rp[t.a] + (int64_t)t.b * kWarpPiece;
-    t.a1 = min(rp[t.a + 1], t.a0 + (int64_t)kWarpPiece);
+    t.a0 = rp[t.a] + (int64_t)t.b * piece;
+    t.a1 = min(rp[t.a + 1], t.a0 + (int64_t)piece);
   } else {
     t.a0 = rp[t.a];
     t.a1 = rp[t.b];
@@ -256,7 +258,13 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   FJ_CUDA(cudaMallocAsync(&npc, sizeof(int64_t) * (n + 1), st));
   FJ_CUDA(cudaMallocAsync(&scan, sizeof(int64_t) * (n + 1), st));
   fj::count_launch();
-  k_piece_counts<<<gridn(n + 1), kBlock, 0, st>>>(n, L->rp, npc);
+  // hub rows are split in warp pieces: long pieces (fewer partial combines)
+  // for one-phase sweeps; short ones for colored sweeps, where every phase
+  // waits for its slowest warp (FJ_PIECE overrides, diagnostics)
+  int piece = ncolors > 1 ? 256 : kWarpPiece;
+  if (getenv("FJ_PIECE")) piece = std::max(32, atoi(getenv("FJ_PIECE")));
+  L->piece = piece;
+  k_piece_counts<<<gridn(n + 1), kBlock, 0, st>>>(n, L->rp, piece, npc);
   {
     size_t tmp = 0;
     FJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, npc, scan, n + 1, st));
@@ -346,7 +354,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     const int64_t cnt = lst == L->tasks ? nt : lst == L->wtasks ? nwt : nrt;
     if (cnt > 0) {
       fj::count_launch();
-      k_task_arcs<<<gridn(cnt), kBlock, 0, st>>>((int)cnt, L->rp, lst);
+      k_task_arcs<<<gridn(cnt), kBlock, 0, st>>>((int)cnt, L->rp, piece, lst);
     }
   }
   FJ_CUDA(cudaStreamSynchronize(st));  // host vectors above are stack-owned

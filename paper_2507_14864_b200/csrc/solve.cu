@@ -28,6 +28,7 @@
 namespace fj {
 
 enum Mode { RELAX = 0, CERT = 1, DIS = 2, SPMV = 3 };
+constexpr int kClaim = 16;  // work items per dynamic claim
 
 struct Scalars {
   double c;        // shift (Alg. 2; reading R5)
@@ -75,6 +76,7 @@ struct KP {
   double *dis;
   double *rout;                  // CERT: optional residual output (layout order)
   int dbg;                       // diagnostics (env FJ_DBG_SKIP): 1 skip warp units, 2 skip tiles
+  int dyn;                       // dynamic work claiming in k_sweep (env FJ_DYN)
 };
 
 // CSR streams are read once per sweep: read-only path, no L1 allocation, so
@@ -273,7 +275,10 @@ template <int MODE, bool W>
 __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Task &tk, TAcc &t) {
   // rows above 256 arcs accumulate in double-double for RELAX and CERT
   using A = typename std::conditional<MODE == DIS || MODE == SPMV, double, dd>::type;
-  constexpr int U = 8;
+#ifndef FJ_WU
+#define FJ_WU 8
+#endif
+  constexpr int U = FJ_WU;  // arcs per lane per step (loads in flight)
   const int lane = threadIdx.x & 31;
   const int row = tk.a, piece = tk.b, np = tk.kind >> 8, slot = tk.slot;
   const int64_t a0 = tk.a0, a1 = tk.a1;
@@ -799,7 +804,24 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
       if (TMA) {
         relax_stream<W>(p, S, p.rphase_begin[k], p.rphase_begin[k + 1] - p.rphase_begin[k], t,
                         ws, phase_bits);
-      } else {  // one warp per work item (hub rows first), next item prefetched
+      } else if (p.dyn) {  // dynamic: warps claim kClaim items at a time
+        const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
+        double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
+        const int lane = threadIdx.x & 31;
+        if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[(phase + 2) % 3] = 0u;
+        for (;;) {
+          int base = 0;
+          if (lane == 0) base = (int)atomicAdd(p.ctr + phase % 3, (unsigned)kClaim);
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (base >= nr) break;
+          const int end = min(nr, base + kClaim);
+          for (int wi = base; wi < end; wi++) {
+            const Task cur = p.rtasks[r0 + wi];
+            if ((cur.kind & 0xff) == kWarp) do_warp<RELAX, W>(p, S, cur, t);
+            else relax_warp_tile<W>(p, S, cur, t, wprod);
+          }
+        }
+      } else {  // static round-robin: one warp per work item, next item prefetched
         const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
         const int stride = gridDim.x * (kBlock / 32);
         double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
@@ -869,7 +891,6 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
 // warp that completes an epoch checks its update count: zero updates (no row
 // had |r| > h when evaluated) stops the loop — the paper's Q = ∅ — and the
 // host-side compensated certificate decides (resuming if a row slipped).
-constexpr int kClaim = 16;   // items per claim
 constexpr int kRing = 8;     // per-epoch counter slots
 struct AsyncCtl {
   unsigned long long next;                 // claim counter (items)
@@ -1981,6 +2002,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   p.omega = omega;
   p.theta = 1.0;
   p.dbg = getenv("FJ_DBG_SKIP") ? atoi(getenv("FJ_DBG_SKIP")) : 0;
+  p.dyn = getenv("FJ_DYN") ? atoi(getenv("FJ_DYN")) : 0;
   p.partial = partial;
   p.arrive = arrive;
   p.max_sweeps = o->max_sweeps;
