@@ -78,6 +78,7 @@ struct KP {
   double *rout;                  // CERT: optional residual output (layout order)
   int dbg;                       // diagnostics (env FJ_DBG_SKIP): 1 skip warp units, 2 skip tiles
   int dyn;                       // dynamic work claiming in k_sweep (env FJ_DYN)
+  int symm;                      // alternate sweep direction (env FJ_SYMM)
 };
 
 // CSR streams are read once per sweep: read-only path, no L1 allocation, so
@@ -831,13 +832,15 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
         const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
         const int stride = gridDim.x * (kBlock / 32);
         double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
+        // FJ_SYMM: odd sweeps walk the work list backwards (symmetric ordering)
+        const bool rev = p.symm && (sw & 1);
         int wi = warp_id;
         Task nxt;
-        if (wi < nr) nxt = p.rtasks[r0 + wi];
+        if (wi < nr) nxt = p.rtasks[r0 + (rev ? nr - 1 - wi : wi)];
         while (wi < nr) {
           const Task cur = nxt;
           const int wn = wi + stride;
-          if (wn < nr) nxt = p.rtasks[r0 + wn];
+          if (wn < nr) nxt = p.rtasks[r0 + (rev ? nr - 1 - wn : wn)];
           if ((cur.kind & 0xff) == kWarp) {
             if (!(p.dbg & 1)) do_warp<RELAX, W>(p, S, cur, t);
           } else if (!(p.dbg & 2)) {
@@ -2009,6 +2012,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   p.theta = 1.0;
   p.dbg = getenv("FJ_DBG_SKIP") ? atoi(getenv("FJ_DBG_SKIP")) : 0;
   p.dyn = getenv("FJ_DYN") ? atoi(getenv("FJ_DYN")) : 0;
+  p.symm = getenv("FJ_SYMM") ? atoi(getenv("FJ_SYMM")) : 0;
   p.partial = partial;
   p.arrive = arrive;
   p.max_sweeps = o->max_sweeps;

@@ -405,3 +405,49 @@ def test_gpu_lemma4_one_sided(dev, name):
         assert np.all(zg <= z + tol)
         assert np.all(zg >= (1 - eps) * z - tol)
         g.close()
+
+
+# ------------------------------------------------ the C-ABI from plain C
+def test_c_program_against_abi(dev, tmp_path):
+    """examples/fj_example.c links libfj.so directly (no Python marshalling)
+    and checks the P2 worked example (tab:measures)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2507_14864_b200")
+    exe = str(tmp_path / "fj_example")
+    subprocess.check_call(["gcc", "-O2", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "examples", "fj_example.c"), "-L", libdir, "-l:libfj.so",
+                           f"-Wl,-rpath,{libdir}", "-lm", "-o", exe])
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "OK" in out.stdout
+
+
+# --------------------------------------- full BASELINE sizes (configs 2–5)
+@pytest.mark.parametrize("cid", [2, 3, 4, 5])
+def test_full_size_config_properties(dev, cid):
+    """At the full BASELINE.json size, in the launch configuration bench.py
+    times (AUTO schedule, ω = 1, ε = 1e-6), with properties that hold at any
+    size: (i) the oracle's compensated certificate of the GPU's ẑ' is ≤ 1, so
+    |ẑ − z| ≤ ε·max(|z|, σ) (Lemma 6 + R5); (ii) the GPU measures equal the
+    oracle's measures of the same z; (iii) min s ≤ z ≤ max s and nodes that
+    listen to no one keep z = s (fundamental matrix row-stochastic).
+    The oracle's own full-size FIFO solves are in profiles/r01_full_parity.md."""
+    p = fjgen.config(cid)
+    g = fj.Graph(p.n, _t(p.row_ptr, dev), _t(p.col, dev), _t(p.w, dev), directed=p.directed)
+    z = torch.empty(p.n, dtype=torch.float32, device=dev)
+    zp = torch.empty(p.n, dtype=torch.float64, device=dev)
+    st = fj.solve(g, _t(p.s, dev), z, 1e-6, 1.0, zprime_out=zp)
+    m = fj.measures(g, z)
+    zh = z.cpu().numpy().astype(np.float64)
+    ratio, _ = oracle.certificate(p.row_ptr, p.col, p.w, p.s, zp.cpu().numpy(), 1e-6)
+    assert st.status == 0 and st.cert_ratio <= 1.0 and ratio <= 1.0
+    om = oracle.measures(p.row_ptr, p.col, p.w, zh, directed=p.directed)
+    assert abs(m["P"] - om["P"]) <= 1e-9 * om["P"] and abs(m["D"] - om["D"]) <= 1e-9 * om["D"]
+    s64 = p.s.astype(np.float64)
+    assert zh.min() >= s64.min() - 1e-6 and zh.max() <= s64.max() + 1e-6
+    outdeg = np.bincount(p.col, minlength=p.n)
+    iso = outdeg == 0
+    np.testing.assert_allclose(zh[iso], s64[iso], rtol=0, atol=2e-7 * np.abs(s64[iso]).max() + 1e-12)
+    g.close()
