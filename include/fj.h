@@ -72,6 +72,12 @@ typedef struct {
   int certify;       /* 1 (default): run the compensated fp64 residual certificate     */
   double *zprime_out;/* optional fp64[n] ẑ' = ẑ + c in node order (host or device), for
                         an independent certificate by the caller; NULL = not written    */
+  const double *z_init; /* optional fp64[n] warm start (unshifted estimate of z, node
+                        order, host or device), e.g. the z of an earlier solve: resume /
+                        checkpoint.  Any start is valid (Lemma 3: the residual is
+                        recomputed from ẑ); the ε rule and certificate are unchanged.
+                        ASYNC/COLORED only (FJ_ERR_INVALID with PUSH).  NULL = start at 0
+                        as Alg. 1 does                                           */
 } fj_opts;
 
 typedef struct {

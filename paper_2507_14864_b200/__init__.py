@@ -37,7 +37,8 @@ class FJError(RuntimeError):
 class _Opts(ctypes.Structure):
     _fields_ = [("sigma", ctypes.c_double), ("c", ctypes.c_double), ("method", ctypes.c_int),
                 ("max_sweeps", ctypes.c_int), ("cert_rounds", ctypes.c_int),
-                ("certify", ctypes.c_int), ("zprime_out", ctypes.c_void_p)]
+                ("certify", ctypes.c_int), ("zprime_out", ctypes.c_void_p),
+                ("z_init", ctypes.c_void_p)]
 
 
 class _Stats(ctypes.Structure):
@@ -192,8 +193,10 @@ class Graph:
 
 def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "auto",
           sigma: float = 1e-5, c: float = 0.0, max_sweeps: int = 0, cert_rounds: int = -1,
-          certify: bool = True, zprime_out=None, raise_on_numeric: bool = True) -> SolveStats:
-    """fj_solve_ex: writes z into ``z_out`` (float32[n]); returns the stats."""
+          certify: bool = True, zprime_out=None, raise_on_numeric: bool = True,
+          z_init=None) -> SolveStats:
+    """fj_solve_ex: writes z into ``z_out`` (float32[n]); returns the stats.
+    ``z_init`` (float64[n], optional): warm start / resume from an earlier z."""
     _dtype_ok(s, "s", "float32")
     _dtype_ok(z_out, "z_out", "float32")
     _dtype_ok(zprime_out, "zprime_out", "float64")
@@ -203,6 +206,9 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
     o.max_sweeps, o.cert_rounds, o.certify = max_sweeps, cert_rounds, int(certify)
     zp = _ptr(zprime_out)
     o.zprime_out = zp.value if zp is not None else None
+    _dtype_ok(z_init, "z_init", "float64")
+    zi = _ptr(z_init)
+    o.z_init = zi.value if zi is not None else None
     st = _Stats()
     rc = lib().fj_solve_ex(g._h, _ptr(s), float(eps), float(omega), ctypes.byref(o),
                            _ptr(z_out), ctypes.byref(st))

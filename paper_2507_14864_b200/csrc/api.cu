@@ -73,6 +73,7 @@ void fj_opts_default(fj_opts *o) {
   o->cert_rounds = 3;
   o->certify = 1;
   o->zprime_out = nullptr;
+  o->z_init = nullptr;
 }
 
 fj_status fj_graph_get_info(fj_graph_t g, fj_graph_info *info) {

@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <cub/cub.cuh>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "fj_internal.cuh"
 
 namespace fj {
@@ -397,8 +399,10 @@ fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t *in_row_ptr, con
     return FJ_ERR_INVALID;
   }
   fj_graph *g = new fj_graph();
+  nvtxRangePushA("fj_graph_create");
   fj_status s = fj::create_impl(n, nnz, in_row_ptr, in_col, in_w, directed,
                                 (cudaStream_t)cuda_stream, g);
+  nvtxRangePop();
   if (s != FJ_OK) {
     fj_graph_destroy(g);
     return s;

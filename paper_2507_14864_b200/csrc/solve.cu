@@ -23,9 +23,16 @@
 #include <type_traits>
 #include <cub/cub.cuh>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "fj_internal.cuh"
 
 namespace fj {
+
+struct NvtxRange {  // tracing: one NVTX range per library phase (nsys/ncu timelines)
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 enum Mode { RELAX = 0, CERT = 1, DIS = 2, SPMV = 3 };
 constexpr int kClaim = 16;  // work items per dynamic claim
@@ -1462,13 +1469,19 @@ __global__ void k_scalars(const float *__restrict__ smin, const float *__restric
 // whose equation is (1 + 0) z_v = s'_v: solved exactly (ẑ'_v = s'_v)
 __global__ void k_init(int64_t n, const int32_t *__restrict__ perm, const int64_t *__restrict__ rp,
                        const float *__restrict__ s, Scalars *__restrict__ S,
-                       float *__restrict__ s_l, double *__restrict__ z) {
+                       float *__restrict__ s_l, double *__restrict__ z,
+                       const double *__restrict__ z_init = nullptr) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float si = s[perm[i]];
   if (!isfinite(si)) atomicOr(&S->bad_input, 1);  // min/max reductions skip NaN
   s_l[i] = si;
-  z[i] = (rp[i + 1] == rp[i]) ? (double)si + S->c : 0.0;
+  if (rp[i + 1] == rp[i]) z[i] = (double)si + S->c;          // d = 0: exact
+  else if (z_init) {                                          // warm start (Lemma 3)
+    const double v = z_init[perm[i]] + S->c;
+    if (!isfinite(v)) atomicOr(&S->bad_input, 2);
+    z[i] = v;
+  } else z[i] = 0.0;                                          // Alg. 1 init
 }
 
 __global__ void k_finalize(int64_t n, const int32_t *__restrict__ iperm, const double *__restrict__ z,
@@ -1570,7 +1583,7 @@ static fj_status finish_status(const Scalars &hs, fj_stats &stats, const fj_opts
                                double omega) {
   fj_status rc = FJ_OK;
   if (hs.bad_input) {
-    set_error("fj_solve: s contains a non-finite value");
+    set_error("fj_solve: s (or z_init) contains a non-finite value");
     rc = FJ_ERR_INVALID;
   } else if (stats.reason == 1) {
     set_error("fj_solve: watchdog, %lld sweeps without convergence", (long long)stats.sweeps);
@@ -1770,6 +1783,7 @@ static fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, dou
 // certificate per right-hand side
 static fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, double omega,
                                   const fj_opts *o, float *Z_out, fj_stats *st_out) {
+  NvtxRange nv("fj_solve_batch");
   cudaStream_t st = g->stream;
   const int64_t n = g->n;
   const int K = k <= 2 ? 2 : 4;
@@ -1931,6 +1945,7 @@ static fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double 
 
 fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, const fj_opts *o,
                      float *z_out, fj_stats *st_out) {
+  NvtxRange nv("fj_solve");
   cudaStream_t st = g->stream;
   const int64_t n = g->n;
   fj_stats stats{};
@@ -1944,7 +1959,13 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   if (method == FJ_METHOD_AUTO)
     method = (omega == 1.0 || g->directed) ? FJ_METHOD_ASYNC : FJ_METHOD_COLORED;
   if (method == FJ_METHOD_COLORED && !g->colors) FJ_TRY(build_coloring(g));
-  if (method == FJ_METHOD_PUSH) return push_solve_impl(g, s_in, eps, omega, o, z_out, st_out);
+  if (method == FJ_METHOD_PUSH) {
+    if (o->z_init) {
+      set_error("fj_solve: z_init (warm start) is supported by ASYNC/COLORED, not PUSH");
+      return FJ_ERR_INVALID;
+    }
+    return push_solve_impl(g, s_in, eps, omega, o, z_out, st_out);
+  }
   const Layout &L = (method == FJ_METHOD_COLORED) ? g->color_layout : g->async_layout;
   const bool W = g->weighted != 0;
 
@@ -2001,8 +2022,20 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   }
   fj::count_launch();
   k_scalars<<<1, 1, 0, st>>>(smin, smax, eps, o->sigma, o->c, S);
+  const double *zinit = nullptr;
+  double *zinit_owned = nullptr;
+  if (o->z_init) {
+    if (is_device_ptr(o->z_init)) {
+      zinit = o->z_init;
+    } else {
+      FJ_CUDA(cudaMallocAsync(&zinit_owned, sizeof(double) * n, st));
+      FJ_CUDA(cudaMemcpyAsync(zinit_owned, o->z_init, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      zinit = zinit_owned;
+    }
+  }
   fj::count_launch();
-  k_init<<<gridn(n), kBlock, 0, st>>>(n, L.perm, L.rp, s.dev, S, s_l, z);
+  k_init<<<gridn(n), kBlock, 0, st>>>(n, L.perm, L.rp, s.dev, S, s_l, z, zinit);
+  if (zinit_owned) FJ_CUDA(cudaFreeAsync(zinit_owned, st));
 
   KP p = make_kp(g, L);
   p.s = s_l;
@@ -2149,6 +2182,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
 }
 
 fj_status measures_impl(fj_graph *g, const float *z_in, const float *s_in, fj_measures_t *out) {
+  NvtxRange nv("fj_measures");
   cudaStream_t st = g->stream;
   const int64_t n = g->n;
   const Layout &L = g->async_layout;

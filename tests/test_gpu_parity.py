@@ -453,3 +453,27 @@ def test_full_size_config_properties(dev, cid):
         np.testing.assert_allclose(zh[iso], s64[iso], rtol=0,
                                    atol=2e-7 * np.abs(s64[iso]).max() + 1e-12)
     g.close()
+
+
+# --------------------------------------------- warm start (resume, §5)
+@pytest.mark.parametrize("name", ["er2000", "rmat12w", "lattice64"])
+def test_warm_start_resume(dev, name):
+    """Resume from an earlier estimate (Lemma 3: any ẑ is a valid state): a
+    solve warm-started from a converged z needs ≤ 2 sweeps and still passes
+    the oracle's certificate; one warm-started from a loose (ε = 1e-2) z
+    converges in fewer sweeps than a cold start."""
+    rp, col, w, s, directed = TINY[name]()
+    n = len(rp) - 1
+    g = fj.Graph(n, _t(rp, dev), _t(col, dev), _t(w, dev), directed=directed)
+    z = torch.empty(n, dtype=torch.float32, device=dev)
+    zp = torch.empty(n, dtype=torch.float64, device=dev)
+    cold = fj.solve(g, _t(s, dev), z, 1e-6, 1.0)
+    fj.solve(g, _t(s, dev), z, 1e-2, 1.0)
+    warm = fj.solve(g, _t(s, dev), z, 1e-6, 1.0, z_init=z.double(), zprime_out=zp)
+    assert warm.sweeps < cold.sweeps
+    assert oracle.certificate(rp, col, w, s, zp.cpu().numpy(), 1e-6)[0] <= 1.0
+    again = fj.solve(g, _t(s, dev), z, 1e-6, 1.0, z_init=(zp - warm.c).contiguous())
+    assert again.sweeps <= 2
+    with pytest.raises(fj.FJError):
+        fj.solve(g, _t(s, dev), z, 1e-6, 1.0, method="push", z_init=(zp - warm.c).contiguous())
+    g.close()
