@@ -477,3 +477,24 @@ def test_warm_start_resume(dev, name):
     with pytest.raises(fj.FJError):
         fj.solve(g, _t(s, dev), z, 1e-6, 1.0, method="push", z_init=(zp - warm.c).contiguous())
     g.close()
+
+
+def test_unsorted_rows_canonicalised(dev):
+    """fj_graph_create accepts rows in any order (the library sorts them,
+    carrying the weights along): same z as the sorted input, bit for bit in
+    COLORED mode (deterministic)."""
+    rp, col, w, s, directed = TINY["rmat12w"]()
+    rng = np.random.default_rng(5)
+    col2 = col.copy()
+    w2 = w.copy()
+    for v in range(len(rp) - 1):
+        a, b = rp[v], rp[v + 1]
+        perm = rng.permutation(b - a)
+        col2[a:b] = col[a:b][perm]
+        w2[a:b] = w[a:b][perm]
+    outs = []
+    for c_, w_ in ((col, w), (col2, w2)):
+        g, z, zp, st = gpu_solve(dev, rp, c_, w_, s, 1e-6, 1.2, directed, method="colored")
+        outs.append(zp)
+        g.close()
+    assert np.array_equal(outs[0], outs[1])
