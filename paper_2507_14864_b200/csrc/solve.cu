@@ -2064,6 +2064,9 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   const size_t sweep_smem =
       tma ? (kBlock / 32) * sizeof(WarpSmem) : (kBlock / 32) * kWarpTileArcs * sizeof(double);
   FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem));
+  if (getenv("FJ_CARVEOUT"))  // shared-memory carveout in percent (diagnostics)
+    FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 atoi(getenv("FJ_CARVEOUT"))));
   const int grid = persistent_grid(fn, g->num_sms, sweep_smem);
   float ms_sweep = 0, ms_cert = 0;
   int rounds = 0;
