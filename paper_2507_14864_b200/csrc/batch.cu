@@ -1,0 +1,458 @@
+// batch.cu — batched right-hand sides: k ≤ 4 opinion
+// vectors share every CSR stream and every gathered ẑ line.
+#include "sweep_common.cuh"
+
+namespace fj {
+
+// ------------------------------------------------- batched RHS
+// K opinion vectors solved together: ẑ is stored node-major [n][K] so one
+// gathered 16–32-byte line serves all K right-hand sides, and the CSR stream
+// is read once per sweep for all of them.  Each RHS has its own shift c_r and
+// thresholds (Alg. 2, reading R5) and its own relax decision per row.
+template <int K>
+__device__ __forceinline__ void gatherK(const double *__restrict__ z, int j, double (&v)[K]) {
+  const double2 *q = reinterpret_cast<const double2 *>(z + (int64_t)j * K);
+#pragma unroll
+  for (int h = 0; h < K / 2; h++) {
+    const double2 a = q[h];
+    v[2 * h] = a.x;
+    v[2 * h + 1] = a.y;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void relax_rowK(const KP &p, const Scalars *SK, int row, int len,
+                                           dd (&tot)[K], const float (&sv)[K],
+                                           const double (&zi)[K], double d1, TAcc &t) {
+  double out[K];
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    const Scalars &S = SK[r];
+    const double sp = (double)sv[r] + S.c;
+    const double h = threshold(S, sp);
+    const double rho = residual_dd(tot[r], sp, d1, zi[r]);
+    const double ar = fabs(rho);
+    out[r] = zi[r];
+    if (ar > p.theta * h) {
+      out[r] = zi[r] + p.omega * rho / d1;
+      t.upd++;
+      t.eu += (unsigned long long)len;
+    }
+    if (!(ar <= S.sentinel)) t.bad = 1;
+  }
+  double2 *q = reinterpret_cast<double2 *>(p.z + (int64_t)row * K);
+#pragma unroll
+  for (int h = 0; h < K / 2; h++) __stcg(q + h, make_double2(out[2 * h], out[2 * h + 1]));
+}
+
+// warp unit (row > kWarpTileArcs arcs, or a piece of one), K right-hand sides
+template <bool W, int K>
+__device__ __forceinline__ void do_warpK(const KP &p, const Scalars *SK, const Task &tk, TAcc &t) {
+  constexpr int U = 4;
+  const int lane = threadIdx.x & 31;
+  const int row = tk.a, piece = tk.b, np = tk.kind >> 8, slot = tk.slot;
+  const int64_t a0 = tk.a0, a1 = tk.a1;
+  // row state on lanes: 1..K s, K+1..2K ẑ, 2K+1 d1, 2K+2/2K+3 row_ptr
+  double pre = 0.0;
+  if (lane >= 1 && lane <= K) pre = (double)__ldg(p.s + (int64_t)row * K + lane - 1);
+  else if (lane > K && lane <= 2 * K) pre = __ldcg(p.z + (int64_t)row * K + lane - K - 1);
+  else if (lane == 2 * K + 1 && W) pre = __ldg(p.d1 + row);
+  else if (lane == 2 * K + 2) pre = (double)__ldg(p.rp + row);
+  else if (lane == 2 * K + 3) pre = (double)__ldg(p.rp + row + 1);
+  dd a[K];
+#pragma unroll
+  for (int r = 0; r < K; r++) a[r] = dd{0.0, 0.0};
+  for (int64_t k0 = a0 + lane; k0 < a1; k0 += 32 * U) {
+    int j[U];
+    float wv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t k = k0 + 32 * u;
+      const bool ok = k < a1;
+      j[u] = ld_stream(p.col + (ok ? k : a0));
+      wv[u] = ok ? (W ? ld_stream(p.w + k) : 1.0f) : 0.0f;
+    }
+    double zj[U][K];
+#pragma unroll
+    for (int u = 0; u < U; u++) gatherK<K>(p.z, j[u], zj[u]);
+#pragma unroll
+    for (int u = 0; u < U; u++)
+#pragma unroll
+      for (int r = 0; r < K; r++) dd_addprod(a[r], (double)wv[u], zj[u][r]);
+  }
+#pragma unroll
+  for (int r = 0; r < K; r++)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc_merge(a[r], acc_shfl(a[r], 0xffffffffu, off));
+  float sv[K];
+  double zi[K];
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    sv[r] = (float)__shfl_sync(0xffffffffu, pre, 1 + r);
+    zi[r] = __shfl_sync(0xffffffffu, pre, 1 + K + r);
+  }
+  const double rbv = __shfl_sync(0xffffffffu, pre, 2 * K + 2);
+  const double rev = __shfl_sync(0xffffffffu, pre, 2 * K + 3);
+  const int len = (int)(rev - rbv);
+  const double d1 = W ? __shfl_sync(0xffffffffu, pre, 2 * K + 1) : (double)(len + 1);
+  if (lane != 0) return;
+  if (np > 1) {
+#pragma unroll
+    for (int r = 0; r < K; r++)
+      __stcg(p.partial + ((int64_t)slot + piece) * K + r, make_double2(a[r].hi, a[r].lo));
+    __threadfence();
+    const int old = atomicAdd(p.arrive + slot, 1);
+    if ((old + 1) % np != 0) return;
+    __threadfence();
+#pragma unroll
+    for (int r = 0; r < K; r++) a[r] = dd{0.0, 0.0};
+    for (int q = 0; q < np; q++)
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        const double2 x = __ldcg(p.partial + ((int64_t)slot + q) * K + r);
+        acc_merge(a[r], dd{x.x, x.y});
+      }
+  }
+  relax_rowK<K>(p, SK, row, len, a, sv, zi, d1, t);
+}
+
+// warp tile (short rows), K right-hand sides: G lanes per row accumulate
+// directly in registers (no shared memory), two row steps
+template <bool W, int K>
+__device__ __forceinline__ void tileK(const KP &p, const Scalars *SK, const Task &tk, TAcc &t) {
+  const int lane = threadIdx.x & 31;
+  const int cls = tk.kind & 0xff;
+  const int G = 1 << cls;
+  const int gl = lane & (G - 1);
+  const int ng = 32 >> cls;
+#pragma unroll 1
+  for (int q = 0; q < 2; q++) {
+    const int row = tk.a + q * ng + (lane >> cls);
+    const bool has = row < tk.b;
+    int64_t rb = 0, re = 0;
+    float sv[K];
+    double zi[K], d1 = 0.0;
+#pragma unroll
+    for (int r = 0; r < K; r++) {
+      sv[r] = 0.f;
+      zi[r] = 0.0;
+    }
+    if (has) {
+      rb = __ldg(p.rp + row);
+      re = __ldg(p.rp + row + 1);
+      if (gl == 0) {
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          sv[r] = __ldg(p.s + (int64_t)row * K + r);
+          zi[r] = __ldcg(p.z + (int64_t)row * K + r);
+        }
+        if (W) d1 = __ldg(p.d1 + row);
+      }
+    }
+    double a[K];
+#pragma unroll
+    for (int r = 0; r < K; r++) a[r] = 0.0;
+#pragma unroll 4
+    for (int64_t k = rb + gl; k < re; k += G) {
+      const int j = ld_stream(p.col + k);
+      const double wk = W ? (double)ld_stream(p.w + k) : 1.0;
+      double v[K];
+      gatherK<K>(p.z, j, v);
+#pragma unroll
+      for (int r = 0; r < K; r++) a[r] = fma(wk, v[r], a[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < K; r++)
+      for (int off = G >> 1; off > 0; off >>= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], off);
+    if (has && gl == 0) {
+      const int len = (int)(re - rb);
+      dd tot[K];
+#pragma unroll
+      for (int r = 0; r < K; r++) tot[r] = dd{a[r], 0.0};
+      relax_rowK<K>(p, SK, row, len, tot, sv, zi, W ? d1 : (double)(len + 1), t);
+    }
+  }
+}
+
+template <bool W, int K>
+__global__ void __launch_bounds__(kBlock, 4) k_sweep_batch(KP p, AsyncCtl *c) {
+  __shared__ Scalars sk[K];
+  if (threadIdx.x < K) sk[threadIdx.x] = p.sc[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const unsigned long long nr = (unsigned long long)(p.rphase_begin[1] - p.rphase_begin[0]);
+  const Task *items = p.rtasks + p.rphase_begin[0];
+  const unsigned long long limit = nr * (unsigned long long)p.max_sweeps;
+  unsigned long long my_epoch = ~0ull;
+  TAcc t{};
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&c->next, (unsigned long long)kClaim);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const unsigned int stop = *(volatile unsigned int *)&c->stop;
+    if (stop || base >= limit || nr == 0) break;
+    unsigned long long ep = base / nr, cnt = 0;
+    // bounded staleness: a warp may run at most kRing/2 - 1 sweeps ahead of
+    // the oldest unfinished one (keeps the per-sweep counter slots distinct;
+    // the oldest sweep's holders are never blocked, so this cannot deadlock)
+    if (lane == 0)
+      while (ep >= (unsigned long long)*(volatile unsigned int *)&c->epochs + kRing / 2 - 1 &&
+             !*(volatile unsigned int *)&c->stop)
+        __nanosleep(256);
+    __syncwarp();
+    for (int q = 0; q < kClaim; q++) {
+      const unsigned long long it = base + q;
+      if (it >= limit) break;
+      const unsigned long long e = it / nr;
+      if (e != ep) {
+        async_settle(c, ep, nr, t, cnt);
+        cnt = 0;
+        ep = e;
+      }
+      if (e != my_epoch) {
+        __threadfence();
+        my_epoch = e;
+      }
+      const Task tk = items[it - e * nr];
+      if ((tk.kind & 0xff) == kWarp) do_warpK<W, K>(p, sk, tk, t);
+      else tileK<W, K>(p, sk, tk, t);
+      cnt++;
+    }
+    async_settle(c, ep, nr, t, cnt);
+  }
+}
+
+// s (node order, k columns) → layout order, K padded columns (pad = last)
+__global__ void k_init_batch(int64_t n, int k, int K, const int32_t *__restrict__ perm,
+                             const int64_t *__restrict__ rp, const float *__restrict__ S,
+                             Scalars *__restrict__ SK, float *__restrict__ sK,
+                             double *__restrict__ zK) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t u = perm[i];
+  const bool empty = rp[i + 1] == rp[i];
+  for (int r = 0; r < K; r++) {
+    const float si = S[u * k + (r < k ? r : k - 1)];
+    if (!isfinite(si)) atomicOr(&SK[0].bad_input, 1);
+    sK[i * K + r] = si;
+    zK[i * K + r] = empty ? (double)si + SK[r].c : 0.0;  // d = 0 rows: exact
+  }
+}
+// column r of S (node order) → contiguous fp32 (for the per-RHS min/max)
+__global__ void k_column(int64_t n, int k, int r, const float *__restrict__ S, float *__restrict__ out) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u < n) out[u] = S[u * k + r];
+}
+// column r of the layout-order state → contiguous (for the per-RHS certificate)
+__global__ void k_columnL(int64_t n, int K, int r, const float *__restrict__ sK,
+                          const double *__restrict__ zK, float *__restrict__ s1,
+                          double *__restrict__ z1) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  s1[i] = sK[i * K + r];
+  z1[i] = zK[i * K + r];
+}
+__global__ void k_finalize_batch(int64_t n, int k, int K, const int32_t *__restrict__ iperm,
+                                 const double *__restrict__ zK, const Scalars *__restrict__ SK,
+                                 float *__restrict__ Z) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const int64_t i = iperm[u];
+  for (int r = 0; r < k; r++) Z[u * k + r] = (float)(zK[i * K + r] - SK[r].c);
+}
+
+// k ≤ 4 right-hand sides per solve, ASYNC schedule, one
+// certificate per right-hand side
+fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, double omega,
+                                  const fj_opts *o, float *Z_out, fj_stats *st_out) {
+  NvtxRange nv("fj_solve_batch");
+  cudaStream_t st = g->stream;
+  const int64_t n = g->n;
+  const int K = k <= 2 ? 2 : 4;
+  const Layout &L = g->async_layout;
+  const bool W = g->weighted != 0;
+  fj_stats stats{};
+  stats.colors = 1;
+  cudaEvent_t e0, e1, es0, es1;
+  FJ_CUDA(cudaEventCreate(&e0));
+  FJ_CUDA(cudaEventCreate(&e1));
+  FJ_CUDA(cudaEventCreate(&es0));
+  FJ_CUDA(cudaEventCreate(&es1));
+  FJ_CUDA(cudaEventRecord(e0, st));
+  const float *S = S_in;
+  float *S_owned = nullptr;
+  if (!is_device_ptr(S_in)) {
+    FJ_CUDA(cudaMallocAsync(&S_owned, sizeof(float) * n * k, st));
+    FJ_CUDA(cudaMemcpyAsync(S_owned, S_in, sizeof(float) * n * k, cudaMemcpyHostToDevice, st));
+    S = S_owned;
+  }
+  const bool zdev = is_device_ptr(Z_out);
+  float *sK = nullptr, *col = nullptr, *mm = nullptr, *s1 = nullptr, *Zd = nullptr;
+  double *zK = nullptr, *z1 = nullptr;
+  double2 *partial = nullptr;
+  int *arrive = nullptr, *arrive2 = nullptr;
+  Scalars *SK = nullptr;
+  AsyncCtl *actl = nullptr;
+  unsigned long long *outv = nullptr;
+  unsigned *ctl = nullptr;
+  const size_t np = (size_t)std::max(1, L.npartials);
+  FJ_CUDA(cudaMallocAsync(&sK, sizeof(float) * n * K, st));
+  FJ_CUDA(cudaMallocAsync(&zK, sizeof(double) * n * K, st));
+  FJ_CUDA(cudaMallocAsync(&col, sizeof(float) * n, st));
+  FJ_CUDA(cudaMallocAsync(&mm, sizeof(float) * 2, st));
+  FJ_CUDA(cudaMallocAsync(&s1, sizeof(float) * n, st));
+  FJ_CUDA(cudaMallocAsync(&z1, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&partial, sizeof(double2) * np * K, st));
+  FJ_CUDA(cudaMallocAsync(&arrive, sizeof(int) * np, st));
+  FJ_CUDA(cudaMallocAsync(&arrive2, sizeof(int) * np, st));
+  FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * np, st));
+  FJ_CUDA(cudaMallocAsync(&SK, sizeof(Scalars) * K, st));
+  FJ_CUDA(cudaMallocAsync(&actl, sizeof(AsyncCtl), st));
+  FJ_CUDA(cudaMallocAsync(&outv, sizeof(unsigned long long) * 8, st));
+  FJ_CUDA(cudaMallocAsync(&ctl, sizeof(unsigned) * 8, st));
+  if (!zdev) FJ_CUDA(cudaMallocAsync(&Zd, sizeof(float) * n * k, st));
+  // a2 per right-hand side: shift and thresholds (Alg. 2, reading R5)
+  {
+    size_t t1 = 0, t2 = 0;
+    FJ_CUDA(cub::DeviceReduce::Min(nullptr, t1, col, mm, n, st));
+    FJ_CUDA(cub::DeviceReduce::Max(nullptr, t2, col, mm + 1, n, st));
+    void *t = nullptr;
+    FJ_CUDA(cudaMallocAsync(&t, std::max(t1, t2), st));
+    for (int r = 0; r < K; r++) {
+      fj::count_launch();
+      k_column<<<gridn(n), kBlock, 0, st>>>(n, k, r < k ? r : k - 1, S, col);
+      FJ_CUDA(cub::DeviceReduce::Min(t, t1, col, mm, n, st));
+      FJ_CUDA(cub::DeviceReduce::Max(t, t2, col, mm + 1, n, st));
+      fj::count_launch();
+      k_scalars<<<1, 1, 0, st>>>(mm, mm + 1, eps, o->sigma, o->c, SK + r);
+    }
+    FJ_CUDA(cudaFreeAsync(t, st));
+  }
+  fj::count_launch();
+  k_init_batch<<<gridn(n), kBlock, 0, st>>>(n, k, K, L.perm, L.rp, S, SK, sK, zK);
+  KP p = make_kp(g, L);
+  p.s = sK;
+  p.z = zK;
+  p.sc = SK;
+  p.omega = omega;
+  p.theta = 1.0;
+  p.partial = partial;
+  p.arrive = arrive;
+  p.max_sweeps = o->max_sweeps;
+  const void *fn = K == 2 ? (W ? (const void *)k_sweep_batch<true, 2> : (const void *)k_sweep_batch<false, 2>)
+                          : (W ? (const void *)k_sweep_batch<true, 4> : (const void *)k_sweep_batch<false, 4>);
+  const int grid = persistent_grid(fn, g->num_sms);
+  const void *cf = W ? (const void *)k_pass<CERT, true> : (const void *)k_pass<CERT, false>;
+  const int cgrid = persistent_grid(cf, g->num_sms);
+  float ms_sweep = 0;
+  int rounds = 0;
+  for (;;) {
+    FJ_CUDA(cudaMemsetAsync(actl, 0, sizeof(AsyncCtl), st));
+    FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 8, st));
+    FJ_CUDA(cudaEventRecord(es0, st));
+    void *args[] = {&p, &actl};
+    fj::count_launch();
+    FJ_CUDA(cudaLaunchKernel(fn, grid, kBlock, args, 0, st));
+    fj::count_launch();
+    k_async_result<<<1, 1, 0, st>>>(actl, outv, (unsigned long long)p.max_sweeps);
+    FJ_CUDA(cudaEventRecord(es1, st));
+    unsigned long long h[8];
+    FJ_CUDA(cudaMemcpyAsync(h, outv, sizeof(h), cudaMemcpyDeviceToHost, st));
+    // compensated certificate of every right-hand side
+    double worst = 0.0;
+    for (int r = 0; r < k; r++) {
+      fj::count_launch();
+      k_columnL<<<gridn(n), kBlock, 0, st>>>(n, K, r, sK, zK, s1, z1);
+      KP q = make_kp(g, L);
+      q.s = s1;
+      q.z = z1;
+      q.sc = SK + r;
+      q.partial = partial;
+      q.arrive = arrive2;
+      q.ctr = ctl;
+      q.cert_max = outv + 4;
+      FJ_CUDA(cudaMemsetAsync(arrive2, 0, sizeof(int) * np, st));
+      FJ_CUDA(cudaMemsetAsync(outv + 4, 0, sizeof(unsigned long long), st));
+      void *cargs[] = {&q};
+      fj::count_launch();
+      FJ_CUDA(cudaLaunchKernel(cf, cgrid, kBlock, cargs, 0, st));
+      unsigned long long bits = 0;
+      FJ_CUDA(cudaMemcpyAsync(&bits, outv + 4, sizeof(bits), cudaMemcpyDeviceToHost, st));
+      FJ_CUDA(cudaStreamSynchronize(st));
+      const double ratio = __builtin_bit_cast(double, bits);
+      if (!(ratio <= worst)) worst = ratio;
+    }
+    FJ_CUDA(cudaStreamSynchronize(st));
+    float a = 0;
+    FJ_CUDA(cudaEventElapsedTime(&a, es0, es1));
+    ms_sweep += a;
+    stats.sweeps += (int64_t)h[0];
+    stats.relaxations += (int64_t)h[1];
+    stats.edge_updates += (int64_t)h[2];
+    stats.reason = (int)h[3];
+    stats.cert_ratio = worst;
+    if (stats.reason != 0 || stats.cert_ratio <= 1.0 || rounds >= o->cert_rounds) break;
+    rounds++;
+    p.theta *= 0.5;
+    p.max_sweeps = std::min(o->max_sweeps, 2000);
+  }
+  stats.cert_rounds = rounds;
+  stats.phases = stats.sweeps;
+  stats.rows_read = stats.sweeps * L.active_rows;
+  stats.arcs_read = stats.sweeps * L.m;
+  stats.relaxations += L.empty_rows * k;
+  fj::count_launch();
+  k_finalize_batch<<<gridn(n), kBlock, 0, st>>>(n, k, K, L.iperm, zK, SK, zdev ? Z_out : Zd);
+  if (!zdev) FJ_CUDA(cudaMemcpyAsync(Z_out, Zd, sizeof(float) * n * k, cudaMemcpyDeviceToHost, st));
+  Scalars hs{};
+  FJ_CUDA(cudaMemcpyAsync(&hs, SK, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaEventRecord(e1, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  float ms = 0;
+  FJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  stats.solve_ms = ms;
+  stats.sweep_ms = ms_sweep;
+  stats.c = hs.c;
+  stats.eps_prime = hs.eps_p;
+  for (void *q : {(void *)sK, (void *)zK, (void *)col, (void *)mm, (void *)s1, (void *)z1,
+                  (void *)partial, (void *)arrive, (void *)arrive2, (void *)SK, (void *)actl,
+                  (void *)outv, (void *)ctl, (void *)Zd, (void *)S_owned})
+    if (q) cudaFreeAsync(q, st);
+  for (cudaEvent_t e : {e0, e1, es0, es1}) cudaEventDestroy(e);
+  FJ_CUDA(cudaGetLastError());
+  fj_status rc = finish_status(hs, stats, o, omega);
+  if (st_out) *st_out = stats;
+  return rc;
+}
+
+}  // namespace fj
+
+extern "C" {
+
+fj_status fj_solve_batch(fj_graph_t g, const float *S, int k, double eps, double omega,
+                         const fj_opts *o, float *Z_out, fj_stats *st) {
+  fj_opts d;
+  fj_opts_default(&d);
+  if (o) {
+    d = *o;
+    if (!(d.sigma > 0)) d.sigma = 1e-5;
+    if (d.max_sweeps <= 0) d.max_sweeps = 1000000;
+    if (d.cert_rounds < 0) d.cert_rounds = 3;
+  }
+  if (!g || !S || !Z_out || k < 1 || k > 4) {
+    fj::set_error("fj_solve_batch: need non-null arguments and 1 <= k <= 4");
+    return FJ_ERR_INVALID;
+  }
+  if (!(eps > 0.0 && eps < 1.0) || !(omega > 0.0 && omega < 2.0)) {
+    fj::set_error("fj_solve_batch: eps in (0,1) and omega in (0,2) required");
+    return FJ_ERR_INVALID;
+  }
+  if (d.method != FJ_METHOD_AUTO && d.method != FJ_METHOD_ASYNC) {
+    fj::set_error("fj_solve_batch: only the ASYNC schedule is batched");
+    return FJ_ERR_INVALID;
+  }
+  return fj::batch_solve_impl(g, S, k, eps, omega, &d, Z_out, st);
+}
+
+
+}  // extern "C"

@@ -1,0 +1,351 @@
+// push.cu — FJ_METHOD_PUSH (§8 row a3 in its literal form): Alg. 1/3 made data
+// parallel — a pop phase and an fp64-atomic scatter phase per color — with the
+// certificate on the pull layout and residual replacement on resume.
+#include "sweep_common.cuh"
+
+namespace fj {
+
+// ------------------------------------------------------------ frontier push
+// FJ_METHOD_PUSH: Alg. 1 / Alg. 3 in data-parallel form on the push layout
+// (rows = in-rows: row v lists the u with an arc u→v, i.e. v's scatter list).
+// Per color phase:
+//   A (pop):  every v of the color with |r_v| > θ h_v takes q_v = ω r_v/(1+d_v),
+//             ẑ_v += q_v (equ:sor1), r_v ← (1−ω) r_v (equ:sor2); else q_v = 0;
+//   B (push): every popped v adds a_uv q_v to r_u for u ∈ N_v (equ:sor3)
+//             with fp64 atomics.
+// Rows of one color share no arc, so a phase equals popping its frontier one
+// node after another (Lemma 3 holds for any order).
+struct PP {
+  const int64_t *__restrict__ rp;
+  const int32_t *__restrict__ col;
+  const float *__restrict__ w;
+  const double *__restrict__ d1;
+  const Task *__restrict__ tasks;
+  const Task *__restrict__ wtasks;
+  const int *phase_begin, *wphase_begin;
+  const int64_t *crow;
+  int ncolors;
+  int64_t n;
+  const float *__restrict__ s;
+  double *z, *r, *q;
+  const Scalars *sc;
+  double omega, theta;
+  int max_sweeps;
+  unsigned *bar;
+  SweepCounters *cnt;
+  unsigned long long *out;
+};
+
+__device__ __forceinline__ void push_pop(const PP &p, const Scalars &S, int64_t b, int64_t e,
+                                         TAcc &t) {
+  for (int64_t v = b + blockIdx.x * (int64_t)kBlock + threadIdx.x; v < e;
+       v += (int64_t)gridDim.x * kBlock) {
+    const double sp = (double)p.s[v] + S.c;
+    const double h = threshold(S, sp);
+    const double rv = p.r[v];
+    double qv = 0.0;
+    if (fabs(rv) > p.theta * h) {                       // |r_v| > h_v
+      qv = p.omega * rv / p.d1[v];                      // ω r_v/(1+d_v)
+      p.z[v] += qv;                                     // equ:sor1
+      p.r[v] = rv - p.omega * rv;                       // equ:sor2: (1−ω) r_v
+      t.upd++;
+      t.eu += (unsigned long long)(p.rp[v + 1] - p.rp[v]);
+    }
+    if (!(fabs(rv) <= S.sentinel)) t.bad = 1;
+    p.q[v] = qv;
+  }
+}
+
+template <bool W>
+__device__ __forceinline__ void push_scatter_arcs(const PP &p, int64_t k0, int64_t k1, int step,
+                                                  double qv) {
+  for (int64_t k = k0; k < k1; k += step) {
+    const int u = ld_stream(p.col + k);
+    const double a = W ? (double)ld_stream(p.w + k) : 1.0;
+    atomicAdd(p.r + u, a * qv);                          // equ:sor3
+  }
+}
+
+template <bool W>
+__global__ void __launch_bounds__(kBlock, 4) k_push(PP p) {
+  __shared__ unsigned long long s_dec[3];
+  const Scalars S = *p.sc;
+  TAcc t{};
+  unsigned long long tot_upd = 0, tot_eu = 0;
+  int sweeps = 0, reason = 1;
+  const int lane = threadIdx.x & 31;
+  const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+  for (int sw = 0; sw < p.max_sweeps; ++sw) {
+    for (int k = 0; k < p.ncolors; ++k) {
+      push_pop(p, S, p.crow[k], p.crow[k + 1], t);
+      if (k == p.ncolors - 1) push_pop(p, S, p.crow[p.ncolors], p.n, t);  // rows with no in-arcs
+      grid_sync(p.bar);
+      // B: warp units (long scatter lists), then tile tasks (group per row)
+      const int w0 = p.wphase_begin[k], nw = p.wphase_begin[k + 1] - w0;
+      for (int wi = warp_id; wi < nw; wi += gridDim.x * (kBlock / 32)) {
+        const Task tk = p.wtasks[w0 + wi];
+        const double qv = p.q[tk.a];
+        if (qv != 0.0) push_scatter_arcs<W>(p, tk.a0 + lane, tk.a1, 32, qv);
+      }
+      const int t0 = p.phase_begin[k], nt = p.phase_begin[k + 1] - t0;
+      for (int ti = blockIdx.x; ti < nt; ti += gridDim.x) {
+        const Task tk = p.tasks[t0 + ti];
+        const int cls = tk.kind & 0xff;
+        const int G = 1 << cls;
+        const int row = tk.a + (threadIdx.x >> cls);
+        if (row < tk.b) {
+          const double qv = p.q[row];
+          if (qv != 0.0)
+            push_scatter_arcs<W>(p, p.rp[row] + (threadIdx.x & (G - 1)), p.rp[row + 1], G, qv);
+        }
+      }
+      grid_sync(p.bar);
+    }
+    unsigned long long u = t.upd, e = t.eu, b = t.bad;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      u += __shfl_xor_sync(0xffffffffu, u, off);
+      e += __shfl_xor_sync(0xffffffffu, e, off);
+      b |= __shfl_xor_sync(0xffffffffu, b, off);
+    }
+    SweepCounters *c = p.cnt + sw % 3;
+    if (lane == 0 && (u | e | b)) {
+      atomicAdd(&c->upd, u);
+      atomicAdd(&c->eu, e);
+      if (b) atomicOr(&c->bad, b);
+    }
+    t.upd = t.eu = t.bad = 0;
+    grid_sync(p.bar);
+    if (threadIdx.x == 0) {
+      s_dec[0] = __ldcg(&c->upd);
+      s_dec[1] = __ldcg(&c->eu);
+      s_dec[2] = __ldcg(&c->bad);
+      if (blockIdx.x == 0) {
+        SweepCounters *zc = p.cnt + (sw + 2) % 3;
+        zc->upd = zc->eu = zc->bad = 0;
+      }
+    }
+    __syncthreads();
+    tot_upd += s_dec[0];
+    tot_eu += s_dec[1];
+    sweeps = sw + 1;
+    const bool bad = s_dec[2] != 0, done = s_dec[0] == 0;
+    __syncthreads();
+    if (bad) { reason = 2; break; }
+    if (done) { reason = 0; break; }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.out[0] = (unsigned long long)sweeps;
+    p.out[1] = tot_upd;
+    p.out[2] = tot_eu;
+    p.out[3] = (unsigned long long)reason;
+  }
+}
+
+// push-layout init: s in push order, ẑ' = 0, r = s' (Alg. 1 init)
+__global__ void k_push_init(int64_t n, const int32_t *__restrict__ perm, const float *__restrict__ s,
+                            Scalars *__restrict__ S, float *__restrict__ s_l, double *__restrict__ z,
+                            double *__restrict__ r) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float si = s[perm[i]];
+  if (!isfinite(si)) atomicOr(&S->bad_input, 1);
+  s_l[i] = si;
+  z[i] = 0.0;
+  r[i] = (double)si + S->c;
+}
+
+// dst[i] = src[idx[i]]
+__global__ void k_gather64(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ src,
+                           double *__restrict__ dst) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+// dst[idx[i]] = src[i]
+__global__ void k_scatter64(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ src,
+                            double *__restrict__ dst) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[idx[i]] = src[i];
+}
+
+// FJ_METHOD_PUSH: frontier push on the in-row layout; certificate on the pull
+// layout (the residual needs out-rows); residual replacement on resume.
+fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double omega,
+                                 const fj_opts *o, float *z_out, fj_stats *st_out) {
+  cudaStream_t st = g->stream;
+  const int64_t n = g->n;
+  const bool colored = omega != 1.0;
+  if (colored && !g->colors) FJ_TRY(build_coloring(g));
+  Layout &P = colored ? g->push_color_layout : g->push_layout;
+  if (!P.tasks)
+    FJ_TRY(build_layout_from_out(g, g->in_rp, g->in_col, g->in_w, colored ? g->colors : nullptr,
+                                 colored ? g->ncolors : 1, &P, true));
+  const Layout &L = g->async_layout;
+  const bool W = g->weighted != 0;
+  fj_stats stats{};
+  stats.colors = P.ncolors;
+
+  cudaEvent_t e0, e1, es0, es1;
+  FJ_CUDA(cudaEventCreate(&e0));
+  FJ_CUDA(cudaEventCreate(&e1));
+  FJ_CUDA(cudaEventCreate(&es0));
+  FJ_CUDA(cudaEventCreate(&es1));
+  FJ_CUDA(cudaEventRecord(e0, st));
+  Staged s{};
+  FJ_TRY(stage_in(s_in, n, st, s));
+  const bool zdev = is_device_ptr(z_out);
+  const bool zpdev = o->zprime_out && is_device_ptr(o->zprime_out);
+  float *sP = nullptr, *sL = nullptr, *smin = nullptr, *zo = nullptr;
+  double *zP = nullptr, *rP = nullptr, *qP = nullptr, *zL = nullptr, *tmp = nullptr, *zp = nullptr;
+  double *RL = nullptr;
+  Scalars *S = nullptr;
+  unsigned *ctl = nullptr;
+  SweepCounters *cnt = nullptr;
+  unsigned long long *outv = nullptr;
+  FJ_CUDA(cudaMallocAsync(&sP, sizeof(float) * n, st));
+  FJ_CUDA(cudaMallocAsync(&sL, sizeof(float) * n, st));
+  FJ_CUDA(cudaMallocAsync(&zP, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&rP, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&qP, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&zL, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&tmp, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&RL, sizeof(double) * n, st));
+  FJ_CUDA(cudaMallocAsync(&smin, sizeof(float) * 2, st));
+  FJ_CUDA(cudaMallocAsync(&S, sizeof(Scalars), st));
+  FJ_CUDA(cudaMallocAsync(&ctl, sizeof(unsigned) * kCtlWords, st));
+  FJ_CUDA(cudaMallocAsync(&cnt, sizeof(SweepCounters) * 3, st));
+  FJ_CUDA(cudaMallocAsync(&outv, sizeof(unsigned long long) * 8, st));
+  if (!zdev) FJ_CUDA(cudaMallocAsync(&zo, sizeof(float) * n, st));
+  if (o->zprime_out && !zpdev) FJ_CUDA(cudaMallocAsync(&zp, sizeof(double) * n, st));
+  {
+    size_t t1 = 0, t2 = 0;
+    FJ_CUDA(cub::DeviceReduce::Min(nullptr, t1, s.dev, smin, n, st));
+    FJ_CUDA(cub::DeviceReduce::Max(nullptr, t2, s.dev, smin + 1, n, st));
+    void *t = nullptr;
+    FJ_CUDA(cudaMallocAsync(&t, std::max(t1, t2), st));
+    FJ_CUDA(cub::DeviceReduce::Min(t, t1, s.dev, smin, n, st));
+    FJ_CUDA(cub::DeviceReduce::Max(t, t2, s.dev, smin + 1, n, st));
+    FJ_CUDA(cudaFreeAsync(t, st));
+  }
+  fj::count_launch();
+  k_scalars<<<1, 1, 0, st>>>(smin, smin + 1, eps, o->sigma, o->c, S);
+  fj::count_launch();
+  k_push_init<<<gridn(n), kBlock, 0, st>>>(n, P.perm, s.dev, S, sP, zP, rP);
+  fj::count_launch();
+  k_init<<<gridn(n), kBlock, 0, st>>>(n, L.perm, L.rp, s.dev, S, sL, zL);
+
+  PP pp{};
+  pp.rp = P.rp;
+  pp.col = P.col;
+  pp.w = P.w;
+  pp.d1 = P.d1;
+  pp.tasks = P.tasks;
+  pp.wtasks = P.wtasks;
+  pp.phase_begin = P.d_phase_begin;
+  pp.wphase_begin = P.d_wphase_begin;
+  pp.crow = P.d_crow;
+  pp.ncolors = P.ncolors;
+  pp.n = n;
+  pp.s = sP;
+  pp.z = zP;
+  pp.r = rP;
+  pp.q = qP;
+  pp.sc = S;
+  pp.omega = omega;
+  pp.theta = 1.0;
+  pp.max_sweeps = o->max_sweeps;
+  pp.bar = ctl + 8;
+  pp.cnt = cnt;
+  pp.out = outv;
+  KP kq = make_kp(g, L);
+  kq.s = sL;
+  kq.z = zL;
+  kq.sc = S;
+  kq.ctr = ctl + 5;
+  kq.cert_max = outv + 4;
+  kq.rout = RL;
+  double2 *partial = nullptr;  // long-row partials of the pull layout (certificate)
+  int *arrive = nullptr;
+  FJ_CUDA(cudaMallocAsync(&partial, sizeof(double2) * std::max(1, L.npartials), st));
+  FJ_CUDA(cudaMallocAsync(&arrive, sizeof(int) * std::max(1, L.npartials), st));
+  FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
+  kq.partial = partial;
+  kq.arrive = arrive;
+
+  const void *fn = W ? (const void *)k_push<true> : (const void *)k_push<false>;
+  const int grid = persistent_grid(fn, g->num_sms);
+  const void *cf = W ? (const void *)k_pass<CERT, true> : (const void *)k_pass<CERT, false>;
+  float ms_sweep = 0;
+  int rounds = 0;
+  for (;;) {
+    FJ_CUDA(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * kCtlWords, st));
+    FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(SweepCounters) * 3, st));
+    FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 8, st));
+    void *args[] = {&pp};
+    FJ_CUDA(cudaEventRecord(es0, st));
+    fj::count_launch();
+    FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, 0, st));
+    FJ_CUDA(cudaEventRecord(es1, st));
+    // certificate on the pull layout: ẑ' push order → node order → pull order
+    fj::count_launch();
+    k_scatter64<<<gridn(n), kBlock, 0, st>>>(n, P.perm, zP, tmp);
+    fj::count_launch();
+    k_gather64<<<gridn(n), kBlock, 0, st>>>(n, L.perm, tmp, zL);
+    void *cargs[] = {&kq};
+    fj::count_launch();
+    FJ_CUDA(cudaLaunchKernel(cf, persistent_grid(cf, g->num_sms), kBlock, cargs, 0, st));
+    unsigned long long h[8];
+    FJ_CUDA(cudaMemcpyAsync(h, outv, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FJ_CUDA(cudaStreamSynchronize(st));
+    float a = 0;
+    FJ_CUDA(cudaEventElapsedTime(&a, es0, es1));
+    ms_sweep += a;
+    stats.sweeps += (int64_t)h[0];
+    stats.relaxations += (int64_t)h[1];
+    stats.edge_updates += (int64_t)h[2];
+    stats.reason = (int)h[3];
+    stats.cert_ratio = __builtin_bit_cast(double, h[4]);
+    if (stats.reason != 0) break;
+    if (stats.cert_ratio <= 1.0 || rounds >= o->cert_rounds) break;
+    rounds++;
+    // residual replacement (Lemma 3: r = s' − (I+L)ẑ'), pull order → push order
+    fj::count_launch();
+    k_scatter64<<<gridn(n), kBlock, 0, st>>>(n, L.perm, RL, tmp);
+    fj::count_launch();
+    k_gather64<<<gridn(n), kBlock, 0, st>>>(n, P.perm, tmp, rP);
+    pp.theta *= 0.5;
+    pp.max_sweeps = std::min(o->max_sweeps, 2000);
+  }
+  stats.cert_rounds = rounds;
+  stats.phases = stats.sweeps * P.ncolors * 2;
+  stats.rows_read = stats.sweeps * n;
+  stats.arcs_read = stats.edge_updates;
+  fj::count_launch();
+  k_finalize<<<gridn(n), kBlock, 0, st>>>(n, P.iperm, zP, S, zdev ? z_out : zo,
+                                          o->zprime_out ? (zpdev ? o->zprime_out : zp) : nullptr);
+  if (!zdev) FJ_CUDA(cudaMemcpyAsync(z_out, zo, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+  if (o->zprime_out && !zpdev)
+    FJ_CUDA(cudaMemcpyAsync(o->zprime_out, zp, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  Scalars hs{};
+  FJ_CUDA(cudaMemcpyAsync(&hs, S, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaEventRecord(e1, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  float ms = 0;
+  FJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  stats.solve_ms = ms;
+  stats.sweep_ms = ms_sweep;
+  stats.c = hs.c;
+  stats.eps_prime = hs.eps_p;
+  for (void *q : {(void *)sP, (void *)sL, (void *)zP, (void *)rP, (void *)qP, (void *)zL,
+                  (void *)tmp, (void *)RL, (void *)smin, (void *)S, (void *)ctl, (void *)cnt,
+                  (void *)outv, (void *)zo, (void *)zp, (void *)s.owned, (void *)partial,
+                  (void *)arrive})
+    if (q) cudaFreeAsync(q, st);
+  for (cudaEvent_t e : {e0, e1, es0, es1}) cudaEventDestroy(e);
+  FJ_CUDA(cudaGetLastError());
+  fj_status rc = finish_status(hs, stats, o, omega);
+  if (st_out) *st_out = stats;
+  return rc;
+}
+
+}  // namespace fj

@@ -1,0 +1,667 @@
+// sweep_common.cuh — device building blocks shared by the sweep, push and
+// batch translation units (internal; not part of the ABI).  See solve.cu for
+// the method notes (Theorem 3 sweep form of the paper's push).
+#pragma once
+#include <stdlib.h>
+
+#include <algorithm>
+#include <cuda/atomic>
+#include <cub/cub.cuh>
+#include <nvtx3/nvToolsExt.h>
+#include <type_traits>
+
+#include "fj_internal.cuh"
+
+namespace fj {
+
+struct NvtxRange {  // tracing: one NVTX range per library phase (nsys/ncu timelines)
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+enum Mode { RELAX = 0, CERT = 1, DIS = 2, SPMV = 3 };
+constexpr int kClaim = 16;  // work items per dynamic claim
+constexpr int kCtlWords = 256;  // control block: [0..2] claim counters, [5] cert counter, [8..] barrier
+
+struct Scalars {
+  double c;        // shift (Alg. 2; reading R5)
+  double eps_p;    // ε' = σε/(c+σ)
+  double hs;       // h = hs·s'            (s_min ≥ 0)
+  double heps;     // h = heps·max(hs·s', σ) (s_min < 0, floored, R5)
+  double sigma;
+  double sentinel; // divergence sentinel 1e6·max|s'|
+  int floored;
+  int bad_input;
+};
+
+struct SweepCounters {
+  unsigned long long upd, eu;
+  unsigned long long bad, pad;
+};
+
+struct KP {
+  const int64_t *__restrict__ rp;
+  const int32_t *__restrict__ col;
+  const float *__restrict__ w;
+  const double *__restrict__ d1;
+  const Task *__restrict__ tasks;
+  const Task *__restrict__ wtasks;
+  const Task *__restrict__ rtasks;
+  const int *rphase_begin;
+  const float *__restrict__ s;  // layout order
+  double *z;                    // ẑ' (RELAX/CERT) or z (DIS), layout order
+  const Scalars *sc;
+  double omega;
+  double theta;  // sweep relaxes |r| > θ·h: θ = 1 first, < 1 on certificate resumes
+  double2 *partial;
+  int *arrive;
+  const int *phase_begin;
+  const int *wphase_begin;
+  int ncolors;
+  int ntasks_all;
+  int nwtasks_all;
+  int max_sweeps;
+  unsigned *ctr;          // [3]
+  SweepCounters *cnt;     // [3]
+  unsigned *bar;          // [2]
+  unsigned long long *out;  // [4] sweeps, relaxations, edge updates, reason
+  unsigned long long *cert_max;  // double bits
+  double *dis;
+  double *rout;                  // CERT: optional residual output (layout order)
+  int dbg;                       // diagnostics (env FJ_DBG_SKIP): 1 skip warp units, 2 skip tiles
+  int dyn;                       // dynamic work claiming in k_sweep (env FJ_DYN)
+  int symm;                      // alternate sweep direction (env FJ_SYMM)
+};
+
+// CSR streams are read once per sweep: read-only path, no L1 allocation, so
+// L1 keeps the gathered ẑ values (hub rows are hit by many arcs)
+__device__ __forceinline__ int ld_stream(const int *q) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(q));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float *q) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(q));
+  return v;
+}
+// ẑ gathers: L1-cached.  ẑ is written during the sweep kernel, so an SM may
+// read a value another SM has since replaced; asynchronous relaxation allows
+// that (Lemma 3 holds for any order).  Every grid barrier executes a
+// gpu-scope fence, which invalidates L1, so the certifying zero-update sweep
+// and every color phase read current values.
+// (weak loads: the compiler may batch them; __ldca compiles to a strong load)
+__device__ __forceinline__ double ld_z(const double *q) { return *q; }
+
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ void dd_add(dd &a, double x) {
+  double s = a.hi + x;
+  double bb = s - a.hi;
+  a.lo += (a.hi - (s - bb)) + (x - bb);
+  a.hi = s;
+}
+__device__ __forceinline__ void dd_addprod(dd &a, double x, double y) {
+  double p = x * y;
+  double e = fma(x, y, -p);
+  dd_add(a, p);
+  a.lo += e;
+}
+
+template <int MODE>
+struct AccT {
+  using T = double;
+};
+template <>
+struct AccT<CERT> {
+  using T = dd;
+};
+
+__device__ __forceinline__ void acc_zero(double &a) { a = 0.0; }
+__device__ __forceinline__ void acc_zero(dd &a) { a.hi = a.lo = 0.0; }
+__device__ __forceinline__ double acc_shfl(double a, unsigned mask, int off) {
+  return __shfl_xor_sync(mask, a, off);
+}
+__device__ __forceinline__ dd acc_shfl(dd a, unsigned mask, int off) {
+  dd b;
+  b.hi = __shfl_xor_sync(mask, a.hi, off);
+  b.lo = __shfl_xor_sync(mask, a.lo, off);
+  return b;
+}
+__device__ __forceinline__ void acc_merge(double &a, double b) { a += b; }
+__device__ __forceinline__ void acc_merge(dd &a, dd b) {
+  dd_add(a, b.hi);
+  a.lo += b.lo;
+}
+
+struct TAcc {
+  unsigned long long upd, eu, bad;
+  double certmax, dis;
+};
+
+// ---------------------------------------------------------- per-row finish
+__device__ __forceinline__ double threshold(const Scalars &S, double sp) {
+  // h_v (reading R5): ε' s'_v, or (ε/2)·max(σ s'_v/(c+σ), σ) for signed s
+  return S.floored ? S.heps * fmax(S.hs * sp, S.sigma) : S.hs * sp;
+}
+
+// residual r_i = s'_i − (1+d_i) ẑ_i + Σ_j a_ij ẑ_j combined in double-double:
+// at hub rows (d ~ 1e4–1e5) the two large terms cancel to ~h ≈ 5e-12, below
+// the rounding noise of a plain fp64 combination
+__device__ __forceinline__ double residual_dd(dd sum, double sp, double d1, double zi) {
+  dd_add(sum, sp);
+  dd_addprod(sum, -d1, zi);
+  return sum.hi + sum.lo;
+}
+
+// relax one row from its residual; row state loaded by the caller (prefetched)
+__device__ __forceinline__ void relax_row_pre(const KP &p, const Scalars &S, int row, int len,
+                                              dd total, float sv, double zi, double d1, TAcc &t) {
+  const double sp = (double)sv + S.c;
+  const double h = threshold(S, sp);
+  const double rho = residual_dd(total, sp, d1, zi);
+  const double ar = fabs(rho);
+  if (ar > p.theta * h) {
+    __stcg(p.z + row, zi + p.omega * rho / d1);
+    t.upd++;
+    t.eu += (unsigned long long)len;
+  }
+  if (!(ar <= S.sentinel)) t.bad = 1;
+}
+
+template <bool W>
+__device__ __forceinline__ void cert_row(const KP &p, const Scalars &S, int row, int len, dd total,
+                                         TAcc &t) {
+  const double sp = (double)p.s[row] + S.c;
+  const double h = threshold(S, sp);
+  const double zi = p.z[row];
+  const double d1 = W ? p.d1[row] : (double)(len + 1);
+  const double R = residual_dd(total, sp, d1, zi);
+  if (p.rout) p.rout[row] = R;
+  const double ratio = fabs(R) / h;
+  if (!(ratio <= t.certmax)) t.certmax = ratio;  // NaN sticks
+}
+
+// arc accumulation
+template <int MODE, bool W>
+__device__ __forceinline__ void arc_acc(typename AccT<MODE>::T &a, const KP &p, int64_t k,
+                                        double zr) {
+  const int j = ld_stream(p.col + k);
+  const double wk = W ? (double)ld_stream(p.w + k) : 1.0;
+  if constexpr (MODE == RELAX) {
+    a = fma(wk, ld_z(p.z + j), a);
+  } else if constexpr (MODE == CERT) {
+    if (W) dd_addprod(a, wk, p.z[j]);
+    else dd_add(a, p.z[j]);
+  } else if constexpr (MODE == SPMV) {
+    a = fma(wk, p.z[j], a);
+  } else {
+    const double dz = zr - p.z[j];
+    a = fma(wk * dz, dz, a);
+  }
+}
+
+template <int MODE, int G, bool W>
+__device__ __forceinline__ void do_group(const KP &p, const Scalars &S, int rb, int re, TAcc &t) {
+  using A = typename AccT<MODE>::T;
+  const int lane = threadIdx.x & (G - 1);
+  const int grp = threadIdx.x / G;
+  const unsigned gmask =
+      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  for (int row = rb + grp; row < re; row += kBlock / G) {
+    const int64_t beg = p.rp[row], end = p.rp[row + 1];
+    const double zr = (MODE == DIS) ? p.z[row] : 0.0;
+    A a;
+    acc_zero(a);
+#pragma unroll 4
+    for (int64_t k = beg + lane; k < end; k += G) arc_acc<MODE, W>(a, p, k, zr);
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) acc_merge(a, acc_shfl(a, gmask, off));
+    if (lane == 0) {
+      const int len = (int)(end - beg);
+      static_assert(MODE != RELAX, "RELAX runs as warp tiles / warp units");
+      if constexpr (MODE == CERT) cert_row<W>(p, S, row, len, a, t);
+      else if constexpr (MODE == SPMV) p.rout[row] = a;
+      else t.dis += a;
+    }
+  }
+}
+
+// block-wide deterministic reduction; result valid in thread 0
+template <class A>
+__device__ __forceinline__ A block_reduce(A a, A *sm) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc_merge(a, acc_shfl(a, 0xffffffffu, off));
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sm[w] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < kBlock / 32; i++) acc_merge(a, sm[i]);
+  }
+  __syncthreads();
+  return a;
+}
+
+// Warp unit (rows above 256 arcs): one warp accumulates a whole row or one
+// kWarpPiece-arc piece of it in registers — 8 independent col/w loads, then 8
+// ẑ gathers per lane per step — and reduces with shuffles (no block barrier).
+// Pieces of one row are combined by the last-arriving warp in piece order
+// (deterministic).
+template <int MODE, bool W>
+__device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Task &tk, TAcc &t) {
+  // rows above 256 arcs accumulate in double-double for RELAX and CERT
+  using A = typename std::conditional<MODE == DIS || MODE == SPMV, double, dd>::type;
+#ifndef FJ_WU
+#define FJ_WU 8
+#endif
+  constexpr int U = FJ_WU;  // arcs per lane per step (loads in flight)
+  const int lane = threadIdx.x & 31;
+  const int row = tk.a, piece = tk.b, np = tk.kind >> 8, slot = tk.slot;
+  const int64_t a0 = tk.a0, a1 = tk.a1;
+  const double zr = (MODE == DIS) ? p.z[row] : 0.0;
+  // RELAX: lanes 1..5 fetch the row state now so that the final relax does
+  // not wait on another round trip (s, ẑ_row, 1+d, row_ptr pair)
+  double pre = 0.0;
+  if constexpr (MODE == RELAX) {
+    if (lane == 1) pre = (double)__ldg(p.s + row);
+    else if (lane == 2) pre = __ldcg(p.z + row);
+    else if (lane == 3 && W) pre = __ldg(p.d1 + row);
+    else if (lane == 4) pre = (double)__ldg(p.rp + row);
+    else if (lane == 5) pre = (double)__ldg(p.rp + row + 1);
+  }
+  A a;
+  acc_zero(a);
+  for (int64_t k0 = a0 + lane; k0 < a1; k0 += 32 * U) {
+    // stage 1: all column / weight loads of this step (out-of-range lanes
+    // read a valid dummy slot and contribute weight 0)
+    int j[U];
+    float wv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t k = k0 + 32 * u;
+      const bool ok = k < a1;
+      j[u] = ld_stream(p.col + (ok ? k : a0));
+      wv[u] = W ? ld_stream(p.w + (ok ? k : a0)) : 1.0f;
+      if (!ok) wv[u] = 0.0f;
+    }
+    // stage 2: all gathers
+    double zj[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
+    // stage 3: accumulate
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if constexpr (MODE == SPMV) {
+        a = fma((double)wv[u], zj[u], a);
+      } else if constexpr (MODE != DIS) {
+#ifdef FJ_PLAIN_WARP
+        a.hi = fma((double)wv[u], zj[u], a.hi);  // diagnostics only
+#else
+        dd_addprod(a, (double)wv[u], zj[u]);
+#endif
+      } else {
+        const double dz = zr - zj[u];
+        a = fma((double)wv[u] * dz, dz, a);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc_merge(a, acc_shfl(a, 0xffffffffu, off));
+  float sv = 0.f;
+  double zi = 0.0, d1 = 0.0;
+  int len = 0;
+  if constexpr (MODE == RELAX) {
+    sv = (float)__shfl_sync(0xffffffffu, pre, 1);
+    zi = __shfl_sync(0xffffffffu, pre, 2);
+    const double rb = __shfl_sync(0xffffffffu, pre, 4), re = __shfl_sync(0xffffffffu, pre, 5);
+    len = (int)(re - rb);
+    d1 = W ? __shfl_sync(0xffffffffu, pre, 3) : (double)(len + 1);
+  }
+  if (lane != 0) return;
+  if constexpr (MODE == DIS) {
+    t.dis += a;
+    return;
+  } else if constexpr (MODE == SPMV) {
+    atomicAdd(p.rout + row, a);  // pieces of one row add up (y zeroed first)
+    return;
+  } else {
+    if (np > 1) {
+      __stcg(p.partial + slot + piece, make_double2(a.hi, a.lo));
+      __threadfence();
+      // cumulative arrival count: the np-th, 2np-th, ... arrival finishes the
+      // row (no reset, so overlapping sweeps of the barrier-free kernel can
+      // never lose an arrival; mixing partials of two sweeps is still a
+      // valid relaxation amount by Lemma 3 and the certificate decides)
+      const int old = atomicAdd(p.arrive + slot, 1);
+      if ((old + 1) % np != 0) return;
+      __threadfence();
+      acc_zero(a);
+      for (int q = 0; q < np; q++) {  // fixed order ⇒ deterministic row sum
+        const double2 x = __ldcg(p.partial + slot + q);
+        acc_merge(a, dd{x.x, x.y});
+      }
+    }
+    if constexpr (MODE == RELAX) {
+      // a non-final piece returned above; a multi-piece row is finished by
+      // the last-arriving warp, whose prefetched ẑ_row is still current (only
+      // this row's finisher writes it, once per phase)
+      relax_row_pre(p, S, row, len, a, sv, zi, d1, t);
+    } else {
+      const int lenc = (int)(__ldg(p.rp + row + 1) - __ldg(p.rp + row));
+      cert_row<W>(p, S, row, lenc, a, t);
+    }
+  }
+}
+
+// RELAX on a GROUP task, smem-staged (the hot loop).  All global loads of
+// the task are issued up front for memory-level parallelism:
+//   row state of the task's rows (rp pair, s, ẑ, 1+d) — one G-lane group per row;
+//   phase 1: the task's contiguous arc range, ≤ kTileArcs = 8 per thread:
+//            col + w loads, then the ẑ gathers, products a_ij ẑ_j → smem;
+//   phase 2: each group sums its row's products from smem, lane 0 relaxes.
+// One __syncthreads per task (smem double-buffered across tasks).
+template <bool W>
+__device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, const Task &tk,
+                                                TAcc &t, double *wprod) {
+  constexpr int U = kWarpTileArcs / 32;
+  const int lane = threadIdx.x & 31;
+  const int cls = tk.kind & 0xff;
+  const int G = 1 << cls;
+  const int gl = lane & (G - 1);
+  const int ng = 32 >> cls;  // groups per warp = rows per step
+  // row state is loaded per step in phase 2: loading both steps up front
+  // spilled (148 B/thread) and was 9 % slower on C4, 16 % on C5
+  int64_t rb[2], re[2];
+  float sv[2];
+  double zi[2], d1[2];
+  const int64_t a0 = tk.a0;
+  const int na = (int)(tk.a1 - a0);
+  int j[U];
+  float wv[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int e = u * 32 + lane;
+    const bool ok = e < na;
+    j[u] = ld_stream(p.col + a0 + (ok ? e : 0));
+    wv[u] = W ? ld_stream(p.w + a0 + (ok ? e : 0)) : 1.0f;
+  }
+  double zj[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int e = u * 32 + lane;
+    if (e < na) wprod[e] = (double)wv[u] * zj[u];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    {
+      const int row = tk.a + q * ng + (lane >> cls);
+      rb[q] = re[q] = 0;
+      sv[q] = 0.f;
+      zi[q] = d1[q] = 0.0;
+      if (row < tk.b) {
+        rb[q] = __ldg(p.rp + row);
+        re[q] = __ldg(p.rp + row + 1);
+        if (gl == 0) {
+          sv[q] = __ldg(p.s + row);
+          zi[q] = __ldcg(p.z + row);
+          if (W) d1[q] = __ldg(p.d1 + row);
+        }
+      }
+    }
+    double a = 0.0;
+    const int kb = (int)(rb[q] - a0), ke = (int)(re[q] - a0);
+    for (int k = kb + gl; k < ke; k += G) a += wprod[k];
+    for (int off = G >> 1; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+    const int row = tk.a + q * ng + (lane >> cls);
+    if (row < tk.b && gl == 0) {
+      const int len = (int)(re[q] - rb[q]);
+      relax_row_pre(p, S, row, len, dd{a, 0.0}, sv[q], zi[q], W ? d1[q] : (double)(len + 1), t);
+    }
+  }
+  __syncwarp();  // the slice is reused by this warp's next task
+}
+
+template <int MODE, bool W>
+__device__ __forceinline__ void dispatch_tile(const KP &p, const Scalars &S, const Task &tk, TAcc &t) {
+  switch (tk.kind & 0xff) {
+    case kG1: do_group<MODE, 1, W>(p, S, tk.a, tk.b, t); break;
+    case kG2: do_group<MODE, 2, W>(p, S, tk.a, tk.b, t); break;
+    case kG4: do_group<MODE, 4, W>(p, S, tk.a, tk.b, t); break;
+    case kG8: do_group<MODE, 8, W>(p, S, tk.a, tk.b, t); break;
+    case kG16: do_group<MODE, 16, W>(p, S, tk.a, tk.b, t); break;
+    default: do_group<MODE, 32, W>(p, S, tk.a, tk.b, t); break;
+  }
+}
+
+// Grid-wide barrier of a cooperative launch (all CTAs co-resident): one
+// arrival counter and a generation word (sense reversal).  The gpu-scope
+// fences order every CTA's prior writes (bar.sync makes them cumulative) and
+// invalidate L1, so plain ẑ loads after the barrier see current values.
+// (A two-level tree measured slower: 6.7 vs 4.5 µs per barrier on 592 CTAs.)
+// bar layout: [0] count, [1] generation
+__device__ __forceinline__ void grid_sync(unsigned *bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    cuda::atomic_ref<unsigned, cuda::thread_scope_device> cnt(bar[0]), gen(bar[1]);
+    const unsigned g = gen.load(cuda::memory_order_relaxed);
+    __threadfence();
+    if (cnt.fetch_add(1u, cuda::memory_order_acq_rel) == gridDim.x - 1) {
+      cnt.store(0u, cuda::memory_order_relaxed);
+      gen.store(g + 1u, cuda::memory_order_release);
+    } else {
+      while (gen.load(cuda::memory_order_acquire) == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+#ifndef FJ_MINB
+#define FJ_MINB 4
+#endif
+
+// ------------------------------------------- barrier-free asynchronous sweeps
+// ASYNC with one phase: warps claim batches of work items from one monotonic
+// counter; item c belongs to epoch (sweep) c / nr.  Epochs therefore run back
+// to back without a grid barrier, and the claim order balances the load.  The
+// warp that completes an epoch checks its update count: zero updates (no row
+// had |r| > h when evaluated) stops the loop — the paper's Q = ∅ — and the
+// host-side compensated certificate decides (resuming if a row slipped).
+constexpr int kRing = 8;     // per-epoch counter slots
+struct AsyncCtl {
+  unsigned long long next;                 // claim counter (items)
+  unsigned long long upd[kRing], eu[kRing], done[kRing];
+  unsigned long long tot_upd, tot_eu;
+  unsigned int stop, bad, epochs, pad;
+};
+
+// settle one warp's counts for an epoch part: warp-reduce, then lane 0 adds
+// them; the warp that completes the epoch decides whether to stop
+static __device__ __forceinline__ void async_settle(AsyncCtl *c, unsigned long long ep,
+                                             unsigned long long nr, TAcc &t,
+                                             unsigned long long cnt) {
+  unsigned long long u = t.upd, e2 = t.eu, b = t.bad;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    u += __shfl_xor_sync(0xffffffffu, u, off);
+    e2 += __shfl_xor_sync(0xffffffffu, e2, off);
+    b |= __shfl_xor_sync(0xffffffffu, b, off);
+  }
+  t = TAcc{};
+  if ((threadIdx.x & 31) != 0 || cnt == 0) return;
+  const int slot = (int)(ep % kRing);
+  if (u) atomicAdd(&c->upd[slot], u);
+  atomicAdd(&c->tot_upd, u);
+  atomicAdd(&c->tot_eu, e2);
+  if (b) atomicOr(&c->bad, 1u);
+  __threadfence();
+  if (atomicAdd(&c->done[slot], cnt) + cnt == nr) {  // epoch ep complete
+    __threadfence();
+    const unsigned long long uu = atomicAdd(&c->upd[slot], 0ull);
+    atomicMax(&c->epochs, (unsigned int)(ep + 1));
+    if (uu == 0 || atomicAdd(&c->bad, 0u)) atomicExch(&c->stop, 1u);
+    const int z = (int)((ep + kRing / 2) % kRing);  // recycle a slot well ahead
+    c->upd[z] = 0;
+    c->done[z] = 0;
+  }
+}
+
+// out[0..3] = sweeps, relaxations, edge updates, reason (as k_sweep writes)
+static __global__ void k_async_result(const AsyncCtl *c, unsigned long long *out,
+                               unsigned long long max_sweeps) {
+  out[0] = c->epochs;
+  out[1] = c->tot_upd;
+  out[2] = c->tot_eu;
+  out[3] = c->bad ? 2ull : (c->stop ? 0ull : 1ull);
+}
+
+// ------------------------------------------ one pass over all tasks (CERT/DIS)
+template <int MODE, bool W>
+__global__ void __launch_bounds__(kBlock, 4) k_pass(KP p) {
+  Scalars S{};
+  if (MODE == CERT) S = *p.sc;
+  TAcc t{};
+  const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+  for (int wi = warp_id; wi < p.nwtasks_all; wi += gridDim.x * (kBlock / 32))
+    do_warp<MODE, W>(p, S, p.wtasks[wi], t);
+  for (int ti = blockIdx.x; ti < p.ntasks_all; ti += gridDim.x)
+    dispatch_tile<MODE, W>(p, S, p.tasks[ti], t);
+  if constexpr (MODE == CERT) {
+    double m = t.certmax;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (isnan(t.certmax)) m = t.certmax;
+    if ((threadIdx.x & 31) == 0 && m != 0.0)
+      atomicMax(p.cert_max, (unsigned long long)__double_as_longlong(m));
+  } else if constexpr (MODE == DIS) {
+    double sdis = t.dis;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sdis += __shfl_xor_sync(0xffffffffu, sdis, off);
+    if ((threadIdx.x & 31) == 0 && sdis != 0.0) atomicAdd(p.dis, sdis);
+  }
+}
+
+// ----------------------------------------------------------- node kernels
+static __global__ void k_scalars(const float *__restrict__ smin, const float *__restrict__ smax,
+                          double eps, double sigma, double c_override, Scalars *S) {
+  const double lo = (double)*smin, hi = (double)*smax;
+  Scalars s{};
+  s.bad_input = !(isfinite(lo) && isfinite(hi));
+  s.sigma = sigma;
+  s.c = c_override > 0 ? c_override : sigma + fmax(0.0, -lo);   // reading R5
+  s.eps_p = sigma / (s.c + sigma) * eps;
+  s.floored = lo < 0.0;
+  s.hs = s.floored ? sigma / (s.c + sigma) : s.eps_p;
+  s.heps = 0.5 * eps;
+  s.sentinel = 1e6 * fmax(fabs(hi + s.c), fabs(lo + s.c));
+  *S = s;
+}
+
+// s into layout order; ẑ' = 0 (Alg. 1 init) except rows with no arcs,
+// whose equation is (1 + 0) z_v = s'_v: solved exactly (ẑ'_v = s'_v)
+static __global__ void k_init(int64_t n, const int32_t *__restrict__ perm, const int64_t *__restrict__ rp,
+                       const float *__restrict__ s, Scalars *__restrict__ S,
+                       float *__restrict__ s_l, double *__restrict__ z,
+                       const double *__restrict__ z_init = nullptr) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float si = s[perm[i]];
+  if (!isfinite(si)) atomicOr(&S->bad_input, 1);  // min/max reductions skip NaN
+  s_l[i] = si;
+  if (rp[i + 1] == rp[i]) z[i] = (double)si + S->c;          // d = 0: exact
+  else if (z_init) {                                          // warm start (Lemma 3)
+    const double v = z_init[perm[i]] + S->c;
+    if (!isfinite(v)) atomicOr(&S->bad_input, 2);
+    z[i] = v;
+  } else z[i] = 0.0;                                          // Alg. 1 init
+}
+
+static __global__ void k_finalize(int64_t n, const int32_t *__restrict__ iperm, const double *__restrict__ z,
+                           const Scalars *__restrict__ S, float *__restrict__ zout,
+                           double *__restrict__ zprime) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const double zp = z[iperm[u]];
+  zout[u] = (float)(zp - S->c);  // ẑ_v − c
+  if (zprime) zprime[u] = zp;
+}
+
+// ------------------------------------------------------------- host side
+static unsigned gridn(int64_t work) {
+  int64_t b = (work + kBlock - 1) / kBlock;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 1 << 30));
+}
+
+static int persistent_grid(const void *fn, int num_sms, size_t smem = 0) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, smem);
+  if (per_sm < 1) per_sm = 1;
+  return per_sm * num_sms;
+}
+
+struct Staged {
+  const float *dev = nullptr;
+  float *owned = nullptr;
+};
+
+static fj_status stage_in(const float *src, int64_t n, cudaStream_t st, Staged &out) {
+  if (is_device_ptr(src)) {
+    out.dev = src;
+    return FJ_OK;
+  }
+  FJ_CUDA(cudaMallocAsync(&out.owned, sizeof(float) * n, st));
+  FJ_CUDA(cudaMemcpyAsync(out.owned, src, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+  out.dev = out.owned;
+  return FJ_OK;
+}
+
+static KP make_kp(const fj_graph *g, const Layout &L) {
+  KP p{};
+  p.rp = L.rp;
+  p.col = L.col;
+  p.w = L.w;
+  p.d1 = L.d1;
+  p.tasks = L.tasks;
+  p.wtasks = L.wtasks;
+  p.rtasks = L.rtasks;
+  p.rphase_begin = L.d_rphase_begin;
+  p.phase_begin = L.d_phase_begin;
+  p.wphase_begin = L.d_wphase_begin;
+  p.ncolors = L.ncolors;
+  p.ntasks_all = L.ntasks;
+  p.nwtasks_all = L.nwtasks;
+  return p;
+}
+
+static fj_status finish_status(const Scalars &hs, fj_stats &stats, const fj_opts *o,
+                               double omega) {
+  fj_status rc = FJ_OK;
+  if (hs.bad_input) {
+    set_error("fj_solve: s (or z_init) contains a non-finite value");
+    rc = FJ_ERR_INVALID;
+  } else if (stats.reason == 1) {
+    set_error("fj_solve: watchdog, %lld sweeps without convergence", (long long)stats.sweeps);
+    rc = FJ_ERR_NUMERIC;
+  } else if (stats.reason == 2) {
+    set_error("fj_solve: divergence sentinel |r| > 1e6 max|s'| (omega = %g)", omega);
+    rc = FJ_ERR_NUMERIC;
+  } else if (o->certify && !(stats.cert_ratio <= 1.0)) {
+    set_error("fj_solve: fp64 residual certificate failed (max |r|/h = %g)", stats.cert_ratio);
+    rc = FJ_ERR_NUMERIC;
+  }
+  stats.status = rc;
+  return rc;
+}
+
+
+// implemented in push.cu / batch.cu / solve.cu
+fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double omega,
+                          const fj_opts *o, float *z_out, fj_stats *st_out);
+fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, double omega,
+                           const fj_opts *o, float *Z_out, fj_stats *st_out);
+
+}  // namespace fj
