@@ -33,7 +33,7 @@ bool is_device_ptr(const void *p) {
 void Layout::release(cudaStream_t st) {
   for (void *q : {(void *)perm, (void *)iperm, (void *)rp, (void *)col, (void *)w, (void *)d1,
                   (void *)tasks, (void *)wtasks, (void *)d_phase_begin, (void *)d_wphase_begin,
-                  (void *)d_crow, (void *)rtasks, (void *)d_rphase_begin})
+                  (void *)d_crow, (void *)rtasks, (void *)d_rphase_begin, (void *)tail_beta})
     if (q) cudaFreeAsync(q, st);
   perm = iperm = nullptr;
   rp = nullptr;
@@ -44,6 +44,9 @@ void Layout::release(cudaStream_t st) {
   d_phase_begin = d_wphase_begin = nullptr;
   d_crow = nullptr;
   crow.clear();
+  tail_beta = nullptr;
+  tail_phase = -1;
+  tail_row0 = tail_row1 = 0;
   rtasks = nullptr;
   d_rphase_begin = nullptr;
   nrtasks = 0;

@@ -74,6 +74,109 @@ __global__ void k_jp_round(int64_t n, const int64_t *__restrict__ irp, const int
   }
 }
 
+// rows per color
+__global__ void k_color_hist(int64_t n, const int32_t *__restrict__ c, int nc,
+                             unsigned long long *__restrict__ cnt) {
+  extern __shared__ unsigned long long h[];
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(h + c[v], 1ull);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nc; i += blockDim.x)
+    if (h[i]) atomicAdd(cnt + i, h[i]);
+}
+
+__global__ void k_color_clamp(int64_t n, int32_t *__restrict__ c, int K) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    if (c[v] > K) c[v] = K;
+}
+
+// Tail merge (reading R23).  First-fit colorings of power-law graphs have a
+// long tail of tiny colors (the dense core: C3 has 96 colors, the last ~85
+// holding ~2% of the rows), and every color costs a grid barrier plus a
+// phase tail.  Colors K.. are merged into ONE phase whose rows may be
+// adjacent and are relaxed asynchronously.  Rows of colors < K keep the exact
+// sequential SOR semantics with the caller's ω.  A tail row i relaxes with
+// ω_i = min(ω, 1.98/(1+β_i)), β_i = Σ_{j in tail} a_ij/(1+d_i): then every
+// row of the tail block's iteration matrix T = I − Ω D⁻¹ A_BB has
+// |1−ω_i| + ω_i β_i < 1, i.e. ‖T‖_∞ < 1, the Chazan–Miranker condition under
+// which asynchronous relaxation of the block converges whatever the update
+// order and staleness.  K = the smallest index whose tail holds at most
+// FJ_TAIL_FRAC (default 1%) of the rows; 0 disables the merge.
+static fj_status merge_tail_colors(fj_graph *g) {
+  cudaStream_t st = g->stream;
+  const int nc = g->ncolors;
+  g->ncolors_raw = nc;
+  g->tail_color = -1;
+  double frac = 0.01;
+  if (const char *e = getenv("FJ_TAIL_FRAC")) frac = atof(e);
+  if (!(frac > 0.0) || nc <= 2 || nc > 6000) return FJ_OK;
+  unsigned long long *cnt = nullptr;
+  FJ_CUDA(cudaMallocAsync(&cnt, sizeof(unsigned long long) * nc, st));
+  FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * nc, st));
+  fj::count_launch();
+  k_color_hist<<<std::max(1, std::min(g->num_sms * 4, (int)((g->n + kBlock - 1) / kBlock))), kBlock,
+                 sizeof(unsigned long long) * nc, st>>>(g->n, g->colors, nc, cnt);
+  std::vector<unsigned long long> h(nc);
+  FJ_CUDA(cudaMemcpyAsync(h.data(), cnt, sizeof(unsigned long long) * nc, cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(cnt, st);
+  const double cap = frac * (double)g->n;
+  int K = nc;
+  double tail = 0.0;
+  while (K > 0 && tail + (double)h[K - 1] <= cap) tail += (double)h[--K];
+  if (nc - K < 2) return FJ_OK;  // nothing to merge
+  fj::count_launch();
+  k_color_clamp<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((g->n + kBlock - 1) / kBlock, (int64_t)g->num_sms * 8)), kBlock, 0, st>>>(g->n, g->colors, K);
+  g->ncolors = K + 1;
+  g->tail_color = K;
+  return FJ_OK;
+}
+
+// β_i for the rows [r0, r1) of the tail phase (warp per row)
+template <bool W>
+__global__ void k_tail_beta(int64_t r0, int64_t r1, const int64_t *__restrict__ rp,
+                            const int32_t *__restrict__ col, const float *__restrict__ w,
+                            const double *__restrict__ d1, float *__restrict__ beta) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t i = r0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); i < r1; i += nw) {
+    const int64_t b = rp[i], e = rp[i + 1];
+    double a = 0.0;
+    for (int64_t k = b + lane; k < e; k += 32) {
+      const int32_t j = col[k];
+      if (j >= r0 && j < r1) a += W ? (double)w[k] : 1.0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) beta[i - r0] = (float)(a / (W ? d1[i] : (double)(e - b + 1)));
+  }
+}
+
+fj_status tail_bounds(fj_graph *g, Layout *L) {
+  L->tail_phase = g->tail_color;
+  if (g->tail_color < 0) return FJ_OK;
+  cudaStream_t st = g->stream;
+  const int64_t r0 = L->crow[g->tail_color], r1 = L->crow[g->tail_color + 1];
+  L->tail_row0 = r0;
+  L->tail_row1 = r1;
+  FJ_CUDA(cudaMallocAsync(&L->tail_beta, sizeof(float) * std::max<int64_t>(1, r1 - r0), st));
+  if (r1 > r0) {
+    const unsigned blocks =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(((r1 - r0) * 32 + kBlock - 1) / kBlock,
+                                                         (int64_t)g->num_sms * 8));
+    fj::count_launch();
+    if (g->weighted)
+      k_tail_beta<true><<<blocks, kBlock, 0, st>>>(r0, r1, L->rp, L->col, L->w, L->d1, L->tail_beta);
+    else
+      k_tail_beta<false><<<blocks, kBlock, 0, st>>>(r0, r1, L->rp, L->col, L->w, L->d1, L->tail_beta);
+  }
+  return FJ_OK;
+}
+
 fj_status build_coloring(fj_graph *g) {
   cudaStream_t st = g->stream;
   const int64_t n = g->n;
@@ -115,7 +218,9 @@ fj_status build_coloring(fj_graph *g) {
   cudaFreeAsync(c1, st);
   cudaFreeAsync(rem, st);
   cudaFreeAsync(maxc, st);
+  FJ_TRY(merge_tail_colors(g));
   fj_status s = build_layout_from_out(g, ort, ocol, ow, g->colors, g->ncolors, &g->color_layout);
+  if (s == FJ_OK) s = tail_bounds(g, &g->color_layout);
   cudaFreeAsync(ort, st);
   cudaFreeAsync(ocol, st);
   if (ow) cudaFreeAsync(ow, st);

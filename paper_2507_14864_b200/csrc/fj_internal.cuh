@@ -65,6 +65,9 @@ struct alignas(16) Task {
 // (color, class, id) order; ids in `col` are permuted ids.
 struct Layout {
   int ncolors = 0;
+  int tail_phase = -1;  // merged tail colors (reading R23); −1 if none
+  int64_t tail_row0 = 0, tail_row1 = 0;  // (permuted) rows of the tail phase
+  float *tail_beta = nullptr;     // β_i = Σ_{j in tail} a_ij / (1 + d_i) per tail row
   int64_t n = 0, m = 0;
   int32_t *perm = nullptr;   // new -> old
   int32_t *iperm = nullptr;  // old -> new
@@ -114,8 +117,10 @@ struct fj_graph {
   fj::Layout color_layout;   // lazily built for COLORED solves
   fj::Layout push_layout;    // lazily built for PUSH (in-rows: scatter lists)
   fj::Layout push_color_layout;
-  int32_t *colors = nullptr; // color per original node (lazy)
-  int ncolors = 0;
+  int32_t *colors = nullptr; // color per original node (lazy); tail colors merged
+  int ncolors = 0;           // phases of a colored sweep (tail merged)
+  int ncolors_raw = 0;       // colors of the distance-1 coloring before the merge
+  int tail_color = -1;       // merged tail phase (−1: none)
 };
 
 namespace fj {

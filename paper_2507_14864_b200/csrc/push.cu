@@ -25,6 +25,7 @@ struct PP {
   const int *phase_begin, *wphase_begin;
   const int64_t *crow;
   int ncolors;
+  int tail_phase;  // colored: merged tail colors relaxed with ω = 1 (reading R23)
   int64_t n;
   const float *__restrict__ s;
   double *z, *r, *q;
@@ -37,7 +38,7 @@ struct PP {
 };
 
 __device__ __forceinline__ void push_pop(const PP &p, const Scalars &S, int64_t b, int64_t e,
-                                         TAcc &t) {
+                                         TAcc &t, double om) {
   for (int64_t v = b + blockIdx.x * (int64_t)kBlock + threadIdx.x; v < e;
        v += (int64_t)gridDim.x * kBlock) {
     const double sp = (double)p.s[v] + S.c;
@@ -45,9 +46,9 @@ __device__ __forceinline__ void push_pop(const PP &p, const Scalars &S, int64_t 
     const double rv = p.r[v];
     double qv = 0.0;
     if (fabs(rv) > p.theta * h) {                       // |r_v| > h_v
-      qv = p.omega * rv / p.d1[v];                      // ω r_v/(1+d_v)
+      qv = om * rv / p.d1[v];                           // ω r_v/(1+d_v)
       p.z[v] += qv;                                     // equ:sor1
-      p.r[v] = rv - p.omega * rv;                       // equ:sor2: (1−ω) r_v
+      p.r[v] = rv - om * rv;                            // equ:sor2: (1−ω) r_v
       t.upd++;
       t.eu += (unsigned long long)(p.rp[v + 1] - p.rp[v]);
     }
@@ -77,8 +78,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_push(PP p) {
   const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
     for (int k = 0; k < p.ncolors; ++k) {
-      push_pop(p, S, p.crow[k], p.crow[k + 1], t);
-      if (k == p.ncolors - 1) push_pop(p, S, p.crow[p.ncolors], p.n, t);  // rows with no in-arcs
+      const double om = k == p.tail_phase ? 1.0 : p.omega;
+      push_pop(p, S, p.crow[k], p.crow[k + 1], t, om);
+      if (k == p.ncolors - 1) push_pop(p, S, p.crow[p.ncolors], p.n, t, om);  // rows with no in-arcs
       grid_sync(p.bar);
       // B: warp units (long scatter lists), then tile tasks (group per row)
       const int w0 = p.wphase_begin[k], nw = p.wphase_begin[k + 1] - w0;
@@ -177,9 +179,11 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   const bool colored = omega != 1.0;
   if (colored && !g->colors) FJ_TRY(build_coloring(g));
   Layout &P = colored ? g->push_color_layout : g->push_layout;
-  if (!P.tasks)
+  if (!P.tasks) {
     FJ_TRY(build_layout_from_out(g, g->in_rp, g->in_col, g->in_w, colored ? g->colors : nullptr,
                                  colored ? g->ncolors : 1, &P, true));
+    P.tail_phase = colored ? g->tail_color : -1;
+  }
   const Layout &L = g->async_layout;
   const bool W = g->weighted != 0;
   fj_stats stats{};
@@ -245,6 +249,7 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   pp.wphase_begin = P.d_wphase_begin;
   pp.crow = P.d_crow;
   pp.ncolors = P.ncolors;
+  pp.tail_phase = P.tail_phase;
   pp.n = n;
   pp.s = sP;
   pp.z = zP;

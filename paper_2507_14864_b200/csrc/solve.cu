@@ -272,10 +272,6 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
   int phase = 0;
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
     for (int k = 0; k < p.ncolors; ++k, ++phase) {
-      // static round-robin (tasks are balanced by construction; no claim
-      // atomics on the hot loop): warp units first (hub rows), then tiles
-      const int w0 = p.wphase_begin[k], nw = p.wphase_begin[k + 1] - w0;
-      const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
       if (TMA) {
         relax_stream<W>(p, S, p.rphase_begin[k], p.rphase_begin[k + 1] - p.rphase_begin[k], t,
                         ws, phase_bits);
@@ -297,6 +293,8 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
           }
         }
       } else {  // static round-robin: one warp per work item, next item prefetched
+        // (tasks are balanced by construction; no claim atomics on the hot loop)
+        const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
         const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
         const int stride = gridDim.x * (kBlock / 32);
         double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;

@@ -58,6 +58,9 @@ struct KP {
   const int *phase_begin;
   const int *wphase_begin;
   int ncolors;
+  int tail_phase;           // merged tail colors (reading R23); −1 if none
+  int64_t tail_row0, tail_row1;  // rows of the tail phase (empty range if none)
+  const float *tail_beta;   // per tail row: β_i (see color.cu)
   int ntasks_all;
   int nwtasks_all;
   int max_sweeps;
@@ -163,7 +166,11 @@ __device__ __forceinline__ void relax_row_pre(const KP &p, const Scalars &S, int
   const double rho = residual_dd(total, sp, d1, zi);
   const double ar = fabs(rho);
   if (ar > p.theta * h) {
-    __stcg(p.z + row, zi + p.omega * rho / d1);
+    // tail phase (R23): ω_i = min(ω, 1.98/(1+β_i)) keeps |1−ω_i| + ω_i β_i < 1
+    double om = p.omega;
+    if (row >= p.tail_row0 && row < p.tail_row1)
+      om = fmin(om, 1.98 / (1.0 + (double)p.tail_beta[row - p.tail_row0]));
+    __stcg(p.z + row, zi + om * rho / d1);
     t.upd++;
     t.eu += (unsigned long long)len;
   }
@@ -419,7 +426,8 @@ __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, c
     const int row = tk.a + q * ng + (lane >> cls);
     if (row < tk.b && gl == 0) {
       const int len = (int)(re[q] - rb[q]);
-      relax_row_pre(p, S, row, len, dd{a, 0.0}, sv[q], zi[q], W ? d1[q] : (double)(len + 1), t);
+      relax_row_pre(p, S, row, len, dd{a, 0.0}, sv[q], zi[q], W ? d1[q] : (double)(len + 1),
+                          t);
     }
   }
   __syncwarp();  // the slice is reused by this warp's next task
@@ -632,6 +640,10 @@ static KP make_kp(const fj_graph *g, const Layout &L) {
   p.phase_begin = L.d_phase_begin;
   p.wphase_begin = L.d_wphase_begin;
   p.ncolors = L.ncolors;
+  p.tail_phase = L.tail_phase;
+  p.tail_row0 = L.tail_row0;
+  p.tail_row1 = L.tail_row1;
+  p.tail_beta = L.tail_beta;
   p.ntasks_all = L.ntasks;
   p.nwtasks_all = L.nwtasks;
   return p;

@@ -200,13 +200,53 @@ def test_long_rows_star(dev, hub_deg):
     check_parity(dev, rp, col, w, s, 1e-6, 1.5, False)
 
 
-def test_determinism_colored(dev):
-    """COLORED sweeps read only other colors' values: bit-reproducible."""
+def test_determinism_colored(dev, monkeypatch):
+    """COLORED sweeps read only other colors' values: bit-reproducible (with the
+    tail merge of reading R23 off: the merged tail phase is asynchronous)."""
+    monkeypatch.setenv("FJ_TAIL_FRAC", "0")
     rp, col, w, s, directed = TINY["rmat12w"]()
     a = gpu_solve(dev, rp, col, w, s, 1e-6, 1.2, directed, method="colored")
     b = gpu_solve(dev, rp, col, w, s, 1e-6, 1.2, directed, method="colored")
     assert np.array_equal(a[2], b[2])
     a[0].close(); b[0].close()
+
+
+# ------------------------------------------- tail-color merge (reading R23)
+@pytest.mark.parametrize("name", ["chunglu4k", "er2000", "rmat12w"])
+@pytest.mark.parametrize("omega", [1.3, 1.7])
+def test_tail_merge_parity(dev, monkeypatch, name, omega):
+    """Merged tail phase: certified, same z as the oracle, fewer phases."""
+    rp, col, w, s, directed = TINY[name]()
+    if directed and omega > 1.5:
+        pytest.skip("SOR with ω > 1 on a non-symmetric M-matrix may diverge (as in exact SOR)")
+    ref_omega = 1.0 if directed else None
+    monkeypatch.setenv("FJ_TAIL_FRAC", "0")
+    st0, z0, ref = check_parity(dev, rp, col, w, s, 1e-6, omega, directed, method="colored",
+                                ref_omega=ref_omega)
+    monkeypatch.setenv("FJ_TAIL_FRAC", "0.2")
+    st1, z1, _ = check_parity(dev, rp, col, w, s, 1e-6, omega, directed, method="colored",
+                              ref_omega=ref_omega)
+    assert st1.colors <= st0.colors
+    if st0.colors > 3:
+        assert st1.colors < st0.colors
+
+
+@pytest.mark.parametrize("omega", [1.5, 1.9])
+def test_tail_merge_complete_graph(dev, monkeypatch, omega):
+    """K_200: every color holds one row, so merging 90% of the rows makes a
+    tail whose rows are all adjacent (β_i ≈ 0.9).  The per-row bound
+    ω_i = min(ω, 1.98/(1+β_i)) keeps the asynchronous tail a contraction; the
+    result is the closed form of oracle.closed_forms.complete_graph."""
+    k = 200
+    edges = [(i, j) for i in range(k) for j in range(i + 1, k)]
+    rp, col, w = G.in_csr_from_edges(k, edges)
+    s = fjgen.uniform(k, 77)
+    monkeypatch.setenv("FJ_TAIL_FRAC", "0.9")
+    g, z, zp, st = gpu_solve(dev, rp, col, w, s, 1e-6, omega, False, method="colored")
+    assert st.status == 0 and st.colors < k
+    assert oracle.certificate(rp, col, w, s, zp, 1e-6)[0] <= 1.0
+    assert rel_err(z, cf.complete_graph(s.astype(np.float64))) <= 1e-4
+    g.close()
 
 
 def test_invalid_inputs(dev):
