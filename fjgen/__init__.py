@@ -232,3 +232,30 @@ def config(cid: int, shrink: int = 0) -> Problem:
 
 def num_threads() -> int:
     return lib().fjgen_num_threads()
+
+
+# --------------------------------------------------- sharded inputs (row f4)
+def to_out_csr(row_ptr, col, w=None):
+    """Transpose an in-CSR (row v lists the u with u→v) into the out-CSR
+    (row u lists the v with u→v, ascending): index shuffling only."""
+    row_ptr = np.asarray(row_ptr, np.int64)
+    col = np.asarray(col, np.int32)
+    n = len(row_ptr) - 1
+    v = np.repeat(np.arange(n, dtype=np.int64), np.diff(row_ptr))
+    order = np.lexsort((v, col.astype(np.int64)))
+    orp = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(col, minlength=n), out=orp[1:])
+    ocol = v[order].astype(np.int32)
+    ow = None if w is None else np.asarray(w, np.float32)[order]
+    return orp, ocol, ow
+
+
+def shard_rows(out_rp, out_col, out_w, begin, rank: int):
+    """Rank `rank`'s rows [begin[rank], begin[rank+1]) of an out-CSR, row_ptr
+    rebased to 0, columns kept global."""
+    a, b = int(begin[rank]), int(begin[rank + 1])
+    k0, k1 = int(out_rp[a]), int(out_rp[b])
+    rp = (np.asarray(out_rp[a:b + 1], np.int64) - k0).copy()
+    col = np.ascontiguousarray(out_col[k0:k1], np.int32)
+    w = None if out_w is None else np.ascontiguousarray(out_w[k0:k1], np.float32)
+    return rp, col, w

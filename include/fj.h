@@ -197,6 +197,95 @@ fj_status fj_measures(fj_graph_t g, const float *z, double *polarization,
 /* All four measures of tab:measures; s (fp32[n]) may be NULL. */
 fj_status fj_measures_ex(fj_graph_t g, const float *z, const float *s, fj_measures_t *out);
 
+/*
+ * ---------------------------------------------------------------------------
+ * Sharded solve: one graph split over ranks by a
+ * 1-D node partition begin[0] = 0 ≤ begin[1] ≤ … ≤ begin[world] = n.  Rank r
+ * owns the equations of its nodes u ∈ [begin[r], begin[r+1]) — row u of
+ * (I+L)z = s (Lemma 1) reads a_uv along u's OUT-arcs u→v — and the
+ * estimate ẑ_u.  Every sweep each rank relaxes its own rows exactly as
+ * fj_solve's ASYNC schedule does (|r_u| > h_u), reading the other
+ * ranks' ẑ from the last exchange; then the ranks exchange their ẑ segments
+ * and reduce (relaxations, divergence flag).  A sweep in which no rank
+ * relaxes anything read only final values, so the loop ends on the paper's
+ * rule (Q = ∅) exactly as on one GPU; the fp64 certificate (Lemma 3,
+ * P:231) then runs on every rank and its maximum decides, with the same
+ * resume rule (reading R21).  Across ranks the schedule is block-Jacobi with
+ * in-place Gauss–Seidel inside each block: convergent at ω = 1 (I+L is an
+ * M-matrix); ω ≠ 1 is allowed and, as with directed ASYNC, the sentinel and
+ * the certificate decide.
+ *
+ * Transport (fj_comm): NCCL (one rank per process and GPU; ranks exchange
+ * segments with grouped ncclSend/ncclRecv and reduce with ncclAllReduce over
+ * NVLink/NVSwitch; libnccl.so.2 is loaded on first use), or an in-process
+ * transport that holds all `world` shards of one process on the current
+ * device and exchanges with device copies (single-GPU use and tests).
+ */
+typedef struct fj_comm *fj_comm_t;
+typedef struct fj_shard *fj_shard_t;
+
+/* Arc-balanced 1-D partition (host only, no device work).  row_ptr: HOST
+   int64[n+1] of the out-CSR (row u = u's out-arcs, i.e. its work per sweep).
+   Writes begin[0..world]: begin[0] = 0, begin[world] = n, every part
+   non-empty (needs n ≥ world), part r ends at the first row boundary at or
+   after r·(m + n)/world in units of (arcs + 1 per row).  FJ_ERR_INVALID on
+   bad arguments. */
+fj_status fj_shard_plan(int64_t n, const int64_t *row_ptr, int world, int64_t *begin);
+
+/* 128-byte NCCL unique id, created on one rank and passed by the caller to
+   every rank (e.g. torch.distributed broadcast of the bytes). */
+fj_status fj_comm_unique_id(void *id128);
+/* NCCL communicator: this process is `rank` of `world`, on the current CUDA
+   device.  All work of the shards of this comm is ordered on one stream the
+   comm owns. */
+fj_status fj_comm_create(const void *id128, int rank, int world, fj_comm_t *out);
+/* In-process transport: all `world` ranks are shards of this process on the
+   current device. */
+fj_status fj_comm_create_local(int world, fj_comm_t *out);
+/* Destroy a comm after every shard created on it. */
+fj_status fj_comm_destroy(fj_comm_t c);
+
+/*
+ * Shard `rank` of an n-node graph: out_row_ptr int64[n_local + 1] (starting at
+ * 0, n_local = begin[rank+1] − begin[rank] ≥ 1), out_col int32[nnz_local]
+ * GLOBAL ids v of the arcs u→v of the owned rows (row i = node begin[rank]+i),
+ * each row strictly increasing; out_w fp32 weights (> 0, finite) or NULL.
+ * begin: host int64[world+1].  directed: as in fj_graph_create (an undirected
+ * graph stores both arcs of every edge; symmetry across ranks is the caller's
+ * contract and is not checked).  Host or device pointers; copied.
+ * FJ_ERR_INVALID: bad begin / rank, empty part, bad row_ptr, id out of range,
+ * self-loop, unsorted or duplicate column, bad weight, n ≥ 2^30.
+ */
+fj_status fj_shard_create(fj_comm_t comm, int rank, int64_t n, const int64_t *begin,
+                          const int64_t *out_row_ptr, const int32_t *out_col,
+                          const float *out_w, int directed, fj_shard_t *out);
+
+/* Collective over the shards this process owns — one with an NCCL comm, all
+   `world` in rank order with a local comm: exchange the sweep layouts' node
+   orders and relabel remote columns.  Required once before solve/measures. */
+fj_status fj_shard_connect(fj_shard_t *shards, int count);
+
+/*
+ * Collective solve over the shards this process owns (as in connect).
+ * s[i]: fp32[n_local(i)] opinions of shard i's nodes; z_out[i]: fp32[n_local(i)]
+ * results; zprime_out (nullable array, entries nullable): fp64 ẑ' = ẑ + c per
+ * shard.  o: as fj_solve_ex (method must be AUTO/ASYNC; z_init and
+ * zprime_out of o must be NULL).  st (nullable): sweeps, relaxations and edge
+ * updates summed over all ranks, worst certificate ratio, device times of
+ * this process.  Guarantee and statuses as fj_solve.
+ */
+fj_status fj_shard_solve(fj_shard_t *shards, int count, const float *const *s, double eps,
+                         double omega, const fj_opts *o, float *const *z_out,
+                         double *const *zprime_out, fj_stats *st);
+
+/* Collective measures of a sharded z (fp32 slices as z_out above); s nullable
+   (then I = 0).  Same definitions as fj_measures_ex. */
+fj_status fj_shard_measures(fj_shard_t *shards, int count, const float *const *z,
+                            const float *const *s, fj_measures_t *out);
+
+/* Free a shard (NULL is a no-op). */
+fj_status fj_shard_destroy(fj_shard_t s);
+
 /* Thread-local message for the last non-OK status of this thread. */
 const char *fj_last_error(void);
 

@@ -25,7 +25,9 @@ METHODS = {"auto": 0, "async": 1, "colored": 2, "push": 3}
 EXPORTS = ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve", "fj_solve_ex",
            "fj_measures", "fj_measures_ex", "fj_opts_default", "fj_last_error",
            "fj_abi_version", "fj_kernel_launches", "fj_omega_opt", "fj_omega_sweep",
-           "fj_solve_batch")
+           "fj_solve_batch", "fj_shard_plan", "fj_comm_unique_id", "fj_comm_create",
+           "fj_comm_create_local", "fj_comm_destroy", "fj_shard_create", "fj_shard_connect",
+           "fj_shard_solve", "fj_shard_measures", "fj_shard_destroy")
 
 
 class FJError(RuntimeError):
@@ -88,9 +90,24 @@ def lib():
         L.fj_omega_opt.argtypes = [P, i, d, ctypes.POINTER(d), ctypes.POINTER(d)]
         L.fj_omega_sweep.argtypes = [P, P, d, d, d, d, i, ctypes.POINTER(d), P,
                                      ctypes.POINTER(i)]
+        PP = ctypes.POINTER(P)
+        L.fj_shard_plan.argtypes = [i64, P, i, P]
+        L.fj_comm_unique_id.argtypes = [P]
+        L.fj_comm_create.argtypes = [P, i, i, PP]
+        L.fj_comm_create_local.argtypes = [i, PP]
+        L.fj_comm_destroy.argtypes = [P]
+        L.fj_shard_create.argtypes = [P, i, i64, P, P, P, P, i, PP]
+        L.fj_shard_connect.argtypes = [PP, i]
+        L.fj_shard_solve.argtypes = [PP, i, PP, d, d, ctypes.POINTER(_Opts), PP, PP,
+                                     ctypes.POINTER(_Stats)]
+        L.fj_shard_measures.argtypes = [PP, i, PP, PP, ctypes.POINTER(_Measures)]
+        L.fj_shard_destroy.argtypes = [P]
         for f in ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve",
                   "fj_solve_ex", "fj_measures", "fj_measures_ex", "fj_omega_opt",
-                  "fj_omega_sweep", "fj_solve_batch"):
+                  "fj_omega_sweep", "fj_solve_batch", "fj_shard_plan", "fj_comm_unique_id",
+                  "fj_comm_create", "fj_comm_create_local", "fj_comm_destroy",
+                  "fj_shard_create", "fj_shard_connect", "fj_shard_solve",
+                  "fj_shard_measures", "fj_shard_destroy"):
             getattr(L, f).restype = i
         _LIB = L
     return _LIB
@@ -278,3 +295,131 @@ def omega_sweep(g: Graph, s, eps: float, lo: float = 1.0, hi: float = 1.95, step
                                 METHODS[method], ctypes.byref(best), table, ctypes.byref(n)))
     rows = [(table[3 * i], int(table[3 * i + 1]), int(table[3 * i + 2])) for i in range(n.value)]
     return best.value, rows
+
+
+# ----------------------------------------------------------------- sharded (f4)
+def shard_plan(row_ptr, world: int):
+    """fj_shard_plan: arc-balanced 1-D partition of the out-CSR row_ptr (host
+    int64[n+1], contiguous); returns begin as a list of world+1 ints."""
+    _dtype_ok(row_ptr, "row_ptr", "int64")
+    begin = (ctypes.c_int64 * (world + 1))()
+    _check(lib().fj_shard_plan(len(row_ptr) - 1, _ptr(row_ptr), int(world), begin))
+    return list(begin)
+
+
+def comm_unique_id() -> bytes:
+    """fj_comm_unique_id: the 128-byte NCCL id (create on one rank, broadcast)."""
+    buf = (ctypes.c_char * 128)()
+    _check(lib().fj_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    """Owning handle of an ``fj_comm_t``: ``Comm.in_process(world)`` (all
+    shards in this process, current device) or ``Comm.nccl(uid, rank, world)``."""
+
+    def __init__(self, h, world: int, rank: int, in_process: bool):
+        self._h, self.world, self.rank, self.in_process_ = h, world, rank, in_process
+
+    @classmethod
+    def in_process(cls, world: int) -> "Comm":
+        h = ctypes.c_void_p()
+        _check(lib().fj_comm_create_local(int(world), ctypes.byref(h)))
+        return cls(h, int(world), 0, True)
+
+    @classmethod
+    def nccl(cls, uid: bytes, rank: int, world: int) -> "Comm":
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        h = ctypes.c_void_p()
+        buf = (ctypes.c_char * 128).from_buffer_copy(uid)
+        _check(lib().fj_comm_create(buf, int(rank), int(world), ctypes.byref(h)))
+        return cls(h, int(world), int(rank), False)
+
+    def close(self):
+        if self._h:
+            lib().fj_comm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Shard:
+    """Owning handle of an ``fj_shard_t``: rank ``rank``'s OUT-rows
+    (``row_ptr`` int64[n_local+1], ``col`` int32 GLOBAL ids, ``w`` float32 or
+    None) of an n-node graph partitioned by ``begin``."""
+
+    def __init__(self, comm: Comm, rank: int, n: int, begin, row_ptr, col, w=None,
+                 directed=True):
+        _dtype_ok(row_ptr, "row_ptr", "int64")
+        _dtype_ok(col, "col", "int32")
+        _dtype_ok(w, "w", "float32")
+        self._b = (ctypes.c_int64 * len(begin))(*[int(x) for x in begin])
+        self._h = ctypes.c_void_p()
+        _check(lib().fj_shard_create(comm._h, int(rank), int(n), self._b, _ptr(row_ptr),
+                                     _ptr(col), _ptr(w), 1 if directed else 0,
+                                     ctypes.byref(self._h)))
+        self.comm, self.rank, self.n = comm, int(rank), int(n)
+        self.n_local = int(self._b[rank + 1] - self._b[rank])
+
+    def close(self):
+        if self._h:
+            lib().fj_shard_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _handles(shards):
+    return (ctypes.c_void_p * len(shards))(*[sh._h.value for sh in shards])
+
+
+def _ptrs(arrs):
+    if arrs is None:
+        return None
+    return (ctypes.c_void_p * len(arrs))(*[(_ptr(a).value if a is not None else None)
+                                           for a in arrs])
+
+
+def shard_connect(shards):
+    """fj_shard_connect (collective over this process's shards, rank order)."""
+    _check(lib().fj_shard_connect(_handles(shards), len(shards)))
+
+
+def shard_solve(shards, s_list, z_list, eps: float, omega: float = 1.0, sigma: float = 1e-5,
+                max_sweeps: int = 0, cert_rounds: int = -1, certify: bool = True,
+                zprime_list=None, raise_on_numeric: bool = True) -> SolveStats:
+    """fj_shard_solve: per-shard float32 slices in, float32 (and optional fp64
+    ẑ') slices out; stats aggregated over ranks."""
+    for a in s_list:
+        _dtype_ok(a, "s", "float32")
+    for a in z_list:
+        _dtype_ok(a, "z_out", "float32")
+    o = _Opts()
+    lib().fj_opts_default(ctypes.byref(o))
+    o.sigma, o.max_sweeps, o.cert_rounds, o.certify = sigma, max_sweeps, cert_rounds, int(certify)
+    st = _Stats()
+    rc = lib().fj_shard_solve(_handles(shards), len(shards), _ptrs(s_list), float(eps),
+                              float(omega), ctypes.byref(o), _ptrs(z_list), _ptrs(zprime_list),
+                              ctypes.byref(st))
+    stats = SolveStats(**{k: getattr(st, k) for k, _ in _Stats._fields_})
+    if rc == FJ_ERR_NUMERIC and not raise_on_numeric:
+        return stats
+    _check(rc)
+    return stats
+
+
+def shard_measures(shards, z_list, s_list=None) -> dict:
+    """fj_shard_measures: P, D, I, C of a sharded z."""
+    m = _Measures()
+    _check(lib().fj_shard_measures(_handles(shards), len(shards), _ptrs(z_list), _ptrs(s_list),
+                                   ctypes.byref(m)))
+    return dict(P=m.polarization, D=m.disagreement, I=m.internal_conflict, C=m.controversy)

@@ -83,7 +83,8 @@ __global__ void k_copy_rows(int64_t n, const int32_t *__restrict__ perm,
     int32_t u = perm[i];
     int64_t b = ort[u], e = ort[u + 1], o = rp[i];
     for (int64_t k = lane; k < e - b; k += 32) {
-      col[o + k] = iperm[ocol[b + k]];
+      const int32_t c = ocol[b + k];
+      col[o + k] = c < n ? iperm[c] : c;  // c ≥ n: a shard's remote column (shard.cu)
       if (w) w[o + k] = ow[b + k];
     }
     if (lane == 0 && d1) d1[i] = 1.0 + deg[u];

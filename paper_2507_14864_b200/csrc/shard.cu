@@ -1,0 +1,949 @@
+// shard.cu — sharded solve over ranks.
+//
+// A 1-D node partition: rank r owns the equations (rows of I + L, Lemma 1,
+// P:87) and the estimates ẑ_u of the nodes u ∈ [begin[r], begin[r+1]).  Its
+// sweep layout is fj_solve's (layout.cu) built over the owned OUT-rows only;
+// columns are relabelled into the rank's ẑ buffer
+//
+//     [ own n_local rows (layout order) | slot 0 | slot 1 | … | slot W−2 ]
+//
+// where slot j holds rank (r + 1 + j) mod W's segment in THAT rank's layout
+// order (seg_max entries each).  The sweep kernel is fj_solve's k_sweep, one
+// sweep per launch, unchanged: own columns and remote columns are both plain
+// indices into the buffer.  After every sweep the ranks exchange segments
+// (grouped ncclSend/ncclRecv over NVLink, or device copies for the
+// in-process transport) and all-reduce (relaxations, edge updates, sentinel
+// flag, bad-input flag).  A sweep with zero relaxations on every rank read
+// only final values (the last exchange delivered every segment as it still
+// is), which is the paper's stopping rule Q = ∅; then the fp64
+// certificate (Lemma 3) runs on every rank and the maximum decides,
+// with the resume rule of reading R21.
+//
+// Schedule across ranks: block-Jacobi with in-place Gauss–Seidel inside each
+// block — an asynchronous relaxation with bounded staleness, convergent at
+// ω = 1 because I + L is an M-matrix.
+#include <dlfcn.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <mutex>
+
+#include <nvtx3/nvToolsExt.h>
+
+#include "sweep_common.cuh"
+
+// node kernels of solve.cu
+namespace fj {
+__global__ void k_meas_nodes1(int64_t n, const int32_t *__restrict__ perm,
+                              const float *__restrict__ z, double *__restrict__ zl,
+                              double *__restrict__ sums);
+}
+
+struct fj_comm {
+  int world = 1, rank = 0;
+  bool local = true;
+  ncclComm_t nc = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+};
+
+struct fj_shard {
+  fj_comm *comm = nullptr;
+  int rank = 0;
+  int64_t n = 0;                 // global nodes
+  std::vector<int64_t> begin;    // [world + 1]
+  int64_t n_local = 0, seg_max = 0, nz = 0;
+  fj_graph *g = nullptr;         // owned rows: n = n_local, async layout
+  bool connected = false;
+};
+
+namespace fj {
+
+// ------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char *(*GetErrorString)(ncclResult_t);
+};
+
+static const NcclApi *nccl() {
+  static std::once_flag once;
+  static NcclApi api{};
+  static bool ok = false;
+  std::call_once(once, [] {
+    // in a PyTorch process this resolves to the libnccl.so.2 torch loaded
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+#define FJ_SYM(f, name) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, name))
+    FJ_SYM(GetUniqueId, "ncclGetUniqueId");
+    FJ_SYM(CommInitRank, "ncclCommInitRank");
+    FJ_SYM(CommDestroy, "ncclCommDestroy");
+    FJ_SYM(AllReduce, "ncclAllReduce");
+    FJ_SYM(AllGather, "ncclAllGather");
+    FJ_SYM(Send, "ncclSend");
+    FJ_SYM(Recv, "ncclRecv");
+    FJ_SYM(GroupStart, "ncclGroupStart");
+    FJ_SYM(GroupEnd, "ncclGroupEnd");
+    FJ_SYM(GetErrorString, "ncclGetErrorString");
+#undef FJ_SYM
+    ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce &&
+         api.AllGather && api.Send && api.Recv && api.GroupStart && api.GroupEnd &&
+         api.GetErrorString;
+  });
+  return ok ? &api : nullptr;
+}
+
+#define FJ_NCCL(call)                                                               \
+  do {                                                                              \
+    ncclResult_t r_ = (call);                                                       \
+    if (r_ != ncclSuccess) {                                                        \
+      fj::set_error("NCCL %s: %s", #call, fj::nccl()->GetErrorString(r_));          \
+      return FJ_ERR_CUDA;                                                           \
+    }                                                                               \
+  } while (0)
+
+// ------------------------------------------------------------------ kernels
+// warp per owned row: ids in range, no self-loop, strictly increasing, valid
+// weights; then the column code: own node → local id, remote → n_local + v
+__global__ void k_shard_rows(int64_t n_local, int64_t b0, int64_t n, const int64_t *__restrict__ rp,
+                             const int32_t *__restrict__ col, const float *__restrict__ w,
+                             int32_t *__restrict__ enc, int *__restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n_local; u += nw) {
+    int bad = 0;
+    for (int64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
+      const int32_t v = col[e];
+      if (v < 0 || v >= n) {
+        bad |= 2;
+        continue;
+      }
+      if ((int64_t)v == b0 + u) bad |= 4;
+      if (w && !(w[e] > 0.0f && isfinite(w[e]))) bad |= 8;
+      if (e > rp[u] && col[e - 1] >= v) bad |= 16;
+      enc[e] = (v >= b0 && v < b0 + n_local) ? (int32_t)(v - b0) : (int32_t)(n_local + v);
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0 && bad) atomicOr(err, bad);
+  }
+}
+
+__global__ void k_shard_rowptr(int64_t n, int64_t m, const int64_t *__restrict__ rp,
+                               int *__restrict__ err) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const int64_t x = rp[i];
+  if ((i == 0 && x != 0) || (i == n && x != m) || (i < n && rp[i + 1] < x) || x < 0 || x > m)
+    atomicOr(err, 1);
+}
+
+__global__ void k_shard_rowsum(int64_t n, const int64_t *__restrict__ rp, const float *__restrict__ w,
+                               double *__restrict__ d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
+    double s = 0.0;
+    if (w) {
+      for (int64_t k = rp[u] + lane; k < rp[u + 1]; k += 32) s += (double)w[k];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    } else {
+      s = (double)(rp[u + 1] - rp[u]);
+    }
+    if (lane == 0) d[u] = s;  // d_u = Σ_v a_uv
+  }
+}
+
+// remote column codes n_local + v → n_local + slot·seg_max + (owner's layout position)
+__global__ void k_shard_remap(int64_t m, int32_t *__restrict__ col, int64_t n_local, int rank,
+                              int world, int64_t seg_max, const int64_t *__restrict__ begin,
+                              const int32_t *__restrict__ iperm_all, int *__restrict__ err) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int32_t c = col[k];
+  if (c < n_local) return;
+  const int64_t v = (int64_t)c - n_local;
+  int lo = 0, hi = world - 1;  // owner: last r with begin[r] <= v
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (begin[mid] <= v) lo = mid;
+    else hi = mid - 1;
+  }
+  const int32_t pos = iperm_all[(int64_t)lo * seg_max + (v - begin[lo])];
+  if (lo == rank || pos < 0) {
+    atomicOr(err, 1);
+    return;
+  }
+  const int slot = (lo - rank - 1 + world) % world;
+  col[k] = (int32_t)(n_local + (int64_t)slot * seg_max + pos);
+}
+
+// per-sweep reduction words: relaxations, edge updates, sentinel, bad input
+__global__ void k_shard_counts(const unsigned long long *__restrict__ out, const Scalars *__restrict__ S,
+                               unsigned long long *__restrict__ agg) {
+  agg[0] = out[1];
+  agg[1] = out[2];
+  agg[2] = out[3] == 2 ? 1ull : 0ull;
+  agg[3] = S->bad_input ? 1ull : 0ull;
+}
+
+// Σ (z − mean)², Σ (z − s)², Σ z² with the GLOBAL mean (reading R15)
+__global__ void k_shard_meas2(int64_t n_local, double n_global, const float *__restrict__ z,
+                              const float *__restrict__ s, double *__restrict__ sums) {
+  __shared__ double sm[kBlock / 32];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const double mean = sums[0] / n_global;
+  double P = 0, I = 0, C = 0;
+  if (i < n_local) {
+    const double zi = (double)z[i];
+    P = (zi - mean) * (zi - mean);
+    C = zi * zi;
+    if (s) I = (zi - (double)s[i]) * (zi - (double)s[i]);
+  }
+  P = block_reduce<double>(P, sm);
+  I = block_reduce<double>(I, sm);
+  C = block_reduce<double>(C, sm);
+  if (threadIdx.x == 0) {
+    atomicAdd(sums + 1, P);
+    atomicAdd(sums + 2, I);
+    atomicAdd(sums + 3, C);
+  }
+}
+
+// ------------------------------------------------------------ collectives
+// over the shards this process owns: 1 (NCCL) or all `world` (local)
+enum RedOp { kSum, kMin, kMax };
+enum RedType { kU64, kF32, kF64 };
+
+template <class T>
+static T combine(T a, T b, RedOp op) {
+  return op == kSum ? a + b : op == kMin ? std::min(a, b) : std::max(a, b);
+}
+
+// in-place all-reduce of `len` words of type t
+static fj_status allreduce(fj_shard **sh, int count, void **buf, size_t len, RedType t, RedOp op) {
+  fj_comm *cm = sh[0]->comm;
+  cudaStream_t st = cm->stream;
+  if (!cm->local) {
+    const ncclRedOp_t o = op == kSum ? ncclSum : op == kMin ? ncclMin : ncclMax;
+    const ncclDataType_t dt = t == kU64 ? ncclUint64 : t == kF32 ? ncclFloat32 : ncclFloat64;
+    FJ_NCCL(nccl()->AllReduce(buf[0], buf[0], len, dt, o, cm->nc, st));
+    return FJ_OK;
+  }
+  if (count == 1) return FJ_OK;
+  const size_t word = t == kF32 ? 4 : 8, bytes = len * word;
+  std::vector<unsigned char> h(bytes * count);
+  for (int i = 0; i < count; i++)
+    FJ_CUDA(cudaMemcpyAsync(h.data() + bytes * i, buf[i], bytes, cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  for (size_t k = 0; k < len; k++) {
+    for (int i = 1; i < count; i++) {  // rank order, as a reduction tree would not be: fixed
+      if (t == kU64) {
+        auto *x = reinterpret_cast<unsigned long long *>(h.data());
+        x[k] = combine(x[k], x[len * i + k], op);
+      } else if (t == kF32) {
+        auto *x = reinterpret_cast<float *>(h.data());
+        x[k] = combine(x[k], x[len * i + k], op);
+      } else {
+        auto *x = reinterpret_cast<double *>(h.data());
+        x[k] = combine(x[k], x[len * i + k], op);
+      }
+    }
+  }
+  for (int i = 0; i < count; i++)
+    FJ_CUDA(cudaMemcpyAsync(buf[i], h.data(), bytes, cudaMemcpyHostToDevice, st));
+  FJ_CUDA(cudaStreamSynchronize(st));  // h is stack-owned
+  return FJ_OK;
+}
+
+// offset of rank `src`'s segment in rank `dst`'s buffer
+static int64_t slot_offset(const fj_shard *dst, int src) {
+  const int W = dst->comm->world;
+  return dst->n_local + (int64_t)((src - dst->rank - 1 + W) % W) * dst->seg_max;
+}
+
+// every rank's own segment [0, n_local) into its slot in every other rank's buffer
+static fj_status exchange(fj_shard **sh, int count, double **buf) {
+  fj_comm *cm = sh[0]->comm;
+  cudaStream_t st = cm->stream;
+  const int W = cm->world;
+  if (W == 1) return FJ_OK;
+  if (!cm->local) {
+    const fj_shard *me = sh[0];
+    FJ_NCCL(nccl()->GroupStart());
+    for (int q = 0; q < W; q++) {
+      if (q == me->rank) continue;
+      FJ_NCCL(nccl()->Send(buf[0], (size_t)me->n_local, ncclFloat64, q, cm->nc, st));
+      FJ_NCCL(nccl()->Recv(buf[0] + slot_offset(me, q),
+                           (size_t)(me->begin[q + 1] - me->begin[q]), ncclFloat64, q, cm->nc, st));
+    }
+    FJ_NCCL(nccl()->GroupEnd());
+    return FJ_OK;
+  }
+  for (int r = 0; r < count; r++)
+    for (int q = 0; q < count; q++)
+      if (q != r)
+        FJ_CUDA(cudaMemcpyAsync(buf[q] + slot_offset(sh[q], r), buf[r],
+                                sizeof(double) * sh[r]->n_local, cudaMemcpyDeviceToDevice, st));
+  return FJ_OK;
+}
+
+static fj_status check_set(fj_shard **sh, int count, const char *who) {
+  if (!sh || count < 1 || !sh[0] || !sh[0]->comm) {
+    set_error("%s: need count >= 1 non-null shards", who);
+    return FJ_ERR_INVALID;
+  }
+  fj_comm *cm = sh[0]->comm;
+  if (cm->local ? count != cm->world : count != 1) {
+    set_error("%s: pass %s", who, cm->local ? "all world shards of a local comm" : "exactly one shard");
+    return FJ_ERR_INVALID;
+  }
+  for (int i = 0; i < count; i++) {
+    if (!sh[i] || sh[i]->comm != cm || sh[i]->rank != (cm->local ? i : cm->rank)) {
+      set_error("%s: shards must share one comm and come in rank order", who);
+      return FJ_ERR_INVALID;
+    }
+  }
+  return FJ_OK;
+}
+
+// ------------------------------------------------------------------ create
+static fj_status shard_create_impl(fj_comm *cm, int rank, int64_t n, const int64_t *begin,
+                                   const int64_t *rp_in, const int32_t *col_in, const float *w_in,
+                                   int directed, fj_shard *s) {
+  cudaStream_t st = cm->stream;
+  const int W = cm->world;
+  s->comm = cm;
+  s->rank = rank;
+  s->n = n;
+  s->begin.assign(begin, begin + W + 1);
+  s->n_local = begin[rank + 1] - begin[rank];
+  for (int r = 0; r < W; r++) s->seg_max = std::max(s->seg_max, begin[r + 1] - begin[r]);
+  s->nz = s->n_local + (int64_t)(W - 1) * s->seg_max;
+  int64_t m = 0;
+  FJ_CUDA(cudaMemcpy(&m, rp_in + s->n_local, sizeof(int64_t), cudaMemcpyDefault));
+  if (m < 0 || m >= (int64_t(1) << 40) || (m > 0 && !col_in)) {
+    set_error("fj_shard_create: out_row_ptr[n_local] = %lld out of range or out_col NULL",
+              (long long)m);
+    return FJ_ERR_INVALID;
+  }
+  fj_graph *g = new fj_graph();
+  s->g = g;
+  g->n = s->n_local;
+  g->m = m;
+  g->directed = directed ? 1 : 0;
+  g->weighted = w_in ? 1 : 0;
+  g->stream = st;
+  g->num_sms = cm->num_sms;
+  int64_t *rp = nullptr;
+  int32_t *col = nullptr, *enc = nullptr;
+  float *w = nullptr;
+  int *err = nullptr;
+  const int64_t nl = s->n_local;
+  FJ_CUDA(cudaMallocAsync(&rp, sizeof(int64_t) * (nl + 1), st));
+  FJ_CUDA(cudaMallocAsync(&col, sizeof(int32_t) * (m + 8), st));
+  FJ_CUDA(cudaMallocAsync(&enc, sizeof(int32_t) * (m + 8), st));
+  if (w_in) FJ_CUDA(cudaMallocAsync(&w, sizeof(float) * (m + 8), st));
+  FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
+  FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  FJ_CUDA(cudaMemcpyAsync(rp, rp_in, sizeof(int64_t) * (nl + 1), cudaMemcpyDefault, st));
+  if (m > 0) {
+    FJ_CUDA(cudaMemcpyAsync(col, col_in, sizeof(int32_t) * m, cudaMemcpyDefault, st));
+    if (w_in) FJ_CUDA(cudaMemcpyAsync(w, w_in, sizeof(float) * m, cudaMemcpyDefault, st));
+  }
+  auto done = [&](fj_status rc) {
+    for (void *q : {(void *)rp, (void *)col, (void *)enc, (void *)w, (void *)err})
+      if (q) cudaFreeAsync(q, st);
+    cudaStreamSynchronize(st);
+    return rc;
+  };
+  int herr = 0;
+  count_launch();
+  k_shard_rowptr<<<gridn(nl + 1), kBlock, 0, st>>>(nl, m, rp, err);
+  FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  if (herr) {
+    set_error("fj_shard_create: out_row_ptr must start at 0, be non-decreasing and end at nnz");
+    return done(FJ_ERR_INVALID);
+  }
+  const unsigned wgrid = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((nl * 32 + kBlock - 1) / kBlock, (int64_t)cm->num_sms * 64));
+  count_launch();
+  k_shard_rows<<<wgrid, kBlock, 0, st>>>(nl, begin[rank], n, rp, col, w, enc, err);
+  FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  if (herr) {
+    set_error("fj_shard_create: %s%s%s%s", herr & 2 ? "column id out of range; " : "",
+              herr & 4 ? "self-loop; " : "", herr & 8 ? "weight not positive and finite; " : "",
+              herr & 16 ? "row not strictly increasing (unsorted or duplicate arc); " : "");
+    return done(FJ_ERR_INVALID);
+  }
+  FJ_CUDA(cudaMallocAsync(&g->deg, sizeof(double) * nl, st));
+  count_launch();
+  k_shard_rowsum<<<wgrid, kBlock, 0, st>>>(nl, rp, w, g->deg);
+  fj_status rc = build_layout_from_out(g, rp, enc, w, nullptr, 1, &g->async_layout);
+  return done(rc);
+}
+
+static fj_status connect_impl(fj_shard **sh, int count) {
+  fj_comm *cm = sh[0]->comm;
+  cudaStream_t st = cm->stream;
+  const int W = cm->world;
+  const int64_t seg = sh[0]->seg_max;
+  std::vector<int32_t *> pad(count), all(count);
+  for (int i = 0; i < count; i++) {
+    FJ_CUDA(cudaMallocAsync(&pad[i], sizeof(int32_t) * seg, st));
+    FJ_CUDA(cudaMallocAsync(&all[i], sizeof(int32_t) * seg * W, st));
+    FJ_CUDA(cudaMemsetAsync(pad[i], 0xff, sizeof(int32_t) * seg, st));
+    FJ_CUDA(cudaMemcpyAsync(pad[i], sh[i]->g->async_layout.iperm, sizeof(int32_t) * sh[i]->n_local,
+                            cudaMemcpyDeviceToDevice, st));
+  }
+  if (!cm->local) {
+    FJ_NCCL(nccl()->AllGather(pad[0], all[0], (size_t)seg, ncclInt32, cm->nc, st));
+  } else {
+    for (int i = 0; i < count; i++)
+      for (int r = 0; r < count; r++)
+        FJ_CUDA(cudaMemcpyAsync(all[i] + (int64_t)r * seg, pad[r], sizeof(int32_t) * seg,
+                                cudaMemcpyDeviceToDevice, st));
+  }
+  int *err = nullptr;
+  int64_t *dbeg = nullptr;
+  FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
+  FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  FJ_CUDA(cudaMallocAsync(&dbeg, sizeof(int64_t) * (W + 1), st));
+  FJ_CUDA(cudaMemcpyAsync(dbeg, sh[0]->begin.data(), sizeof(int64_t) * (W + 1),
+                          cudaMemcpyHostToDevice, st));
+  for (int i = 0; i < count; i++) {
+    Layout &L = sh[i]->g->async_layout;
+    if (L.m > 0) {
+      count_launch();
+      k_shard_remap<<<gridn(L.m), kBlock, 0, st>>>(L.m, L.col, sh[i]->n_local, sh[i]->rank, W, seg,
+                                                   dbeg, all[i], err);
+    }
+  }
+  int herr = 0;
+  FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < count; i++) {
+    cudaFreeAsync(pad[i], st);
+    cudaFreeAsync(all[i], st);
+  }
+  cudaFreeAsync(err, st);
+  cudaFreeAsync(dbeg, st);
+  FJ_CUDA(cudaStreamSynchronize(st));
+  if (herr) {
+    set_error("fj_shard_connect: inconsistent partitions across ranks");
+    return FJ_ERR_INVALID;
+  }
+  for (int i = 0; i < count; i++) sh[i]->connected = true;
+  return FJ_OK;
+}
+
+// ------------------------------------------------------------------- solve
+struct ShardWork {
+  Staged s{};
+  float *s_l = nullptr, *smm = nullptr, *zo = nullptr;
+  double *z = nullptr, *zp = nullptr;
+  double2 *partial = nullptr;
+  int *arrive = nullptr;
+  Scalars *S = nullptr;
+  unsigned *ctl = nullptr;
+  SweepCounters *cnt = nullptr;
+  unsigned long long *outv = nullptr, *agg = nullptr;
+  KP p{};
+};
+
+static fj_status shard_solve_impl(fj_shard **sh, int count, const float *const *s_in, double eps,
+                                  double omega, const fj_opts *o, float *const *z_out,
+                                  double *const *zp_out, fj_stats *st_out) {
+  NvtxRange nv("fj_shard_solve");
+  fj_comm *cm = sh[0]->comm;
+  cudaStream_t st = cm->stream;
+  fj_stats stats{};
+  stats.colors = 1;
+  std::vector<ShardWork> wk(count);
+  std::vector<void *> red(count);
+  std::vector<double *> zb(count);
+  cudaEvent_t e0, e1, es0, es1;
+  FJ_CUDA(cudaEventCreate(&e0));
+  FJ_CUDA(cudaEventCreate(&e1));
+  FJ_CUDA(cudaEventCreate(&es0));
+  FJ_CUDA(cudaEventCreate(&es1));
+  FJ_CUDA(cudaEventRecord(e0, st));
+  for (int i = 0; i < count; i++) {
+    ShardWork &w = wk[i];
+    const Layout &L = sh[i]->g->async_layout;
+    const int64_t nl = sh[i]->n_local;
+    FJ_TRY(stage_in(s_in[i], nl, st, w.s));
+    FJ_CUDA(cudaMallocAsync(&w.s_l, sizeof(float) * nl, st));
+    FJ_CUDA(cudaMallocAsync(&w.smm, sizeof(float) * 2, st));
+    FJ_CUDA(cudaMallocAsync(&w.z, sizeof(double) * sh[i]->nz, st));
+    FJ_CUDA(cudaMemsetAsync(w.z, 0, sizeof(double) * sh[i]->nz, st));
+    FJ_CUDA(cudaMallocAsync(&w.S, sizeof(Scalars), st));
+    FJ_CUDA(cudaMallocAsync(&w.partial, sizeof(double2) * std::max(1, L.npartials), st));
+    FJ_CUDA(cudaMallocAsync(&w.arrive, sizeof(int) * std::max(1, L.npartials), st));
+    FJ_CUDA(cudaMemsetAsync(w.arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
+    FJ_CUDA(cudaMallocAsync(&w.ctl, sizeof(unsigned) * kCtlWords, st));
+    FJ_CUDA(cudaMallocAsync(&w.cnt, sizeof(SweepCounters) * 3, st));
+    FJ_CUDA(cudaMallocAsync(&w.outv, sizeof(unsigned long long) * 12, st));
+    w.agg = w.outv + 8;
+    if (!is_device_ptr(z_out[i])) FJ_CUDA(cudaMallocAsync(&w.zo, sizeof(float) * nl, st));
+    if (zp_out && zp_out[i] && !is_device_ptr(zp_out[i]))
+      FJ_CUDA(cudaMallocAsync(&w.zp, sizeof(double) * nl, st));
+    size_t tmp = 0, tmp2 = 0;
+    FJ_CUDA(cub::DeviceReduce::Min(nullptr, tmp, w.s.dev, w.smm, nl, st));
+    FJ_CUDA(cub::DeviceReduce::Max(nullptr, tmp2, w.s.dev, w.smm + 1, nl, st));
+    tmp = std::max(tmp, tmp2);
+    void *t = nullptr;
+    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    FJ_CUDA(cub::DeviceReduce::Min(t, tmp, w.s.dev, w.smm, nl, st));
+    FJ_CUDA(cub::DeviceReduce::Max(t, tmp, w.s.dev, w.smm + 1, nl, st));
+    FJ_CUDA(cudaFreeAsync(t, st));
+  }
+  // a2: global shift from the global min / max of s (Alg. 2)
+  {
+    std::vector<void *> lo(count), hi(count);
+    for (int i = 0; i < count; i++) {
+      lo[i] = wk[i].smm;
+      hi[i] = wk[i].smm + 1;
+    }
+    FJ_TRY(allreduce(sh, count, lo.data(), 1, kF32, kMin));
+    FJ_TRY(allreduce(sh, count, hi.data(), 1, kF32, kMax));
+  }
+  for (int i = 0; i < count; i++) {
+    ShardWork &w = wk[i];
+    const Layout &L = sh[i]->g->async_layout;
+    count_launch();
+    k_scalars<<<1, 1, 0, st>>>(w.smm, w.smm + 1, eps, o->sigma, o->c, w.S);
+    count_launch();
+    k_init<<<gridn(sh[i]->n_local), kBlock, 0, st>>>(sh[i]->n_local, L.perm, L.rp, w.s.dev, w.S,
+                                                     w.s_l, w.z, nullptr);
+    KP &p = w.p;
+    p = make_kp(sh[i]->g, L);
+    p.s = w.s_l;
+    p.z = w.z;
+    p.sc = w.S;
+    p.omega = omega;
+    p.theta = 1.0;
+    p.partial = w.partial;
+    p.arrive = w.arrive;
+    p.max_sweeps = 1;  // one sweep per launch: the exchange follows every sweep
+    p.ctr = w.ctl;
+    p.bar = w.ctl + 8;
+    p.cnt = w.cnt;
+    p.out = w.outv;
+    p.cert_max = w.outv + 4;
+    zb[i] = w.z;
+    red[i] = w.agg;
+  }
+  FJ_TRY(exchange(sh, count, zb.data()));
+
+  const bool W = sh[0]->g->weighted != 0;
+  const void *fn = sweep_kernel(W);
+  const size_t smem = sweep_kernel_smem();
+  FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = persistent_grid(fn, cm->num_sms, smem);
+  const void *cf = W ? (const void *)k_pass<CERT, true> : (const void *)k_pass<CERT, false>;
+  const int cgrid = persistent_grid(cf, cm->num_sms);
+  float ms_sweep = 0.f;
+  int rounds = 0, max_sweeps = o->max_sweeps;
+  unsigned long long bad_input = 0;
+  double theta = 1.0;
+  for (;;) {
+    int sw = 0;
+    stats.reason = 1;
+    while (sw < max_sweeps) {
+      FJ_CUDA(cudaEventRecord(es0, st));
+      for (int i = 0; i < count; i++) {
+        ShardWork &w = wk[i];
+        w.p.theta = theta;
+        FJ_CUDA(cudaMemsetAsync(w.ctl, 0, sizeof(unsigned) * kCtlWords, st));
+        FJ_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(SweepCounters) * 3, st));
+        FJ_CUDA(cudaMemsetAsync(w.outv, 0, sizeof(unsigned long long) * 4, st));
+        void *args[] = {&w.p};
+        count_launch();
+        FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, smem, st));
+        count_launch();
+        k_shard_counts<<<1, 1, 0, st>>>(w.outv, w.S, w.agg);
+      }
+      FJ_CUDA(cudaEventRecord(es1, st));
+      FJ_TRY(allreduce(sh, count, red.data(), 4, kU64, kSum));
+      FJ_TRY(exchange(sh, count, zb.data()));
+      unsigned long long h[4];
+      FJ_CUDA(cudaMemcpyAsync(h, wk[0].agg, sizeof(h), cudaMemcpyDeviceToHost, st));
+      FJ_CUDA(cudaStreamSynchronize(st));
+      float a = 0.f;
+      FJ_CUDA(cudaEventElapsedTime(&a, es0, es1));
+      ms_sweep += a;
+      sw++;
+      stats.sweeps++;
+      stats.relaxations += (int64_t)h[0];
+      stats.edge_updates += (int64_t)h[1];
+      bad_input |= h[3];
+      if (h[2] || h[3]) {
+        stats.reason = 2;
+        break;
+      }
+      if (h[0] == 0) {  // no rank relaxed: Q = ∅
+        stats.reason = 0;
+        break;
+      }
+    }
+    if (stats.reason != 0 || !o->certify) break;
+    // fp64 compensated certificate on every rank; the maximum decides
+    std::vector<void *> cb(count);
+    for (int i = 0; i < count; i++) {
+      ShardWork &w = wk[i];
+      FJ_CUDA(cudaMemsetAsync(w.outv + 4, 0, sizeof(unsigned long long), st));
+      KP q = w.p;
+      q.ctr = w.ctl + 5;
+      void *cargs[] = {&q};
+      count_launch();
+      FJ_CUDA(cudaLaunchKernel(cf, cgrid, kBlock, cargs, 0, st));
+      cb[i] = w.outv + 4;
+    }
+    FJ_TRY(allreduce(sh, count, cb.data(), 1, kU64, kMax));  // non-negative doubles order as bits
+    unsigned long long hb = 0;
+    FJ_CUDA(cudaMemcpyAsync(&hb, wk[0].outv + 4, sizeof(hb), cudaMemcpyDeviceToHost, st));
+    FJ_CUDA(cudaStreamSynchronize(st));
+    stats.cert_ratio = __builtin_bit_cast(double, hb);
+    if (stats.cert_ratio <= 1.0 || rounds >= o->cert_rounds) break;
+    rounds++;  // resume from ẑ with a stricter sweep threshold (reading R21)
+    theta *= 0.5;
+    max_sweeps = std::min(o->max_sweeps, 2000);
+  }
+  stats.cert_rounds = rounds;
+  stats.phases = stats.sweeps;
+  int64_t active = 0, arcs = 0, empty = 0;
+  for (int i = 0; i < count; i++) {
+    active += sh[i]->g->async_layout.active_rows;
+    arcs += sh[i]->g->async_layout.m;
+    empty += sh[i]->g->async_layout.empty_rows;
+  }
+  stats.rows_read = stats.sweeps * active;  // this process's shards
+  stats.arcs_read = stats.sweeps * arcs;
+  stats.relaxations += empty;
+
+  // a6: unshift into each shard's slice
+  Scalars hs{};
+  for (int i = 0; i < count; i++) {
+    ShardWork &w = wk[i];
+    const int64_t nl = sh[i]->n_local;
+    float *zo = w.zo ? w.zo : z_out[i];
+    double *zp = (zp_out && zp_out[i]) ? (w.zp ? w.zp : zp_out[i]) : nullptr;
+    count_launch();
+    k_finalize<<<gridn(nl), kBlock, 0, st>>>(nl, sh[i]->g->async_layout.iperm, w.z, w.S, zo, zp);
+    if (w.zo) FJ_CUDA(cudaMemcpyAsync(z_out[i], w.zo, sizeof(float) * nl, cudaMemcpyDeviceToHost, st));
+    if (w.zp) FJ_CUDA(cudaMemcpyAsync(zp_out[i], w.zp, sizeof(double) * nl, cudaMemcpyDeviceToHost, st));
+  }
+  FJ_CUDA(cudaMemcpyAsync(&hs, wk[0].S, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaEventRecord(e1, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  FJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  stats.solve_ms = ms;
+  stats.sweep_ms = ms_sweep;
+  stats.c = hs.c;
+  stats.eps_prime = hs.eps_p;
+  hs.bad_input = bad_input ? 1 : 0;
+  for (ShardWork &w : wk) {
+    for (void *q : {(void *)w.s_l, (void *)w.smm, (void *)w.zo, (void *)w.z, (void *)w.zp,
+                    (void *)w.partial, (void *)w.arrive, (void *)w.S, (void *)w.ctl, (void *)w.cnt,
+                    (void *)w.outv, (void *)w.s.owned})
+      if (q) cudaFreeAsync(q, st);
+  }
+  for (cudaEvent_t e : {e0, e1, es0, es1}) cudaEventDestroy(e);
+  FJ_CUDA(cudaStreamSynchronize(st));
+  FJ_CUDA(cudaGetLastError());
+  fj_status rc = finish_status(hs, stats, o, omega);
+  if (st_out) *st_out = stats;
+  return rc;
+}
+
+static fj_status shard_measures_impl(fj_shard **sh, int count, const float *const *z_in,
+                                     const float *const *s_in, fj_measures_t *out) {
+  NvtxRange nv("fj_shard_measures");
+  fj_comm *cm = sh[0]->comm;
+  cudaStream_t st = cm->stream;
+  std::vector<Staged> z(count), s(count);
+  std::vector<double *> zl(count), sums(count);
+  std::vector<void *> red(count);
+  std::vector<unsigned *> ctr(count);
+  for (int i = 0; i < count; i++) {
+    const int64_t nl = sh[i]->n_local;
+    FJ_TRY(stage_in(z_in[i], nl, st, z[i]));
+    if (s_in && s_in[i]) FJ_TRY(stage_in(s_in[i], nl, st, s[i]));
+    FJ_CUDA(cudaMallocAsync(&zl[i], sizeof(double) * sh[i]->nz, st));
+    FJ_CUDA(cudaMemsetAsync(zl[i], 0, sizeof(double) * sh[i]->nz, st));
+    FJ_CUDA(cudaMallocAsync(&sums[i], sizeof(double) * 5, st));
+    FJ_CUDA(cudaMemsetAsync(sums[i], 0, sizeof(double) * 5, st));
+    FJ_CUDA(cudaMallocAsync(&ctr[i], sizeof(unsigned), st));
+    FJ_CUDA(cudaMemsetAsync(ctr[i], 0, sizeof(unsigned), st));
+    count_launch();
+    k_meas_nodes1<<<gridn(nl), kBlock, 0, st>>>(nl, sh[i]->g->async_layout.perm, z[i].dev, zl[i],
+                                                 sums[i]);
+    red[i] = sums[i];
+  }
+  // remote z for the arc pass, then D along the owned out-rows
+  FJ_TRY(exchange(sh, count, zl.data()));
+  const bool W = sh[0]->g->weighted != 0;
+  const void *fn = W ? (const void *)k_pass<DIS, true> : (const void *)k_pass<DIS, false>;
+  for (int i = 0; i < count; i++) {
+    KP p = make_kp(sh[i]->g, sh[i]->g->async_layout);
+    p.z = zl[i];
+    p.ctr = ctr[i];
+    p.dis = sums[i] + 4;
+    void *args[] = {&p};
+    count_launch();
+    FJ_CUDA(cudaLaunchKernel(fn, persistent_grid(fn, cm->num_sms), kBlock, args, 0, st));
+  }
+  // global Σ z → mean on every rank, then the node sums with that mean
+  FJ_TRY(allreduce(sh, count, red.data(), 1, kF64, kSum));
+  for (int i = 0; i < count; i++) {
+    count_launch();
+    k_shard_meas2<<<gridn(sh[i]->n_local), kBlock, 0, st>>>(
+        sh[i]->n_local, (double)sh[i]->n, z[i].dev, (s_in && s_in[i]) ? s[i].dev : nullptr, sums[i]);
+  }
+  std::vector<void *> tail(count);
+  for (int i = 0; i < count; i++) tail[i] = sums[i] + 1;
+  FJ_TRY(allreduce(sh, count, tail.data(), 4, kF64, kSum));
+  double h[5];
+  FJ_CUDA(cudaMemcpyAsync(h, sums[0], sizeof(h), cudaMemcpyDeviceToHost, st));
+  FJ_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < count; i++) {
+    for (void *q : {(void *)zl[i], (void *)sums[i], (void *)ctr[i], (void *)z[i].owned,
+                    (void *)s[i].owned})
+      if (q) cudaFreeAsync(q, st);
+  }
+  FJ_CUDA(cudaStreamSynchronize(st));
+  FJ_CUDA(cudaGetLastError());
+  out->polarization = h[1];
+  out->disagreement = sh[0]->g->directed ? h[4] : 0.5 * h[4];  // reading R14
+  out->internal_conflict = (s_in && s_in[0]) ? h[2] : 0.0;
+  out->controversy = h[3];
+  return FJ_OK;
+}
+
+}  // namespace fj
+
+// ------------------------------------------------------------------- C-ABI
+extern "C" {
+
+fj_status fj_shard_plan(int64_t n, const int64_t *row_ptr, int world, int64_t *begin) {
+  if (n < 1 || world < 1 || world > n || !row_ptr || !begin) {
+    fj::set_error("fj_shard_plan: need 1 <= world <= n and non-null row_ptr, begin");
+    return FJ_ERR_INVALID;
+  }
+  const int64_t m = row_ptr[n];
+  if (row_ptr[0] != 0 || m < 0) {
+    fj::set_error("fj_shard_plan: row_ptr must start at 0 and end at nnz >= 0");
+    return FJ_ERR_INVALID;
+  }
+  for (int64_t u = 0; u < n; u++)
+    if (row_ptr[u + 1] < row_ptr[u]) {
+      fj::set_error("fj_shard_plan: row_ptr must be non-decreasing");
+      return FJ_ERR_INVALID;
+    }
+  // work of rows [0, u) = row_ptr[u] + u (arcs plus one per row)
+  const double total = (double)m + (double)n;
+  begin[0] = 0;
+  int64_t u = 0;
+  for (int r = 1; r < world; r++) {
+    const double target = total * r / world;
+    while (u < n && (double)(row_ptr[u] + u) < target) u++;
+    begin[r] = std::min(std::max(u, begin[r - 1] + 1), n - (world - r));
+    u = begin[r];
+  }
+  begin[world] = n;
+  return FJ_OK;
+}
+
+fj_status fj_comm_unique_id(void *id128) {
+  if (!id128) {
+    fj::set_error("fj_comm_unique_id: null id");
+    return FJ_ERR_INVALID;
+  }
+  if (!fj::nccl()) {
+    fj::set_error("fj_comm_unique_id: libnccl.so.2 could not be loaded");
+    return FJ_ERR_CUDA;
+  }
+  ncclUniqueId id;
+  FJ_NCCL(fj::nccl()->GetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "NCCL unique id size");
+  memcpy(id128, &id, sizeof(id));
+  return FJ_OK;
+}
+
+static fj_status comm_base(fj_comm *c) {
+  int dev = 0;
+  FJ_CUDA(cudaGetDevice(&dev));
+  FJ_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  FJ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  cudaMemPool_t pool;  // keep stream-ordered allocations pooled (as graph.cu)
+  FJ_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = ~0ull;
+  FJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  return FJ_OK;
+}
+
+fj_status fj_comm_create(const void *id128, int rank, int world, fj_comm_t *out) {
+  if (!out || !id128 || world < 1 || rank < 0 || rank >= world) {
+    fj::set_error("fj_comm_create: need id, 0 <= rank < world, out");
+    return FJ_ERR_INVALID;
+  }
+  *out = nullptr;
+  if (!fj::nccl()) {
+    fj::set_error("fj_comm_create: libnccl.so.2 could not be loaded");
+    return FJ_ERR_CUDA;
+  }
+  fj_comm *c = new fj_comm();
+  c->world = world;
+  c->rank = rank;
+  c->local = false;
+  fj_status s = comm_base(c);
+  if (s == FJ_OK) {
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    ncclResult_t r = fj::nccl()->CommInitRank(&c->nc, world, id, rank);
+    if (r != ncclSuccess) {
+      fj::set_error("NCCL ncclCommInitRank: %s", fj::nccl()->GetErrorString(r));
+      s = FJ_ERR_CUDA;
+    }
+  }
+  if (s != FJ_OK) {
+    fj_comm_destroy(c);
+    return s;
+  }
+  *out = c;
+  return FJ_OK;
+}
+
+fj_status fj_comm_create_local(int world, fj_comm_t *out) {
+  if (!out || world < 1) {
+    fj::set_error("fj_comm_create_local: need world >= 1 and out");
+    return FJ_ERR_INVALID;
+  }
+  *out = nullptr;
+  fj_comm *c = new fj_comm();
+  c->world = world;
+  c->local = true;
+  fj_status s = comm_base(c);
+  if (s != FJ_OK) {
+    fj_comm_destroy(c);
+    return s;
+  }
+  *out = c;
+  return FJ_OK;
+}
+
+fj_status fj_comm_destroy(fj_comm_t c) {
+  if (!c) return FJ_OK;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->nc && fj::nccl()) fj::nccl()->CommDestroy(c->nc);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return FJ_OK;
+}
+
+fj_status fj_shard_create(fj_comm_t comm, int rank, int64_t n, const int64_t *begin,
+                          const int64_t *out_row_ptr, const int32_t *out_col, const float *out_w,
+                          int directed, fj_shard_t *out) {
+  if (!out) {
+    fj::set_error("fj_shard_create: out is NULL");
+    return FJ_ERR_INVALID;
+  }
+  *out = nullptr;
+  if (!comm || !begin || !out_row_ptr || rank < 0 || rank >= comm->world || n < 1 ||
+      n >= (int64_t(1) << 30)) {
+    fj::set_error("fj_shard_create: need comm, begin, row_ptr, 0 <= rank < world, 1 <= n < 2^30");
+    return FJ_ERR_INVALID;
+  }
+  if (!comm->local && rank != comm->rank) {
+    fj::set_error("fj_shard_create: rank %d on the NCCL comm of rank %d", rank, comm->rank);
+    return FJ_ERR_INVALID;
+  }
+  if (begin[0] != 0 || begin[comm->world] != n) {
+    fj::set_error("fj_shard_create: begin[0] must be 0 and begin[world] = n");
+    return FJ_ERR_INVALID;
+  }
+  for (int r = 0; r < comm->world; r++)
+    if (begin[r + 1] <= begin[r]) {
+      fj::set_error("fj_shard_create: every part must be non-empty (begin strictly increasing)");
+      return FJ_ERR_INVALID;
+    }
+  fj_shard *s = new fj_shard();
+  nvtxRangePushA("fj_shard_create");
+  fj_status rc = fj::shard_create_impl(comm, rank, n, begin, out_row_ptr, out_col, out_w, directed, s);
+  nvtxRangePop();
+  if (rc != FJ_OK) {
+    fj_shard_destroy(s);
+    return rc;
+  }
+  *out = s;
+  return FJ_OK;
+}
+
+fj_status fj_shard_connect(fj_shard_t *shards, int count) {
+  FJ_TRY(fj::check_set(shards, count, "fj_shard_connect"));
+  return fj::connect_impl(shards, count);
+}
+
+fj_status fj_shard_solve(fj_shard_t *shards, int count, const float *const *s, double eps,
+                         double omega, const fj_opts *o, float *const *z_out,
+                         double *const *zprime_out, fj_stats *st) {
+  FJ_TRY(fj::check_set(shards, count, "fj_shard_solve"));
+  for (int i = 0; i < count; i++)
+    if (!shards[i]->connected) {
+      fj::set_error("fj_shard_solve: call fj_shard_connect first");
+      return FJ_ERR_INVALID;
+    }
+  fj_opts d;
+  fj_opts_default(&d);
+  if (o) d = *o;
+  if (d.sigma <= 0) d.sigma = 1e-5;
+  if (d.max_sweeps <= 0) d.max_sweeps = 1000000;
+  if (d.cert_rounds < 0) d.cert_rounds = 3;
+  if (!s || !z_out || !(eps > 0 && eps < 1) || !(omega > 0 && omega < 2) ||
+      (d.method != FJ_METHOD_AUTO && d.method != FJ_METHOD_ASYNC) || d.z_init || d.zprime_out) {
+    fj::set_error("fj_shard_solve: need s, z_out, 0 < eps < 1, 0 < omega < 2, method AUTO/ASYNC, "
+                  "no z_init / zprime_out in opts");
+    return FJ_ERR_INVALID;
+  }
+  for (int i = 0; i < count; i++)
+    if (!s[i] || !z_out[i]) {
+      fj::set_error("fj_shard_solve: null s[%d] or z_out[%d]", i, i);
+      return FJ_ERR_INVALID;
+    }
+  return fj::shard_solve_impl(shards, count, s, eps, omega, &d, z_out, zprime_out, st);
+}
+
+fj_status fj_shard_measures(fj_shard_t *shards, int count, const float *const *z,
+                            const float *const *s, fj_measures_t *out) {
+  FJ_TRY(fj::check_set(shards, count, "fj_shard_measures"));
+  if (!z || !out) {
+    fj::set_error("fj_shard_measures: need z and out");
+    return FJ_ERR_INVALID;
+  }
+  for (int i = 0; i < count; i++)
+    if (!shards[i]->connected || !z[i]) {
+      fj::set_error("fj_shard_measures: shard %d not connected or z[%d] null", i, i);
+      return FJ_ERR_INVALID;
+    }
+  return fj::shard_measures_impl(shards, count, z, s, out);
+}
+
+fj_status fj_shard_destroy(fj_shard_t s) {
+  if (!s) return FJ_OK;
+  if (s->g) fj_graph_destroy(s->g);
+  delete s;
+  return FJ_OK;
+}
+
+}  // extern "C"

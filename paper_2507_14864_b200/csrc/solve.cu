@@ -445,6 +445,12 @@ __global__ void k_meas_nodes2(int64_t n, const float *__restrict__ z, const floa
   }
 }
 
+// the one-sweep-per-launch entry of the sharded solve (shard.cu)
+const void *sweep_kernel(bool weighted) {
+  return weighted ? (const void *)k_sweep<true, false> : (const void *)k_sweep<false, false>;
+}
+size_t sweep_kernel_smem() { return (kBlock / 32) * kWarpTileArcs * sizeof(double); }
+
 fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, const fj_opts *o,
                      float *z_out, fj_stats *st_out) {
   NvtxRange nv("fj_solve");

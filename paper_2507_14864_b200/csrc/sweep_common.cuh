@@ -671,6 +671,8 @@ static fj_status finish_status(const Scalars &hs, fj_stats &stats, const fj_opts
 
 
 // implemented in push.cu / batch.cu / solve.cu
+const void *sweep_kernel(bool weighted);  // k_sweep<W, false> (solve.cu)
+size_t sweep_kernel_smem();
 fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double omega,
                           const fj_opts *o, float *z_out, fj_stats *st_out);
 fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, double omega,
