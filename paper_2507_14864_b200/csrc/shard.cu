@@ -59,6 +59,9 @@ struct fj_shard {
 
 namespace fj {
 
+constexpr int kMaxLocal = 64;    // shards of one in-process comm
+constexpr int kSweepBatch = 16;  // sweeps queued per host check (sharded loop)
+
 // ------------------------------------------------------------- NCCL (dlopen)
 struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId *);
@@ -194,6 +197,25 @@ __global__ void k_shard_counts(const unsigned long long *__restrict__ out, const
   agg[3] = S->bad_input ? 1ull : 0ull;
 }
 
+// the loop ends after a sweep with no relaxation on any rank (Q = ∅),
+// a sentinel hit or bad input: later queued sweeps see the flag and return
+__global__ void k_shard_stop(const unsigned long long *__restrict__ agg,
+                             unsigned long long *__restrict__ stop) {
+  if (agg[0] == 0ull || agg[2] || agg[3]) *stop = 1ull;
+}
+
+// in-process all-reduce (sum) of `len` u64 words over shards on one device
+struct PtrSet {
+  unsigned long long *p[kMaxLocal];
+};
+__global__ void k_local_sum(PtrSet ps, int count, int len) {
+  const int k = threadIdx.x;
+  if (k >= len) return;
+  unsigned long long a = 0ull;
+  for (int i = 0; i < count; i++) a += ps.p[i][k];
+  for (int i = 0; i < count; i++) ps.p[i][k] = a;
+}
+
 // Σ (z − mean)², Σ (z − s)², Σ z² with the GLOBAL mean (reading R15)
 __global__ void k_shard_meas2(int64_t n_local, double n_global, const float *__restrict__ z,
                               const float *__restrict__ s, double *__restrict__ sums) {
@@ -238,6 +260,13 @@ static fj_status allreduce(fj_shard **sh, int count, void **buf, size_t len, Red
     return FJ_OK;
   }
   if (count == 1) return FJ_OK;
+  if (t == kU64 && op == kSum && len <= 32) {  // per-sweep counters: stay on the device
+    PtrSet ps{};
+    for (int i = 0; i < count; i++) ps.p[i] = static_cast<unsigned long long *>(buf[i]);
+    count_launch();
+    k_local_sum<<<1, 32, 0, st>>>(ps, count, (int)len);
+    return FJ_OK;
+  }
   const size_t word = t == kF32 ? 4 : 8, bytes = len * word;
   std::vector<unsigned char> h(bytes * count);
   for (int i = 0; i < count; i++)
@@ -456,7 +485,7 @@ struct ShardWork {
   Scalars *S = nullptr;
   unsigned *ctl = nullptr;
   SweepCounters *cnt = nullptr;
-  unsigned long long *outv = nullptr, *agg = nullptr;
+  unsigned long long *outv = nullptr, *stop = nullptr, *agg = nullptr;  // agg: [batch][4]
   KP p{};
 };
 
@@ -492,8 +521,9 @@ static fj_status shard_solve_impl(fj_shard **sh, int count, const float *const *
     FJ_CUDA(cudaMemsetAsync(w.arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
     FJ_CUDA(cudaMallocAsync(&w.ctl, sizeof(unsigned) * kCtlWords, st));
     FJ_CUDA(cudaMallocAsync(&w.cnt, sizeof(SweepCounters) * 3, st));
-    FJ_CUDA(cudaMallocAsync(&w.outv, sizeof(unsigned long long) * 12, st));
-    w.agg = w.outv + 8;
+    FJ_CUDA(cudaMallocAsync(&w.outv, sizeof(unsigned long long) * (9 + 4 * kSweepBatch), st));
+    w.stop = w.outv + 8;
+    w.agg = w.outv + 9;
     if (!is_device_ptr(z_out[i])) FJ_CUDA(cudaMallocAsync(&w.zo, sizeof(float) * nl, st));
     if (zp_out && zp_out[i] && !is_device_ptr(zp_out[i]))
       FJ_CUDA(cudaMallocAsync(&w.zp, sizeof(double) * nl, st));
@@ -540,8 +570,8 @@ static fj_status shard_solve_impl(fj_shard **sh, int count, const float *const *
     p.cnt = w.cnt;
     p.out = w.outv;
     p.cert_max = w.outv + 4;
+    p.stop = w.stop;
     zb[i] = w.z;
-    red[i] = w.agg;
   }
   FJ_TRY(exchange(sh, count, zb.data()));
 
@@ -559,41 +589,59 @@ static fj_status shard_solve_impl(fj_shard **sh, int count, const float *const *
   for (;;) {
     int sw = 0;
     stats.reason = 1;
-    while (sw < max_sweeps) {
+    for (int i = 0; i < count; i++) {
+      wk[i].p.theta = theta;
+      FJ_CUDA(cudaMemsetAsync(wk[i].stop, 0, sizeof(unsigned long long), st));
+    }
+    // queue a batch of sweeps (sweep → counters → all-reduce → stop flag →
+    // exchange); the host reads the batch's counters once.  Sweeps queued
+    // after the stopping one return at once (k_sweep reads the flag).
+    while (sw < max_sweeps && stats.reason == 1) {
+      const int nb = std::min(kSweepBatch, max_sweeps - sw);
       FJ_CUDA(cudaEventRecord(es0, st));
-      for (int i = 0; i < count; i++) {
-        ShardWork &w = wk[i];
-        w.p.theta = theta;
-        FJ_CUDA(cudaMemsetAsync(w.ctl, 0, sizeof(unsigned) * kCtlWords, st));
-        FJ_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(SweepCounters) * 3, st));
-        FJ_CUDA(cudaMemsetAsync(w.outv, 0, sizeof(unsigned long long) * 4, st));
-        void *args[] = {&w.p};
-        count_launch();
-        FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, smem, st));
-        count_launch();
-        k_shard_counts<<<1, 1, 0, st>>>(w.outv, w.S, w.agg);
+      for (int j = 0; j < nb; j++) {
+        for (int i = 0; i < count; i++) {
+          ShardWork &w = wk[i];
+          FJ_CUDA(cudaMemsetAsync(w.ctl, 0, sizeof(unsigned) * kCtlWords, st));
+          FJ_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(SweepCounters) * 3, st));
+          FJ_CUDA(cudaMemsetAsync(w.outv, 0, sizeof(unsigned long long) * 4, st));
+          void *args[] = {&w.p};
+          count_launch();
+          FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, smem, st));
+          count_launch();
+          k_shard_counts<<<1, 1, 0, st>>>(w.outv, w.S, w.agg + 4 * j);
+          red[i] = w.agg + 4 * j;
+        }
+        FJ_TRY(allreduce(sh, count, red.data(), 4, kU64, kSum));
+        for (int i = 0; i < count; i++) {
+          count_launch();
+          k_shard_stop<<<1, 1, 0, st>>>(wk[i].agg + 4 * j, wk[i].stop);
+        }
+        FJ_TRY(exchange(sh, count, zb.data()));
       }
       FJ_CUDA(cudaEventRecord(es1, st));
-      FJ_TRY(allreduce(sh, count, red.data(), 4, kU64, kSum));
-      FJ_TRY(exchange(sh, count, zb.data()));
-      unsigned long long h[4];
-      FJ_CUDA(cudaMemcpyAsync(h, wk[0].agg, sizeof(h), cudaMemcpyDeviceToHost, st));
+      std::vector<unsigned long long> h(4 * nb);
+      FJ_CUDA(cudaMemcpyAsync(h.data(), wk[0].agg, sizeof(unsigned long long) * 4 * nb,
+                              cudaMemcpyDeviceToHost, st));
       FJ_CUDA(cudaStreamSynchronize(st));
       float a = 0.f;
       FJ_CUDA(cudaEventElapsedTime(&a, es0, es1));
       ms_sweep += a;
-      sw++;
-      stats.sweeps++;
-      stats.relaxations += (int64_t)h[0];
-      stats.edge_updates += (int64_t)h[1];
-      bad_input |= h[3];
-      if (h[2] || h[3]) {
-        stats.reason = 2;
-        break;
-      }
-      if (h[0] == 0) {  // no rank relaxed: Q = ∅
-        stats.reason = 0;
-        break;
+      for (int j = 0; j < nb; j++) {
+        const unsigned long long *q = h.data() + 4 * j;
+        sw++;
+        stats.sweeps++;
+        stats.relaxations += (int64_t)q[0];
+        stats.edge_updates += (int64_t)q[1];
+        bad_input |= q[3];
+        if (q[2] || q[3]) {
+          stats.reason = 2;
+          break;
+        }
+        if (q[0] == 0) {  // no rank relaxed: Q = ∅
+          stats.reason = 0;
+          break;
+        }
       }
     }
     if (stats.reason != 0 || !o->certify) break;
@@ -826,8 +874,8 @@ fj_status fj_comm_create(const void *id128, int rank, int world, fj_comm_t *out)
 }
 
 fj_status fj_comm_create_local(int world, fj_comm_t *out) {
-  if (!out || world < 1) {
-    fj::set_error("fj_comm_create_local: need world >= 1 and out");
+  if (!out || world < 1 || world > fj::kMaxLocal) {
+    fj::set_error("fj_comm_create_local: need 1 <= world <= %d and out", fj::kMaxLocal);
     return FJ_ERR_INVALID;
   }
   *out = nullptr;

@@ -257,6 +257,8 @@ template <bool W, bool TMA>
 __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
   extern __shared__ double s_prod[];  // per warp: a WarpSmem (TMA stages + products)
   __shared__ unsigned long long s_dec[3];
+  // sharded solve: sweeps queued after the global stopping sweep do nothing
+  if (p.stop && __ldcg(p.stop) != 0ull) return;
   const Scalars S = *p.sc;
   WarpSmem *ws = reinterpret_cast<WarpSmem *>(s_prod) + (threadIdx.x >> 5);
   uint32_t phase_bits = 0;

@@ -74,6 +74,7 @@ struct KP {
   int dbg;                       // diagnostics (env FJ_DBG_SKIP): 1 skip warp units, 2 skip tiles
   int dyn;                       // dynamic work claiming in k_sweep (env FJ_DYN)
   int symm;                      // alternate sweep direction (env FJ_SYMM)
+  const unsigned long long *stop;  // sharded solve: nonzero = the loop has ended (k_sweep)
 };
 
 // CSR streams are read once per sweep: read-only path, no L1 allocation, so
