@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true",
                     help="skip the per-omega time-to-eps table of the config (untimed)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
+                    help="N>1: independent replicas (default) or ONE problem sharded over the "
+                         "ranks with fj_shard_* over NCCL (row f4; strong scaling)")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     return ap.parse_args()
 
@@ -297,6 +300,101 @@ def run_ours(args, prob, world, rank, local):
     return line
 
 
+def run_sharded(args, prob, world, rank, local):
+    """--mode sharded: one config-4 problem split over the ranks (row f4).
+    Each rank transposes the generated in-CSR to the out-CSR on its GPU
+    (torch, plumbing only), keeps its arc-balanced slice resident in HBM, and a
+    step is fj_shard_create + connect + solve + measures + destroy over NCCL."""
+    import torch
+
+    import paper_2507_14864_b200 as fj
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    n = prob.n
+    rp = torch.from_numpy(prob.row_ptr).to(dev)
+    colt = torch.from_numpy(prob.col).to(dev).long()
+    order = torch.sort(colt, stable=True).indices
+    v = torch.repeat_interleave(torch.arange(n, device=dev), torch.diff(rp))
+    ocol = v[order].int()
+    ow = None if prob.w is None else torch.from_numpy(prob.w).to(dev)[order]
+    orp = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    orp[1:] = torch.cumsum(torch.bincount(colt, minlength=n), 0)
+    del colt, order, v, rp
+    begin = fj.shard_plan(orp.cpu().numpy(), world)
+    a, b = begin[rank], begin[rank + 1]
+    k0, k1 = int(orp[a]), int(orp[b])
+    srp = (orp[a:b + 1] - k0).contiguous()
+    scol = ocol[k0:k1].contiguous()
+    sw = None if ow is None else ow[k0:k1].contiguous()
+    del ocol, ow, orp
+    s = torch.from_numpy(prob.s[a:b].copy()).to(dev)
+    z = torch.empty(b - a, dtype=torch.float32, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        box = [fj.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        uid = box[0]
+    else:
+        uid = fj.comm_unique_id()
+    comm = fj.Comm.nccl(uid, rank, world)
+    torch.cuda.synchronize()
+
+    def step():
+        sh = fj.Shard(comm, rank, n, begin, srp, scol, sw, directed=prob.directed)
+        fj.shard_connect([sh])
+        st = fj.shard_solve([sh], [s], [z], args.eps, args.omega)
+        m = fj.shard_measures([sh], [z])
+        sh.close()
+        return st, m
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    launches0 = fj.lib().fj_kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            stats.append(step())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = fj.lib().fj_kernel_launches() - launches0
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world, dev)
+    eu = sum(st.edge_updates for st, _ in stats)  # already summed over the ranks
+    st0, m0 = stats[-1]
+    pk = peaks()
+    peak = pk["hbm_gbs"] if pk else 6650.0
+    per_arc = 8 if prob.w is not None else 4
+    per_row = 28 if prob.w is not None else 20
+    ab = st0.arcs_read * per_arc + st0.rows_read * per_row + 8 * st0.relaxations / world
+    achieved = ab / (st0.sweep_ms / 1e3) / 1e9
+    comm.close()
+    return {"metric": METRIC, "value": eu / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (fjgen seeded R-MAT-24 weights U(0,1], Beta(2,5) opinions)",
+            "config": config_dict(prob, args, {"method": "sharded-async",
+                                               "parallelism": f"shard{world}",
+                                               "begin": [int(x) for x in begin]}),
+            "time_to_eps_s": statistics.median(st.solve_ms for st, _ in stats) / 1e3,
+            "sweep_kernel_ms": statistics.median(st.sweep_ms for st, _ in stats),
+            "step_breakdown": {"sweeps": st0.sweeps, "relaxations": st0.relaxations,
+                               "edge_updates": st0.edge_updates, "cert_ratio": st0.cert_ratio,
+                               "polarization": m0["P"], "disagreement": m0["D"]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_sweep + per-sweep exchange (rank 0's shard)",
+                         "algorithmic_bytes_per_launch": ab},
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+            "e2e": None, "e2e_note": "not measured in --mode sharded"}
+
+
 def run_omega_table(args, prob, fj, torch, rp, col, w, s, z):
     """Time-to-ε per ω of the config's list (BASELINE config 4: SOR ω swept
     over {1.0, 1.2, 1.4, 1.6, 1.8}); outside the timed steps, graph built once,
@@ -366,6 +464,8 @@ def main():
     prob = fjgen.config(args.config, shrink=args.shrink)
     if args.impl == "reference":
         line = run_reference(args, prob, world, rank)
+    elif args.mode == "sharded":
+        line = run_sharded(args, prob, world, rank, local)
     else:
         line = run_ours(args, prob, world, rank, local)
         if rank == 0 and not args.no_cpu:
