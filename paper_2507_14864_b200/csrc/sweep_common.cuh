@@ -78,7 +78,10 @@ struct KP {
 };
 
 // CSR streams are read once per sweep: read-only path, no L1 allocation, so
-// L1 keeps the gathered ẑ values (hub rows are hit by many arcs)
+// L1 keeps the gathered ẑ values (hub rows are hit by many arcs).  The asm is
+// not volatile (so the compiler may batch these loads) — which also lets it
+// speculate them: never guard a call with a condition (`ok ? ld_stream(q) :
+// 0`), clamp the address to a valid slot instead.
 __device__ __forceinline__ int ld_stream(const int *q) {
   int v;
   asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(q));
