@@ -35,25 +35,58 @@ struct PP {
   unsigned *bar;
   SweepCounters *cnt;
   unsigned long long *out;
+  int32_t *front;                 // compacted frontier of the current phase
+  unsigned long long *fcount;     // [3] frontier sizes (ring over phases)
+  int sparse_div;                 // sparse scatter when |frontier|·div < rows of the phase
 };
 
+// pop one row: q_v = ω r_v/(1+d_v) if |r_v| > h_v; returns whether v has a
+// scatter list to walk
+__device__ __forceinline__ bool pop_row(const PP &p, const Scalars &S, int64_t v, TAcc &t,
+                                        double om) {
+  const double sp = (double)p.s[v] + S.c;
+  const double h = threshold(S, sp);
+  const double rv = p.r[v];
+  double qv = 0.0;
+  bool act = false;
+  if (fabs(rv) > p.theta * h) {                       // |r_v| > h_v
+    qv = om * rv / p.d1[v];                           // ω r_v/(1+d_v)
+    p.z[v] += qv;                                     // equ:sor1
+    p.r[v] = rv - om * rv;                            // equ:sor2: (1−ω) r_v
+    t.upd++;
+    t.eu += (unsigned long long)(p.rp[v + 1] - p.rp[v]);
+    act = p.rp[v + 1] > p.rp[v];
+  }
+  if (!(fabs(rv) <= S.sentinel)) t.bad = 1;
+  p.q[v] = qv;
+  return act;
+}
+
+// pop phase over rows [b, e): dense (q_v marks the frontier)
 __device__ __forceinline__ void push_pop(const PP &p, const Scalars &S, int64_t b, int64_t e,
                                          TAcc &t, double om) {
   for (int64_t v = b + blockIdx.x * (int64_t)kBlock + threadIdx.x; v < e;
-       v += (int64_t)gridDim.x * kBlock) {
-    const double sp = (double)p.s[v] + S.c;
-    const double h = threshold(S, sp);
-    const double rv = p.r[v];
-    double qv = 0.0;
-    if (fabs(rv) > p.theta * h) {                       // |r_v| > h_v
-      qv = om * rv / p.d1[v];                           // ω r_v/(1+d_v)
-      p.z[v] += qv;                                     // equ:sor1
-      p.r[v] = rv - om * rv;                            // equ:sor2: (1−ω) r_v
-      t.upd++;
-      t.eu += (unsigned long long)(p.rp[v + 1] - p.rp[v]);
+       v += (int64_t)gridDim.x * kBlock)
+    pop_row(p, S, v, t, om);
+}
+
+// pop phase with frontier compaction: ballot per warp, one atomic per warp
+// with active rows, popcount prefix for the slots
+__device__ __forceinline__ void push_pop_compact(const PP &p, const Scalars &S, int64_t b,
+                                                 int64_t e, TAcc &t, double om,
+                                                 unsigned long long *fcount) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = b + blockIdx.x * (int64_t)kBlock + (threadIdx.x & ~31); base < e;
+       base += (int64_t)gridDim.x * kBlock) {
+    const int64_t v = base + lane;
+    const bool act = v < e && pop_row(p, S, v, t, om);
+    const unsigned m = __ballot_sync(0xffffffffu, act);
+    if (m) {
+      unsigned long long off = 0;
+      if (lane == 0) off = atomicAdd(fcount, (unsigned long long)__popc(m));
+      off = __shfl_sync(0xffffffffu, off, 0);
+      if (act) p.front[off + __popc(m & ((1u << lane) - 1u))] = (int32_t)v;
     }
-    if (!(fabs(rv) <= S.sentinel)) t.bad = 1;
-    p.q[v] = qv;
   }
 }
 
@@ -67,22 +100,56 @@ __device__ __forceinline__ void push_scatter_arcs(const PP &p, int64_t k0, int64
   }
 }
 
+// scatter of a compacted frontier: warp per active row
 template <bool W>
+__device__ __forceinline__ void scatter_sparse(const PP &p, long long F) {
+  const int lane = threadIdx.x & 31;
+  const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+  for (long long fi = warp_id; fi < F; fi += (long long)gridDim.x * (kBlock / 32)) {
+    const int v = p.front[fi];
+    push_scatter_arcs<W>(p, p.rp[v] + lane, p.rp[v + 1], 32, p.q[v]);
+  }
+}
+
+// CF: frontier compaction (FJ_PUSH_COMPACT=1).  Measured slower than the
+// dense frontier (q_v ≠ 0 marks) on C2/C4/C5 (DESIGN.md §8 tuning log), so
+// the default instantiation keeps the dense loop only.
+template <bool W, bool CF>
 __global__ void __launch_bounds__(kBlock, 4) k_push(PP p) {
   __shared__ unsigned long long s_dec[3];
   const Scalars S = *p.sc;
   TAcc t{};
   unsigned long long tot_upd = 0, tot_eu = 0;
-  int sweeps = 0, reason = 1;
+  int sweeps = 0, reason = 1, phase = 0;
+  unsigned long long last_upd = (unsigned long long)p.n;  // relaxations of the last sweep
   const int lane = threadIdx.x & 31;
   const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
-    for (int k = 0; k < p.ncolors; ++k) {
+    for (int k = 0; k < p.ncolors; ++k, ++phase) {
       const double om = k == p.tail_phase ? 1.0 : p.omega;
-      push_pop(p, S, p.crow[k], p.crow[k + 1], t, om);
-      if (k == p.ncolors - 1) push_pop(p, S, p.crow[p.ncolors], p.n, t, om);  // rows with no in-arcs
+      unsigned long long *fc = p.fcount + phase % 3;
+      if (CF && blockIdx.x == 0 && threadIdx.x == 0) p.fcount[(phase + 1) % 3] = 0ull;  // next
+      // compact only when the last sweep relaxed few rows: early sweeps relax
+      // most rows, and there the dense task walk needs no atomics at all
+      const long long rows = (long long)(p.crow[k + 1] - p.crow[k]);
+      const bool compact = CF && (long long)last_upd * p.sparse_div < (long long)p.n;
+      if (CF && compact) {
+        push_pop_compact(p, S, p.crow[k], p.crow[k + 1], t, om, fc);
+        if (k == p.ncolors - 1) push_pop_compact(p, S, p.crow[p.ncolors], p.n, t, om, fc);
+      } else {
+        push_pop(p, S, p.crow[k], p.crow[k + 1], t, om);
+        if (k == p.ncolors - 1) push_pop(p, S, p.crow[p.ncolors], p.n, t, om);  // no in-arcs
+      }
       grid_sync(p.bar);
-      // B: warp units (long scatter lists), then tile tasks (group per row)
+      // B: scatter.  A small frontier is walked as the compacted list (warp
+      // per active row); a large one by the layout's tasks (q = 0 rows skip)
+      const long long F = compact ? (long long)__ldcg(fc) : rows;
+      if (CF && compact && F * p.sparse_div < rows) {
+        scatter_sparse<W>(p, F);
+        grid_sync(p.bar);
+        continue;
+      }
+      // dense: warp units (long scatter lists), then tile tasks (group per row)
       const int w0 = p.wphase_begin[k], nw = p.wphase_begin[k + 1] - w0;
       for (int wi = warp_id; wi < nw; wi += gridDim.x * (kBlock / 32)) {
         const Task tk = p.wtasks[w0 + wi];
@@ -130,6 +197,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_push(PP p) {
     __syncthreads();
     tot_upd += s_dec[0];
     tot_eu += s_dec[1];
+    last_upd = s_dec[0];
     sweeps = sw + 1;
     const bool bad = s_dec[2] != 0, done = s_dec[0] == 0;
     __syncthreads();
@@ -262,6 +330,11 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   pp.bar = ctl + 8;
   pp.cnt = cnt;
   pp.out = outv;
+  int32_t *front = nullptr;
+  FJ_CUDA(cudaMallocAsync(&front, sizeof(int32_t) * n, st));
+  pp.front = front;
+  pp.fcount = reinterpret_cast<unsigned long long *>(ctl + 16);  // zeroed with ctl
+  pp.sparse_div = getenv("FJ_PUSH_SPARSE_DIV") ? atoi(getenv("FJ_PUSH_SPARSE_DIV")) : 8;
   KP kq = make_kp(g, L);
   kq.s = sL;
   kq.z = zL;
@@ -277,7 +350,9 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   kq.partial = partial;
   kq.arrive = arrive;
 
-  const void *fn = W ? (const void *)k_push<true> : (const void *)k_push<false>;
+  const bool compact = getenv("FJ_PUSH_COMPACT") && atoi(getenv("FJ_PUSH_COMPACT"));
+  const void *fn = W ? (compact ? (const void *)k_push<true, true> : (const void *)k_push<true, false>)
+                     : (compact ? (const void *)k_push<false, true> : (const void *)k_push<false, false>);
   const int grid = persistent_grid(fn, g->num_sms);
   const void *cf = W ? (const void *)k_pass<CERT, true> : (const void *)k_pass<CERT, false>;
   float ms_sweep = 0;
@@ -344,7 +419,7 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   for (void *q : {(void *)sP, (void *)sL, (void *)zP, (void *)rP, (void *)qP, (void *)zL,
                   (void *)tmp, (void *)RL, (void *)smin, (void *)S, (void *)ctl, (void *)cnt,
                   (void *)outv, (void *)zo, (void *)zp, (void *)s.owned, (void *)partial,
-                  (void *)arrive})
+                  (void *)arrive, (void *)front})
     if (q) cudaFreeAsync(q, st);
   for (cudaEvent_t e : {e0, e1, es0, es1}) cudaEventDestroy(e);
   FJ_CUDA(cudaGetLastError());

@@ -346,6 +346,17 @@ def test_tiny_push(dev, name):
     assert st.relaxations > 0 and st.edge_updates > 0
 
 
+@pytest.mark.parametrize("name", ["rmat12w", "chunglu4k", "lattice64"])
+@pytest.mark.parametrize("div", ["1", "64"])
+def test_tiny_push_compacted_frontier(dev, monkeypatch, name, div):
+    """PUSH with frontier compaction (ballot + per-warp atomic slots) and the
+    sparse warp-per-row scatter of the compacted list."""
+    monkeypatch.setenv("FJ_PUSH_COMPACT", "1")
+    monkeypatch.setenv("FJ_PUSH_SPARSE_DIV", div)
+    rp, col, w, s, directed = TINY[name]()
+    check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="push")
+
+
 @pytest.mark.parametrize("name", ["er2000", "lattice64", "chunglu4k"])
 def test_tiny_push_sor_colored(dev, name):
     """FJ_METHOD_PUSH with ω ≠ 1: Alg. 3 per color (pushes of one color commute)."""
