@@ -270,6 +270,18 @@ def run_ours(args, prob, world, rank, local):
         except Exception:
             traffic = None
 
+    # practical roofline: the sweep's memory pattern without its arithmetic
+    # (fj_gather_probe: stream every arc, gather one fp64 per arc), timed live
+    g = fj.Graph(prob.n, rp, col, w, directed=prob.directed)
+    probe_ms = fj.gather_probe(g, 10)
+    g.close()
+    sweep_per = st0.sweep_ms / max(st0.sweeps, 1)
+    ceiling = {"probe_ms_per_pass": probe_ms, "sweep_ms_per_sweep": sweep_per,
+               "frac": probe_ms / sweep_per,
+               "note": "fj_gather_probe over the same layout: every arc's col+w streamed and "
+                       "one fp64 gathered per arc; frac = probe / sweep time (1 = at the gather "
+                       "ceiling)"}
+
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, prob, fj, torch, dev, stream, world)
@@ -293,6 +305,7 @@ def run_ours(args, prob, world, rank, local):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
                          "kernel": "k_sweep (persistent)",
                          "algorithmic_bytes_per_launch": ab},
+            "gather_ceiling": ceiling,
             "omega_sweep": omega_table,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -286,6 +286,16 @@ fj_status fj_shard_measures(fj_shard_t *shards, int count, const float *const *z
 /* Free a shard (NULL is a no-op). */
 fj_status fj_shard_destroy(fj_shard_t s);
 
+/*
+ * Practical roofline of a sweep (diagnostics): one pass over g's
+ * sweep layout that streams every arc's column (and weight) and gathers one
+ * fp64 value per arc at the column's index — the memory pattern of a sweep
+ * without its row structure or arithmetic.  Writes the mean device time of
+ * `reps` ≥ 1 passes (CUDA events on g's stream, after one warm-up pass) to
+ * *ms_per_pass.  Touches no solver state.
+ */
+fj_status fj_gather_probe(fj_graph_t g, int reps, double *ms_per_pass);
+
 /* Thread-local message for the last non-OK status of this thread. */
 const char *fj_last_error(void);
 

@@ -27,7 +27,7 @@ EXPORTS = ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve
            "fj_abi_version", "fj_kernel_launches", "fj_omega_opt", "fj_omega_sweep",
            "fj_solve_batch", "fj_shard_plan", "fj_comm_unique_id", "fj_comm_create",
            "fj_comm_create_local", "fj_comm_destroy", "fj_shard_create", "fj_shard_connect",
-           "fj_shard_solve", "fj_shard_measures", "fj_shard_destroy")
+           "fj_shard_solve", "fj_shard_measures", "fj_shard_destroy", "fj_gather_probe")
 
 
 class FJError(RuntimeError):
@@ -102,12 +102,13 @@ def lib():
                                      ctypes.POINTER(_Stats)]
         L.fj_shard_measures.argtypes = [PP, i, PP, PP, ctypes.POINTER(_Measures)]
         L.fj_shard_destroy.argtypes = [P]
+        L.fj_gather_probe.argtypes = [P, i, ctypes.POINTER(d)]
         for f in ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve",
                   "fj_solve_ex", "fj_measures", "fj_measures_ex", "fj_omega_opt",
                   "fj_omega_sweep", "fj_solve_batch", "fj_shard_plan", "fj_comm_unique_id",
                   "fj_comm_create", "fj_comm_create_local", "fj_comm_destroy",
                   "fj_shard_create", "fj_shard_connect", "fj_shard_solve",
-                  "fj_shard_measures", "fj_shard_destroy"):
+                  "fj_shard_measures", "fj_shard_destroy", "fj_gather_probe"):
             getattr(L, f).restype = i
         _LIB = L
     return _LIB
@@ -273,6 +274,14 @@ def measures_pd(g: Graph, z):
     P, D = ctypes.c_double(), ctypes.c_double()
     _check(lib().fj_measures(g._h, _ptr(z), ctypes.byref(P), ctypes.byref(D)))
     return P.value, D.value
+
+
+def gather_probe(g: Graph, reps: int = 10) -> float:
+    """fj_gather_probe: ms per pass of the sweep's memory pattern (stream every
+    arc, gather one fp64 per arc) — the practical ceiling of a sweep."""
+    ms = ctypes.c_double()
+    _check(lib().fj_gather_probe(g._h, int(reps), ctypes.byref(ms)))
+    return ms.value
 
 
 def omega_opt(g: Graph, max_iters: int = 2000, tol: float = 1e-9):

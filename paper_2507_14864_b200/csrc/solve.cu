@@ -740,6 +740,71 @@ fj_status measures_impl(fj_graph *g, const float *z_in, const float *s_in, fj_me
 }
 
 
+// ------------------------------------------------- practical roofline probe
+// Σ_k w_k · x[col_k] over the layout's arc stream, 8 arcs per thread in
+// flight, grid-stride; the sum only keeps the loads alive
+template <bool W>
+__global__ void __launch_bounds__(kBlock) k_gather_probe(int64_t m, const int32_t *__restrict__ col,
+                                                         const float *__restrict__ w,
+                                                         const double *__restrict__ x,
+                                                         double *__restrict__ sink) {
+  constexpr int U = 8;
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k0 < m; k0 += stride * U) {
+    int j[U];
+    float wv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t k = k0 + u * stride;
+      const bool ok = k < m;
+      j[u] = ld_stream(col + (ok ? k : 0));
+      wv[u] = ok ? (W ? ld_stream(w + (ok ? k : 0)) : 1.0f) : 0.0f;
+    }
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) v[u] = ld_z(x + j[u]);
+#pragma unroll
+    for (int u = 0; u < U; u++) acc = fma((double)wv[u], v[u], acc);
+  }
+  if (acc == 1.2345e300) *sink = acc;
+}
+
+fj_status gather_probe_impl(fj_graph *g, int reps, double *ms_per_pass) {
+  cudaStream_t st = g->stream;
+  const Layout &L = g->async_layout;
+  double *x = nullptr;
+  FJ_CUDA(cudaMallocAsync(&x, sizeof(double) * (g->n + 1), st));
+  FJ_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (g->n + 1), st));
+  const void *fn = L.w ? (const void *)k_gather_probe<true> : (const void *)k_gather_probe<false>;
+  const int grid = persistent_grid(fn, g->num_sms);
+  int64_t m = L.m;
+  const int32_t *col = L.col;
+  const float *w = L.w;
+  double *sink = x + g->n;
+  void *args[] = {&m, &col, &w, &x, &sink};
+  cudaEvent_t a, b;
+  FJ_CUDA(cudaEventCreate(&a));
+  FJ_CUDA(cudaEventCreate(&b));
+  fj::count_launch();
+  FJ_CUDA(cudaLaunchKernel(fn, grid, kBlock, args, 0, st));  // warm-up
+  FJ_CUDA(cudaEventRecord(a, st));
+  for (int r = 0; r < reps; r++) {
+    fj::count_launch();
+    FJ_CUDA(cudaLaunchKernel(fn, grid, kBlock, args, 0, st));
+  }
+  FJ_CUDA(cudaEventRecord(b, st));
+  FJ_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  FJ_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFreeAsync(x, st);
+  FJ_CUDA(cudaStreamSynchronize(st));
+  *ms_per_pass = ms / reps;
+  return FJ_OK;
+}
+
 // ------------------------------------------------------------- ω selection
 // y_i ← ((J x)_i + x_i)/2 with J = (I+D)^{-1} A; Σ y², Σ x·y
 __global__ void k_jacobi_scale(int64_t n, const int64_t *__restrict__ rp, const double *__restrict__ d1,
@@ -859,6 +924,14 @@ fj_status fj_solve_ex(fj_graph_t g, const float *s, double eps, double omega, co
     return FJ_ERR_INVALID;
   }
   return fj::solve_impl(g, s, eps, omega, &d, z_out, st);
+}
+
+fj_status fj_gather_probe(fj_graph_t g, int reps, double *ms_per_pass) {
+  if (!g || reps < 1 || !ms_per_pass) {
+    fj::set_error("fj_gather_probe: need g, reps >= 1, ms_per_pass");
+    return FJ_ERR_INVALID;
+  }
+  return fj::gather_probe_impl(g, reps, ms_per_pass);
 }
 
 fj_status fj_omega_opt(fj_graph_t g, int max_iters, double tol, double *mu, double *omega) {

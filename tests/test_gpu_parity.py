@@ -249,6 +249,17 @@ def test_tail_merge_complete_graph(dev, monkeypatch, omega):
     g.close()
 
 
+def test_gather_probe(dev):
+    """fj_gather_probe runs on the layout and reports a positive time."""
+    rp, col, w, s, directed = TINY["rmat12w"]()
+    g = fj.Graph(len(rp) - 1, rp, col, w, directed=directed)
+    ms = fj.gather_probe(g, 3)
+    assert 0.0 < ms < 100.0
+    with pytest.raises(fj.FJError):
+        fj.gather_probe(g, 0)
+    g.close()
+
+
 def test_invalid_inputs(dev):
     def create(n, arcs, w=None, directed=True, rp=None, col=None):
         if rp is None:
