@@ -113,6 +113,10 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # torchrun pins OMP_NUM_THREADS=1; the input generator (OpenMP, runs
+        # before the timed region) gets an even share of the host cores instead
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // world))
+    if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     return world, rank, local
