@@ -8,8 +8,10 @@ fj_graph_create (a1) → fj_solve_ex (a2–a6) → fj_measures (a7) → destroy.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--omega 1.0] [--impl reference]
 
-N > 1 (torchrun): independent replicas, one per GPU ("replicas only", the
-path has no exchange step).  Rank 0 prints one JSON line.
+N > 1 (torchrun): independent replicas, one per GPU (the default; one C4 solve
+fits one B200), or with --mode sharded ONE problem split over the
+ranks by fj_shard_* over NCCL (row f4, strong scaling).  Rank 0 prints one
+JSON line.
 """
 from __future__ import annotations
 
