@@ -283,6 +283,11 @@ fj_status fj_shard_solve(fj_shard_t *shards, int count, const float *const *s, d
 fj_status fj_shard_measures(fj_shard_t *shards, int count, const float *const *z,
                             const float *const *s, fj_measures_t *out);
 
+/* Rows owned by s and, after fj_shard_connect, its halo: the number of
+   distinct remote nodes its rows read, i.e. the fp64 values it receives per
+   sweep (0 before connect).  Host outputs. */
+fj_status fj_shard_info(fj_shard_t s, int64_t *n_local, int64_t *halo);
+
 /* Free a shard (NULL is a no-op). */
 fj_status fj_shard_destroy(fj_shard_t s);
 

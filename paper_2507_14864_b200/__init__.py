@@ -27,7 +27,7 @@ EXPORTS = ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve
            "fj_abi_version", "fj_kernel_launches", "fj_omega_opt", "fj_omega_sweep",
            "fj_solve_batch", "fj_shard_plan", "fj_comm_unique_id", "fj_comm_create",
            "fj_comm_create_local", "fj_comm_destroy", "fj_shard_create", "fj_shard_connect",
-           "fj_shard_solve", "fj_shard_measures", "fj_shard_destroy", "fj_gather_probe")
+           "fj_shard_solve", "fj_shard_measures", "fj_shard_destroy", "fj_shard_info", "fj_gather_probe")
 
 
 class FJError(RuntimeError):
@@ -103,12 +103,13 @@ def lib():
         L.fj_shard_measures.argtypes = [PP, i, PP, PP, ctypes.POINTER(_Measures)]
         L.fj_shard_destroy.argtypes = [P]
         L.fj_gather_probe.argtypes = [P, i, ctypes.POINTER(d)]
+        L.fj_shard_info.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         for f in ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve",
                   "fj_solve_ex", "fj_measures", "fj_measures_ex", "fj_omega_opt",
                   "fj_omega_sweep", "fj_solve_batch", "fj_shard_plan", "fj_comm_unique_id",
                   "fj_comm_create", "fj_comm_create_local", "fj_comm_destroy",
                   "fj_shard_create", "fj_shard_connect", "fj_shard_solve",
-                  "fj_shard_measures", "fj_shard_destroy", "fj_gather_probe"):
+                  "fj_shard_measures", "fj_shard_destroy", "fj_gather_probe", "fj_shard_info"):
             getattr(L, f).restype = i
         _LIB = L
     return _LIB
@@ -374,6 +375,13 @@ class Shard:
                                      ctypes.byref(self._h)))
         self.comm, self.rank, self.n = comm, int(rank), int(n)
         self.n_local = int(self._b[rank + 1] - self._b[rank])
+
+    def info(self):
+        """(n_local, halo): owned rows and, after connect, the remote values
+        received per sweep."""
+        nl, h = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().fj_shard_info(self._h, ctypes.byref(nl), ctypes.byref(h)))
+        return nl.value, h.value
 
     def close(self):
         if self._h:

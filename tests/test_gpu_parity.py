@@ -470,16 +470,18 @@ def test_gpu_lemma4_one_sided(dev, name):
 
 
 # ------------------------------------------------ the C-ABI from plain C
-def test_c_program_against_abi(dev, tmp_path):
-    """examples/fj_example.c links libfj.so directly (no Python marshalling)
-    and checks the P2 worked example (tab:measures)."""
+@pytest.mark.parametrize("prog", ["fj_example", "fj_shard_example"])
+def test_c_program_against_abi(dev, tmp_path, prog):
+    """examples/*.c link libfj.so directly (no Python marshalling): the P2
+    worked example (tab:measures) and a two-shard path against the
+    tridiagonal closed form."""
     import os
     import subprocess
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     libdir = os.path.join(root, "paper_2507_14864_b200")
-    exe = str(tmp_path / "fj_example")
+    exe = str(tmp_path / prog)
     subprocess.check_call(["gcc", "-O2", "-I", os.path.join(root, "include"),
-                           os.path.join(root, "examples", "fj_example.c"), "-L", libdir, "-l:libfj.so",
+                           os.path.join(root, "examples", prog + ".c"), "-L", libdir, "-l:libfj.so",
                            f"-Wl,-rpath,{libdir}", "-lm", "-o", exe])
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr

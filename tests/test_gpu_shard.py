@@ -85,6 +85,28 @@ def test_shard_parity(dev, name, W):
         assert abs(m[k] - om[k]) <= 1e-9 * abs(om[k]) + 1e-300, (k, m[k], om[k])
 
 
+@pytest.mark.parametrize("name", ["lattice64", "rmat12w", "er2000"])
+def test_shard_halo_exact(dev, name):
+    """Each shard receives exactly the distinct remote nodes its rows read."""
+    rp, col, w, s, directed = TINY[name]()
+    n = len(rp) - 1
+    orp, ocol, ow = fjgen.to_out_csr(rp, col, w)
+    begin = np.array(fj.shard_plan(orp, 4))
+    comm = fj.Comm.in_process(4)
+    shards = make_shards(comm, rp, col, w, directed, begin, True, dev)
+    assert all(sh.info()[1] == 0 for sh in shards)
+    fj.shard_connect(shards)
+    for r, sh in enumerate(shards):
+        c = ocol[orp[begin[r]]:orp[begin[r + 1]]]
+        remote = np.unique(c[(c < begin[r]) | (c >= begin[r + 1])])
+        assert sh.info() == (int(begin[r + 1] - begin[r]), len(remote))
+    if name == "lattice64":  # a grid split into row bands: the halo is the band edges
+        assert sum(sh.info()[1] for sh in shards) < 0.15 * n
+    for sh in shards:
+        sh.close()
+    comm.close()
+
+
 def test_shard_host_pointers(dev):
     rp, col, w, s, directed = TINY["rmat12w"]()
     st, z, zp, m = sharded_solve(dev, rp, col, w, s, 1e-6, 1.0, directed, 3, on_device=False)

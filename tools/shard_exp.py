@@ -46,6 +46,7 @@ for cid in [int(a) for a in sys.argv[1:]]:
         fj.shard_connect(shards)
         torch.cuda.synchronize()
         tb = time.time() - t0
+        halo = sum(sh.info()[1] for sh in shards) / W
         sl = [s[begin[r]:begin[r + 1]].contiguous() for r in range(W)]
         zl = [torch.empty(begin[r + 1] - begin[r], dtype=torch.float32, device=dev)
               for r in range(W)]
@@ -55,7 +56,8 @@ for cid in [int(a) for a in sys.argv[1:]]:
             bs = st if bs is None or st.solve_ms < bs.solve_ms else bs
         zs = torch.cat(zl).cpu().numpy()
         dz = float(np.max(np.abs(zs - z1) / np.maximum(np.abs(z1), 1e-5)))
-        print(f"  W={W}: build {tb * 1e3:.0f} ms, sweeps {bs.sweeps}, solve {bs.solve_ms:.1f} ms, "
+        print(f"  W={W}: build {tb * 1e3:.0f} ms, halo/rank {halo / p.n:.3f}·n, sweeps {bs.sweeps}, "
+              f"solve {bs.solve_ms:.1f} ms, "
               f"sweep kernels {bs.sweep_ms:.1f} ms ({bs.sweep_ms / bs.sweeps:.3f} ms/sweep), "
               f"cert {bs.cert_ratio:.3f}, max rel dz vs single {dz:.1e}", flush=True)
         for sh in shards:
