@@ -25,6 +25,11 @@
  * All device work is ordered on the graph's stream; every call returns after
  * that work has completed (it synchronises the stream).
  *
+ * Threads: different graph handles may be used from different threads at
+ * once (each owns its stream and workspace).  One handle must not be used by
+ * two threads at the same time: a COLORED or PUSH solve builds its layout
+ * lazily inside the handle.
+ *
  * Errors: every call returns an fj_status; on a non-OK status
  * fj_last_error() returns a thread-local message.  Status classes follow the
  * SPEC exit codes: 2 invalid input, 3 numeric (watchdog/divergence),
