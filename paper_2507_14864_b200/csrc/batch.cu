@@ -295,16 +295,14 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
   const bool W = g->weighted != 0;
   fj_stats stats{};
   stats.colors = 1;
+  Workspace ws(st);
   cudaEvent_t e0, e1, es0, es1;
-  FJ_CUDA(cudaEventCreate(&e0));
-  FJ_CUDA(cudaEventCreate(&e1));
-  FJ_CUDA(cudaEventCreate(&es0));
-  FJ_CUDA(cudaEventCreate(&es1));
+  for (cudaEvent_t *e : {&e0, &e1, &es0, &es1}) FJ_CUDA(ws.event(e));
   FJ_CUDA(cudaEventRecord(e0, st));
   const float *S = S_in;
   float *S_owned = nullptr;
   if (!is_device_ptr(S_in)) {
-    FJ_CUDA(cudaMallocAsync(&S_owned, sizeof(float) * n * k, st));
+    FJ_CUDA(ws.alloc(&S_owned, n * k));
     FJ_CUDA(cudaMemcpyAsync(S_owned, S_in, sizeof(float) * n * k, cudaMemcpyHostToDevice, st));
     S = S_owned;
   }
@@ -318,29 +316,29 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
   unsigned *ctl = nullptr, *ctlb = nullptr;
   SweepCounters *cnt = nullptr;
   const size_t np = (size_t)std::max(1, L.npartials);
-  FJ_CUDA(cudaMallocAsync(&sK, sizeof(float) * n * K, st));
-  FJ_CUDA(cudaMallocAsync(&zK, sizeof(double) * n * K, st));
-  FJ_CUDA(cudaMallocAsync(&col, sizeof(float) * n, st));
-  FJ_CUDA(cudaMallocAsync(&mm, sizeof(float) * 2, st));
-  FJ_CUDA(cudaMallocAsync(&s1, sizeof(float) * n, st));
-  FJ_CUDA(cudaMallocAsync(&z1, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&partial, sizeof(double2) * np * K, st));
-  FJ_CUDA(cudaMallocAsync(&arrive, sizeof(int) * np, st));
-  FJ_CUDA(cudaMallocAsync(&arrive2, sizeof(int) * np, st));
+  FJ_CUDA(ws.alloc(&sK, n * K));
+  FJ_CUDA(ws.alloc(&zK, n * K));
+  FJ_CUDA(ws.alloc(&col, n));
+  FJ_CUDA(ws.alloc(&mm, 2));
+  FJ_CUDA(ws.alloc(&s1, n));
+  FJ_CUDA(ws.alloc(&z1, n));
+  FJ_CUDA(ws.alloc(&partial, np * K));
+  FJ_CUDA(ws.alloc(&arrive, np));
+  FJ_CUDA(ws.alloc(&arrive2, np));
   FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * np, st));
-  FJ_CUDA(cudaMallocAsync(&SK, sizeof(Scalars) * K, st));
-  FJ_CUDA(cudaMallocAsync(&outv, sizeof(unsigned long long) * 8, st));
-  FJ_CUDA(cudaMallocAsync(&ctl, sizeof(unsigned) * 8, st));
-  FJ_CUDA(cudaMallocAsync(&ctlb, sizeof(unsigned) * kCtlWords, st));
-  FJ_CUDA(cudaMallocAsync(&cnt, sizeof(SweepCounters) * 3, st));
-  if (!zdev) FJ_CUDA(cudaMallocAsync(&Zd, sizeof(float) * n * k, st));
+  FJ_CUDA(ws.alloc(&SK, K));
+  FJ_CUDA(ws.alloc(&outv, 8));
+  FJ_CUDA(ws.alloc(&ctl, 8));
+  FJ_CUDA(ws.alloc(&ctlb, kCtlWords));
+  FJ_CUDA(ws.alloc(&cnt, 3));
+  if (!zdev) FJ_CUDA(ws.alloc(&Zd, n * k));
   // a2 per right-hand side: shift and thresholds (Alg. 2, reading R5)
   {
     size_t t1 = 0, t2 = 0;
     FJ_CUDA(cub::DeviceReduce::Min(nullptr, t1, col, mm, n, st));
     FJ_CUDA(cub::DeviceReduce::Max(nullptr, t2, col, mm + 1, n, st));
-    void *t = nullptr;
-    FJ_CUDA(cudaMallocAsync(&t, std::max(t1, t2), st));
+    unsigned char *t = nullptr;
+    FJ_CUDA(ws.alloc(&t, std::max(t1, t2)));
     for (int r = 0; r < K; r++) {
       fj::count_launch();
       k_column<<<gridn(n), kBlock, 0, st>>>(n, k, r < k ? r : k - 1, S, col);
@@ -349,7 +347,6 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
       fj::count_launch();
       k_scalars<<<1, 1, 0, st>>>(mm, mm + 1, eps, o->sigma, o->c, SK + r);
     }
-    FJ_CUDA(cudaFreeAsync(t, st));
   }
   fj::count_launch();
   k_init_batch<<<gridn(n), kBlock, 0, st>>>(n, k, K, L.perm, L.rp, S, SK, sK, zK);
@@ -442,12 +439,6 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
   stats.sweep_ms = ms_sweep;
   stats.c = hs.c;
   stats.eps_prime = hs.eps_p;
-  for (void *q : {(void *)sK, (void *)zK, (void *)col, (void *)mm, (void *)s1, (void *)z1,
-                  (void *)partial, (void *)arrive, (void *)arrive2, (void *)SK,
-                  (void *)outv, (void *)ctl, (void *)ctlb, (void *)cnt, (void *)Zd,
-                  (void *)S_owned})
-    if (q) cudaFreeAsync(q, st);
-  for (cudaEvent_t e : {e0, e1, es0, es1}) cudaEventDestroy(e);
   FJ_CUDA(cudaGetLastError());
   fj_status rc = finish_status(hs, stats, o, omega);
   if (st_out) *st_out = stats;

@@ -114,8 +114,9 @@ static fj_status merge_tail_colors(fj_graph *g) {
   double frac = 0.01;
   if (const char *e = getenv("FJ_TAIL_FRAC")) frac = atof(e);
   if (!(frac > 0.0) || nc <= 2 || nc > 6000) return FJ_OK;
+  Workspace ws(st);
   unsigned long long *cnt = nullptr;
-  FJ_CUDA(cudaMallocAsync(&cnt, sizeof(unsigned long long) * nc, st));
+  FJ_CUDA(ws.alloc(&cnt, (size_t)nc));
   FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * nc, st));
   fj::count_launch();
   k_color_hist<<<std::max(1, std::min(g->num_sms * 4, (int)((g->n + kBlock - 1) / kBlock))), kBlock,
@@ -123,7 +124,6 @@ static fj_status merge_tail_colors(fj_graph *g) {
   std::vector<unsigned long long> h(nc);
   FJ_CUDA(cudaMemcpyAsync(h.data(), cnt, sizeof(unsigned long long) * nc, cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
-  cudaFreeAsync(cnt, st);
   const double cap = frac * (double)g->n;
   int K = nc;
   double tail = 0.0;
@@ -180,17 +180,18 @@ fj_status tail_bounds(fj_graph *g, Layout *L) {
 fj_status build_coloring(fj_graph *g) {
   cudaStream_t st = g->stream;
   const int64_t n = g->n;
+  Workspace ws(st);  // the pull CSR and the round buffers; the colors go to g
   int64_t *ort = nullptr;
   int32_t *ocol = nullptr;
   float *ow = nullptr;
-  FJ_TRY(transpose_in_csr(g, &ort, &ocol, &ow));
+  FJ_TRY(transpose_in_csr(g, ws, &ort, &ocol, &ow));
   int32_t *c0 = nullptr, *c1 = nullptr;
   unsigned long long *rem = nullptr;
   int *maxc = nullptr;
-  FJ_CUDA(cudaMallocAsync(&c0, sizeof(int32_t) * n, st));
-  FJ_CUDA(cudaMallocAsync(&c1, sizeof(int32_t) * n, st));
-  FJ_CUDA(cudaMallocAsync(&rem, sizeof(unsigned long long), st));
-  FJ_CUDA(cudaMallocAsync(&maxc, sizeof(int), st));
+  FJ_CUDA(ws.alloc(&c0, (size_t)n));
+  FJ_CUDA(ws.alloc(&c1, (size_t)n));
+  FJ_CUDA(ws.alloc(&rem, 1));
+  FJ_CUDA(ws.alloc(&maxc, 1));
   FJ_CUDA(cudaMemsetAsync(c0, 0xff, sizeof(int32_t) * n, st));
   FJ_CUDA(cudaMemsetAsync(c1, 0xff, sizeof(int32_t) * n, st));
   FJ_CUDA(cudaMemsetAsync(maxc, 0, sizeof(int), st));
@@ -213,17 +214,12 @@ fj_status build_coloring(fj_graph *g) {
   int hmax = 0;
   FJ_CUDA(cudaMemcpyAsync(&hmax, maxc, sizeof(int), cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
+  ws.keep(c0);
   g->ncolors = hmax + 1;
   g->colors = c0;
-  cudaFreeAsync(c1, st);
-  cudaFreeAsync(rem, st);
-  cudaFreeAsync(maxc, st);
   FJ_TRY(merge_tail_colors(g));
   fj_status s = build_layout_from_out(g, ort, ocol, ow, g->colors, g->ncolors, &g->color_layout);
   if (s == FJ_OK) s = tail_bounds(g, &g->color_layout);
-  cudaFreeAsync(ort, st);
-  cudaFreeAsync(ocol, st);
-  if (ow) cudaFreeAsync(ow, st);
   FJ_CUDA(cudaStreamSynchronize(st));
   return s;
 }

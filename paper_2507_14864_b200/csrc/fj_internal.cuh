@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -124,8 +125,43 @@ struct fj_graph {
 };
 
 namespace fj {
+// Stream-ordered workspace of one call: every buffer and event it hands out is
+// released when it goes out of scope, on the normal path and on every early
+// error return (an allocation failure half-way through a solve leaks nothing).
+struct Workspace {
+  cudaStream_t st;
+  std::vector<void *> bufs;
+  std::vector<cudaEvent_t> evs;
+  explicit Workspace(cudaStream_t s) : st(s) {}
+  Workspace(const Workspace &) = delete;
+  Workspace &operator=(const Workspace &) = delete;
+  ~Workspace() {
+    for (void *q : bufs)
+      if (q) cudaFreeAsync(q, st);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  }
+  template <class T>
+  cudaError_t alloc(T **q, size_t count) {
+    *q = nullptr;
+    const cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(q),
+                                          sizeof(T) * std::max<size_t>(count, 1), st);
+    if (e == cudaSuccess) bufs.push_back(*q);
+    return e;
+  }
+  // hand a buffer over to a longer-lived owner (it is no longer freed here)
+  void keep(const void *q) {
+    for (auto &b : bufs)
+      if (b == q) b = nullptr;
+  }
+  cudaError_t event(cudaEvent_t *e) {
+    const cudaError_t r = cudaEventCreate(e);
+    if (r == cudaSuccess) evs.push_back(*e);
+    return r;
+  }
+};
+
 // graph.cu
-fj_status transpose_in_csr(fj_graph *g, int64_t **ort, int32_t **ocol, float **ow);
+fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **ocol, float **ow);
 // layout.cu: sweep layout from the pull CSR (original ids)
 fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *ocol,
                                 const float *ow, const int32_t *color /* nullable */,

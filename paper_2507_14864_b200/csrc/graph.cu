@@ -178,16 +178,16 @@ static unsigned grid_warps(int64_t rows) {  // warp-per-row kernels: grid-stride
 
 template <class K, class V>
 static fj_status sort_pairs(K *&keys, K *&keys_alt, V *&val, V *&val_alt, int64_t m, int nbits,
-                            cudaStream_t st) {
+                            Workspace &ws) {
   if (m == 0) return FJ_OK;
+  cudaStream_t st = ws.st;
   cub::DoubleBuffer<K> dk(keys, keys_alt);
   cub::DoubleBuffer<V> dv(val, val_alt);
   size_t tmp = 0;
   FJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, m, 0, nbits, st));
-  void *t = nullptr;
-  FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+  unsigned char *t = nullptr;
+  FJ_CUDA(ws.alloc(&t, tmp));
   FJ_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, m, 0, nbits, st));
-  FJ_CUDA(cudaFreeAsync(t, st));
   if (dk.Current() != keys) std::swap(keys, keys_alt);
   if (dv.Current() != val) std::swap(val, val_alt);
   return FJ_OK;
@@ -195,34 +195,30 @@ static fj_status sort_pairs(K *&keys, K *&keys_alt, V *&val, V *&val_alt, int64_
 
 // Transpose the canonical in-CSR into the pull CSR (row u lists v with a_uv),
 // rows sorted: a stable radix sort on u alone keeps the v order of the
-// canonical input.  Caller frees *ort, *ocol, *ow (cudaFreeAsync on g->stream).
-fj_status transpose_in_csr(fj_graph *g, int64_t **ort, int32_t **ocol, float **ow) {
+// canonical input.  *ort, *ocol, *ow live in the caller's workspace `ws`.
+fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **ocol, float **ow) {
   cudaStream_t st = g->stream;
   const int64_t n = g->n, m = g->m;
+  Workspace tmp(st);  // sort keys and payloads
   uint32_t *k0 = nullptr, *k1 = nullptr, *i0 = nullptr, *i1 = nullptr, *row = nullptr;
-  FJ_CUDA(cudaMallocAsync(&k0, sizeof(uint32_t) * (m + 1), st));
-  FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint32_t) * (m + 1), st));
-  FJ_CUDA(cudaMallocAsync(&i0, sizeof(uint32_t) * (m + 1), st));
-  FJ_CUDA(cudaMallocAsync(&i1, sizeof(uint32_t) * (m + 1), st));
-  FJ_CUDA(cudaMallocAsync(&row, sizeof(uint32_t) * (m + 1), st));
-  FJ_CUDA(cudaMallocAsync(ort, sizeof(int64_t) * (n + 1), st));
-  FJ_CUDA(cudaMallocAsync(ocol, sizeof(int32_t) * (m + 8), st));
+  FJ_CUDA(tmp.alloc(&k0, (size_t)m + 1));
+  FJ_CUDA(tmp.alloc(&k1, (size_t)m + 1));
+  FJ_CUDA(tmp.alloc(&i0, (size_t)m + 1));
+  FJ_CUDA(tmp.alloc(&i1, (size_t)m + 1));
+  FJ_CUDA(tmp.alloc(&row, (size_t)m + 1));
+  FJ_CUDA(ws.alloc(ort, (size_t)n + 1));
+  FJ_CUDA(ws.alloc(ocol, (size_t)m + 8));
   *ow = nullptr;
-  if (g->in_w) FJ_CUDA(cudaMallocAsync(ow, sizeof(float) * (m + 8), st));
+  if (g->in_w) FJ_CUDA(ws.alloc(ow, (size_t)m + 8));
   fj::count_launch();
   k_out_keys<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, k0, i0, row);
-  FJ_TRY(sort_pairs(k0, k1, i0, i1, m, bits_for(n), st));
+  FJ_TRY(sort_pairs(k0, k1, i0, i1, m, bits_for(n), tmp));
   if (m > 0) {
     fj::count_launch();
     k_out_fill<<<grid_for(m), kBlock, 0, st>>>(m, i0, row, g->in_w, *ocol, *ow);
   }
   fj::count_launch();
   k_bounds<<<grid_for(n + 1), kBlock, 0, st>>>(n, m, k0, *ort);
-  FJ_CUDA(cudaFreeAsync(k0, st));
-  FJ_CUDA(cudaFreeAsync(k1, st));
-  FJ_CUDA(cudaFreeAsync(i0, st));
-  FJ_CUDA(cudaFreeAsync(i1, st));
-  FJ_CUDA(cudaFreeAsync(row, st));
   FJ_CUDA(cudaGetLastError());
   return FJ_OK;
 }
@@ -277,16 +273,16 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
   mark("stage");
 
   // 2. validate
+  Workspace ws(st);  // temporaries of the build; the graph owns the rest
   int *err = nullptr;
   int herr = 0;
-  FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
+  FJ_CUDA(ws.alloc(&err, 1));
   FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
   fj::count_launch();
   k_validate_rowptr<<<grid_for(n + 1), kBlock, 0, st>>>(n, m, g->in_rp, err);
   FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
   if (herr) {
-    cudaFreeAsync(err, st);
     set_error("fj_graph_create: in_row_ptr must start at 0, be non-decreasing and end at nnz");
     return FJ_ERR_INVALID;
   }
@@ -302,33 +298,31 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
     uint32_t *i0 = nullptr, *i1 = nullptr;
     int32_t *col_raw = nullptr;
     float *w_raw = nullptr;
-    FJ_CUDA(cudaMallocAsync(&k0, sizeof(uint64_t) * (m + 1), st));
-    FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint64_t) * (m + 1), st));
-    FJ_CUDA(cudaMallocAsync(&i0, sizeof(uint32_t) * (m + 1), st));
-    FJ_CUDA(cudaMallocAsync(&i1, sizeof(uint32_t) * (m + 1), st));
-    FJ_CUDA(cudaMallocAsync(&col_raw, sizeof(int32_t) * (m + 1), st));
+    Workspace sw(st);  // sort temporaries
+    FJ_CUDA(sw.alloc(&k0, (size_t)m + 1));
+    FJ_CUDA(sw.alloc(&k1, (size_t)m + 1));
+    FJ_CUDA(sw.alloc(&i0, (size_t)m + 1));
+    FJ_CUDA(sw.alloc(&i1, (size_t)m + 1));
+    FJ_CUDA(sw.alloc(&col_raw, (size_t)m + 1));
     FJ_CUDA(cudaMemcpyAsync(col_raw, g->in_col, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, st));
     if (w_in) {
-      FJ_CUDA(cudaMallocAsync(&w_raw, sizeof(float) * (m + 1), st));
+      FJ_CUDA(sw.alloc(&w_raw, (size_t)m + 1));
       FJ_CUDA(cudaMemcpyAsync(w_raw, g->in_w, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
     }
     fj::count_launch();
     k_in_keys<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, col_raw, nb, k0);
     fj::count_launch();
     k_iota_u32<<<grid_for(m), kBlock, 0, st>>>(m, i0);
-    FJ_TRY(sort_pairs(k0, k1, i0, i1, m, 2 * nb, st));
+    FJ_TRY(sort_pairs(k0, k1, i0, i1, m, 2 * nb, sw));
     FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
     fj::count_launch();
     k_unpack_sorted<<<grid_for(m), kBlock, 0, st>>>(m, nb, k0, i0, w_raw, g->in_col, g->in_w, err);
     FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    for (void *q : {(void *)k0, (void *)k1, (void *)i0, (void *)i1, (void *)col_raw, (void *)w_raw})
-      if (q) FJ_CUDA(cudaFreeAsync(q, st));
     FJ_CUDA(cudaStreamSynchronize(st));
     mark("canonicalise (sort)");
   }
   FJ_CUDA(cudaGetLastError());
   if (herr & ~64) {
-    cudaFreeAsync(err, st);
     set_error("fj_graph_create: %s%s%s%s",
               herr & 2 ? "column index out of range; " : "", herr & 4 ? "self-loop; " : "",
               herr & 8 ? "weight not positive and finite; " : "",
@@ -340,7 +334,7 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
   int64_t *ort = nullptr;
   int32_t *ocol = nullptr;
   float *ow = nullptr;
-  FJ_TRY(transpose_in_csr(g, &ort, &ocol, &ow));
+  FJ_TRY(transpose_in_csr(g, ws, &ort, &ocol, &ow));
   FJ_CUDA(cudaMallocAsync(&g->deg, sizeof(double) * n, st));
   fj::count_launch();
   k_row_sums<<<grid_warps(n), kBlock, 0, st>>>(n, ort, ow, g->deg);
@@ -359,22 +353,14 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
     FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
     FJ_CUDA(cudaStreamSynchronize(st));
     if (herr) {
-      cudaFreeAsync(ort, st);
-      cudaFreeAsync(ocol, st);
-      if (ow) cudaFreeAsync(ow, st);
-      cudaFreeAsync(err, st);
       set_error("fj_graph_create: directed = 0 but the arc set is not symmetric with equal weights");
       return FJ_ERR_INVALID;
     }
     mark("symmetry check");
   }
-  FJ_CUDA(cudaFreeAsync(err, st));
 
   // 6. sweep layout (1 color)
   fj_status s = build_layout_from_out(g, ort, ocol, ow, nullptr, 1, &g->async_layout);
-  cudaFreeAsync(ort, st);
-  cudaFreeAsync(ocol, st);
-  if (ow) cudaFreeAsync(ow, st);
   if (s != FJ_OK) return s;
   FJ_CUDA(cudaStreamSynchronize(st));
   FJ_CUDA(cudaGetLastError());

@@ -171,6 +171,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     tt0 = t1;
   };
   L->release(st);
+  Workspace ws(st);  // keys, counts, scans; the layout arrays belong to L
   L->warp_unit_arcs = 0;
   L->n = n;
   L->m = m;
@@ -180,11 +181,11 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   uint64_t *k0 = nullptr, *k1 = nullptr;
   unsigned long long *gcount = nullptr;
   int64_t *len = nullptr;
-  FJ_CUDA(cudaMallocAsync(&k0, sizeof(uint64_t) * n, st));
-  FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint64_t) * n, st));
-  FJ_CUDA(cudaMallocAsync(&gcount, sizeof(unsigned long long) * ngroups, st));
+  FJ_CUDA(ws.alloc(&k0, n));
+  FJ_CUDA(ws.alloc(&k1, n));
+  FJ_CUDA(ws.alloc(&gcount, ngroups));
   FJ_CUDA(cudaMemsetAsync(gcount, 0, sizeof(unsigned long long) * ngroups, st));
-  FJ_CUDA(cudaMallocAsync(&len, sizeof(int64_t) * (n + 1), st));
+  FJ_CUDA(ws.alloc(&len, (n + 1)));
   FJ_CUDA(cudaMemsetAsync(len + n, 0, sizeof(int64_t), st));
   fj::count_launch();
   k_layout_keys<<<gridn(n), kBlock, 0, st>>>(n, ort, color, ncolors, k0, gcount);
@@ -195,10 +196,9 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     cub::DoubleBuffer<uint64_t> dk(k0, k1);
     size_t tmp = 0;
     FJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, dk, n, 0, 31 + gbits, st));
-    void *t = nullptr;
-    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    unsigned char *t = nullptr;
+    FJ_CUDA(ws.alloc(&t, tmp));
     FJ_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, dk, n, 0, 31 + gbits, st));
-    FJ_CUDA(cudaFreeAsync(t, st));
     if (dk.Current() != k0) std::swap(k0, k1);
   }
   FJ_CUDA(cudaMallocAsync(&L->perm, sizeof(int32_t) * n, st));
@@ -212,10 +212,9 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   {
     size_t tmp = 0;
     FJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, len, L->rp, n + 1, st));
-    void *t = nullptr;
-    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    unsigned char *t = nullptr;
+    FJ_CUDA(ws.alloc(&t, tmp));
     FJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, len, L->rp, n + 1, st));
-    FJ_CUDA(cudaFreeAsync(t, st));
   }
   fj::count_launch();
   mark("keys+sort+perm+scan");
@@ -224,17 +223,15 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
 
   int64_t *dmax = nullptr;
   int64_t hmax = 0;
-  FJ_CUDA(cudaMallocAsync(&dmax, sizeof(int64_t), st));
+  FJ_CUDA(ws.alloc(&dmax, 1));
   {
     size_t tmp = 0;
     FJ_CUDA(cub::DeviceReduce::Max(nullptr, tmp, len, dmax, n, st));
-    void *t = nullptr;
-    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    unsigned char *t = nullptr;
+    FJ_CUDA(ws.alloc(&t, tmp));
     FJ_CUDA(cub::DeviceReduce::Max(t, tmp, len, dmax, n, st));
-    FJ_CUDA(cudaFreeAsync(t, st));
   }
   FJ_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  FJ_CUDA(cudaFreeAsync(dmax, st));
   std::vector<unsigned long long> hcount(ngroups);
   FJ_CUDA(cudaMemcpyAsync(hcount.data(), gcount, sizeof(unsigned long long) * ngroups,
                           cudaMemcpyDeviceToHost, st));
@@ -256,8 +253,8 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   // (1) row_ptr and warp-unit scan at every group boundary
   static const int kLmax[6] = {4, 8, 16, 32, 64, kWarpTileArcs > 64 ? kWarpTileArcs : 128};
   int64_t *npc = nullptr, *scan = nullptr, *dpos = nullptr, *dval = nullptr;
-  FJ_CUDA(cudaMallocAsync(&npc, sizeof(int64_t) * (n + 1), st));
-  FJ_CUDA(cudaMallocAsync(&scan, sizeof(int64_t) * (n + 1), st));
+  FJ_CUDA(ws.alloc(&npc, (n + 1)));
+  FJ_CUDA(ws.alloc(&scan, (n + 1)));
   fj::count_launch();
   // hub rows are split in warp pieces: long pieces (fewer partial combines)
   // for one-phase sweeps; short ones for colored sweeps, where every phase
@@ -269,15 +266,14 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   {
     size_t tmp = 0;
     FJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, npc, scan, n + 1, st));
-    void *t = nullptr;
-    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    unsigned char *t = nullptr;
+    FJ_CUDA(ws.alloc(&t, tmp));
     FJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, npc, scan, n + 1, st));
-    FJ_CUDA(cudaFreeAsync(t, st));
   }
   std::vector<int64_t> hpos(ngroups + 1), hrp(ngroups + 1), hscan(ngroups + 1);
   for (int q = 0; q <= ngroups; q++) hpos[q] = gstart[q];
-  FJ_CUDA(cudaMallocAsync(&dpos, sizeof(int64_t) * (ngroups + 1), st));
-  FJ_CUDA(cudaMallocAsync(&dval, sizeof(int64_t) * 2 * (ngroups + 1), st));
+  FJ_CUDA(ws.alloc(&dpos, (ngroups + 1)));
+  FJ_CUDA(ws.alloc(&dval, 2 * (ngroups + 1)));
   FJ_CUDA(cudaMemcpyAsync(dpos, hpos.data(), sizeof(int64_t) * (ngroups + 1), cudaMemcpyHostToDevice, st));
   fj::count_launch();
   k_pick<<<gridn(ngroups + 1), kBlock, 0, st>>>(ngroups + 1, dpos, L->rp, dval);
@@ -333,7 +329,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   }
   TileGroup *dg = nullptr;
   const size_t ngd = ctag.size() + rtag.size();
-  FJ_CUDA(cudaMallocAsync(&dg, sizeof(TileGroup) * std::max<size_t>(1, ngd), st));
+  FJ_CUDA(ws.alloc(&dg, std::max<size_t>(1, ngd)));
   if (!ctag.empty())
     FJ_CUDA(cudaMemcpyAsync(dg, ctag.data(), sizeof(TileGroup) * ctag.size(), cudaMemcpyHostToDevice, st));
   if (!rtag.empty())
@@ -359,7 +355,6 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     }
   }
   FJ_CUDA(cudaStreamSynchronize(st));  // host vectors above are stack-owned
-  for (void *q : {(void *)npc, (void *)scan, (void *)dpos, (void *)dval, (void *)dg}) cudaFreeAsync(q, st);
   mark("task lists");
   // measured on all five configs: direct loads beat the TMA-staged stream
   // once short rows run as warp tiles (the stage buffers take L1 away from
@@ -391,10 +386,6 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   FJ_CUDA(cudaMemcpyAsync(L->d_crow, L->crow.data(), sizeof(int64_t) * (ncolors + 2),
                           cudaMemcpyHostToDevice, st));
   FJ_CUDA(cudaStreamSynchronize(st));  // host vectors above are stack-owned
-  FJ_CUDA(cudaFreeAsync(k0, st));
-  FJ_CUDA(cudaFreeAsync(k1, st));
-  FJ_CUDA(cudaFreeAsync(gcount, st));
-  FJ_CUDA(cudaFreeAsync(len, st));
   FJ_CUDA(cudaGetLastError());
   return FJ_OK;
 }

@@ -257,14 +257,12 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   fj_stats stats{};
   stats.colors = P.ncolors;
 
+  Workspace ws(st);
   cudaEvent_t e0, e1, es0, es1;
-  FJ_CUDA(cudaEventCreate(&e0));
-  FJ_CUDA(cudaEventCreate(&e1));
-  FJ_CUDA(cudaEventCreate(&es0));
-  FJ_CUDA(cudaEventCreate(&es1));
+  for (cudaEvent_t *e : {&e0, &e1, &es0, &es1}) FJ_CUDA(ws.event(e));
   FJ_CUDA(cudaEventRecord(e0, st));
   Staged s{};
-  FJ_TRY(stage_in(s_in, n, st, s));
+  FJ_TRY(stage_in(s_in, n, ws, s));
   const bool zdev = is_device_ptr(z_out);
   const bool zpdev = o->zprime_out && is_device_ptr(o->zprime_out);
   float *sP = nullptr, *sL = nullptr, *smin = nullptr, *zo = nullptr;
@@ -274,30 +272,29 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   unsigned *ctl = nullptr;
   SweepCounters *cnt = nullptr;
   unsigned long long *outv = nullptr;
-  FJ_CUDA(cudaMallocAsync(&sP, sizeof(float) * n, st));
-  FJ_CUDA(cudaMallocAsync(&sL, sizeof(float) * n, st));
-  FJ_CUDA(cudaMallocAsync(&zP, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&rP, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&qP, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&zL, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&tmp, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&RL, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&smin, sizeof(float) * 2, st));
-  FJ_CUDA(cudaMallocAsync(&S, sizeof(Scalars), st));
-  FJ_CUDA(cudaMallocAsync(&ctl, sizeof(unsigned) * kCtlWords, st));
-  FJ_CUDA(cudaMallocAsync(&cnt, sizeof(SweepCounters) * 3, st));
-  FJ_CUDA(cudaMallocAsync(&outv, sizeof(unsigned long long) * 8, st));
-  if (!zdev) FJ_CUDA(cudaMallocAsync(&zo, sizeof(float) * n, st));
-  if (o->zprime_out && !zpdev) FJ_CUDA(cudaMallocAsync(&zp, sizeof(double) * n, st));
+  FJ_CUDA(ws.alloc(&sP, n));
+  FJ_CUDA(ws.alloc(&sL, n));
+  FJ_CUDA(ws.alloc(&zP, n));
+  FJ_CUDA(ws.alloc(&rP, n));
+  FJ_CUDA(ws.alloc(&qP, n));
+  FJ_CUDA(ws.alloc(&zL, n));
+  FJ_CUDA(ws.alloc(&tmp, n));
+  FJ_CUDA(ws.alloc(&RL, n));
+  FJ_CUDA(ws.alloc(&smin, 2));
+  FJ_CUDA(ws.alloc(&S, 1));
+  FJ_CUDA(ws.alloc(&ctl, kCtlWords));
+  FJ_CUDA(ws.alloc(&cnt, 3));
+  FJ_CUDA(ws.alloc(&outv, 8));
+  if (!zdev) FJ_CUDA(ws.alloc(&zo, n));
+  if (o->zprime_out && !zpdev) FJ_CUDA(ws.alloc(&zp, n));
   {
     size_t t1 = 0, t2 = 0;
     FJ_CUDA(cub::DeviceReduce::Min(nullptr, t1, s.dev, smin, n, st));
     FJ_CUDA(cub::DeviceReduce::Max(nullptr, t2, s.dev, smin + 1, n, st));
-    void *t = nullptr;
-    FJ_CUDA(cudaMallocAsync(&t, std::max(t1, t2), st));
+    unsigned char *t = nullptr;
+    FJ_CUDA(ws.alloc(&t, std::max(t1, t2)));
     FJ_CUDA(cub::DeviceReduce::Min(t, t1, s.dev, smin, n, st));
     FJ_CUDA(cub::DeviceReduce::Max(t, t2, s.dev, smin + 1, n, st));
-    FJ_CUDA(cudaFreeAsync(t, st));
   }
   fj::count_launch();
   k_scalars<<<1, 1, 0, st>>>(smin, smin + 1, eps, o->sigma, o->c, S);
@@ -331,7 +328,7 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   pp.cnt = cnt;
   pp.out = outv;
   int32_t *front = nullptr;
-  FJ_CUDA(cudaMallocAsync(&front, sizeof(int32_t) * n, st));
+  FJ_CUDA(ws.alloc(&front, n));
   pp.front = front;
   pp.fcount = reinterpret_cast<unsigned long long *>(ctl + 16);  // zeroed with ctl
   pp.sparse_div = getenv("FJ_PUSH_SPARSE_DIV") ? atoi(getenv("FJ_PUSH_SPARSE_DIV")) : 8;
@@ -344,8 +341,8 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   kq.rout = RL;
   double2 *partial = nullptr;  // long-row partials of the pull layout (certificate)
   int *arrive = nullptr;
-  FJ_CUDA(cudaMallocAsync(&partial, sizeof(double2) * std::max(1, L.npartials), st));
-  FJ_CUDA(cudaMallocAsync(&arrive, sizeof(int) * std::max(1, L.npartials), st));
+  FJ_CUDA(ws.alloc(&partial, std::max(1, L.npartials)));
+  FJ_CUDA(ws.alloc(&arrive, std::max(1, L.npartials)));
   FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
   kq.partial = partial;
   kq.arrive = arrive;
@@ -416,12 +413,6 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   stats.sweep_ms = ms_sweep;
   stats.c = hs.c;
   stats.eps_prime = hs.eps_p;
-  for (void *q : {(void *)sP, (void *)sL, (void *)zP, (void *)rP, (void *)qP, (void *)zL,
-                  (void *)tmp, (void *)RL, (void *)smin, (void *)S, (void *)ctl, (void *)cnt,
-                  (void *)outv, (void *)zo, (void *)zp, (void *)s.owned, (void *)partial,
-                  (void *)arrive, (void *)front})
-    if (q) cudaFreeAsync(q, st);
-  for (cudaEvent_t e : {e0, e1, es0, es1}) cudaEventDestroy(e);
   FJ_CUDA(cudaGetLastError());
   fj_status rc = finish_status(hs, stats, o, omega);
   if (st_out) *st_out = stats;

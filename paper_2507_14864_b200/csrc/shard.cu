@@ -438,28 +438,23 @@ static fj_status shard_create_impl(fj_comm *cm, int rank, int64_t n, const int64
   g->weighted = w_in ? 1 : 0;
   g->stream = st;
   g->num_sms = cm->num_sms;
+  Workspace ws(st);  // staged input and temporaries
   int64_t *rp = nullptr;
   int32_t *col = nullptr, *enc = nullptr;
   float *w = nullptr;
   int *err = nullptr;
   const int64_t nl = s->n_local;
-  FJ_CUDA(cudaMallocAsync(&rp, sizeof(int64_t) * (nl + 1), st));
-  FJ_CUDA(cudaMallocAsync(&col, sizeof(int32_t) * (m + 8), st));
-  FJ_CUDA(cudaMallocAsync(&enc, sizeof(int32_t) * (m + 8), st));
-  if (w_in) FJ_CUDA(cudaMallocAsync(&w, sizeof(float) * (m + 8), st));
-  FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
+  FJ_CUDA(ws.alloc(&rp, (nl + 1)));
+  FJ_CUDA(ws.alloc(&col, (m + 8)));
+  FJ_CUDA(ws.alloc(&enc, (m + 8)));
+  if (w_in) FJ_CUDA(ws.alloc(&w, (m + 8)));
+  FJ_CUDA(ws.alloc(&err, 1));
   FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
   FJ_CUDA(cudaMemcpyAsync(rp, rp_in, sizeof(int64_t) * (nl + 1), cudaMemcpyDefault, st));
   if (m > 0) {
     FJ_CUDA(cudaMemcpyAsync(col, col_in, sizeof(int32_t) * m, cudaMemcpyDefault, st));
     if (w_in) FJ_CUDA(cudaMemcpyAsync(w, w_in, sizeof(float) * m, cudaMemcpyDefault, st));
   }
-  auto done = [&](fj_status rc) {
-    for (void *q : {(void *)rp, (void *)col, (void *)enc, (void *)w, (void *)err})
-      if (q) cudaFreeAsync(q, st);
-    cudaStreamSynchronize(st);
-    return rc;
-  };
   int herr = 0;
   count_launch();
   k_shard_rowptr<<<gridn(nl + 1), kBlock, 0, st>>>(nl, m, rp, err);
@@ -467,7 +462,7 @@ static fj_status shard_create_impl(fj_comm *cm, int rank, int64_t n, const int64
   FJ_CUDA(cudaStreamSynchronize(st));
   if (herr) {
     set_error("fj_shard_create: out_row_ptr must start at 0, be non-decreasing and end at nnz");
-    return done(FJ_ERR_INVALID);
+    return FJ_ERR_INVALID;
   }
   const unsigned wgrid = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>((nl * 32 + kBlock - 1) / kBlock, (int64_t)cm->num_sms * 64));
@@ -479,13 +474,14 @@ static fj_status shard_create_impl(fj_comm *cm, int rank, int64_t n, const int64
     set_error("fj_shard_create: %s%s%s%s", herr & 2 ? "column id out of range; " : "",
               herr & 4 ? "self-loop; " : "", herr & 8 ? "weight not positive and finite; " : "",
               herr & 16 ? "row not strictly increasing (unsorted or duplicate arc); " : "");
-    return done(FJ_ERR_INVALID);
+    return FJ_ERR_INVALID;
   }
   FJ_CUDA(cudaMallocAsync(&g->deg, sizeof(double) * nl, st));
   count_launch();
   k_shard_rowsum<<<wgrid, kBlock, 0, st>>>(nl, rp, w, g->deg);
   fj_status rc = build_layout_from_out(g, rp, enc, w, nullptr, 1, &g->async_layout);
-  return done(rc);
+  FJ_CUDA(cudaStreamSynchronize(st));
+  return rc;
 }
 
 static fj_status connect_impl(fj_shard **sh, int count) {
@@ -493,10 +489,11 @@ static fj_status connect_impl(fj_shard **sh, int count) {
   cudaStream_t st = cm->stream;
   const int W = cm->world;
   const int64_t seg = sh[0]->seg_max;
+  Workspace ws(st);  // temporaries; the halo lists belong to the shards
   std::vector<int32_t *> pad(count), all(count);
   for (int i = 0; i < count; i++) {
-    FJ_CUDA(cudaMallocAsync(&pad[i], sizeof(int32_t) * seg, st));
-    FJ_CUDA(cudaMallocAsync(&all[i], sizeof(int32_t) * seg * W, st));
+    FJ_CUDA(ws.alloc(&pad[i], seg));
+    FJ_CUDA(ws.alloc(&all[i], seg * W));
     FJ_CUDA(cudaMemsetAsync(pad[i], 0xff, sizeof(int32_t) * seg, st));
     FJ_CUDA(cudaMemcpyAsync(pad[i], sh[i]->g->async_layout.iperm, sizeof(int32_t) * sh[i]->n_local,
                             cudaMemcpyDeviceToDevice, st));
@@ -511,9 +508,9 @@ static fj_status connect_impl(fj_shard **sh, int count) {
   }
   int *err = nullptr;
   int64_t *dbeg = nullptr;
-  FJ_CUDA(cudaMallocAsync(&err, sizeof(int), st));
+  FJ_CUDA(ws.alloc(&err, 1));
   FJ_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-  FJ_CUDA(cudaMallocAsync(&dbeg, sizeof(int64_t) * (W + 1), st));
+  FJ_CUDA(ws.alloc(&dbeg, (W + 1)));
   FJ_CUDA(cudaMemcpyAsync(dbeg, sh[0]->begin.data(), sizeof(int64_t) * (W + 1),
                           cudaMemcpyHostToDevice, st));
   // per shard: halo keys of the remote columns, sorted and made unique → the
@@ -526,11 +523,11 @@ static fj_status connect_impl(fj_shard **sh, int count) {
     const int64_t m = L.m;
     uint64_t *keys = nullptr, *k1 = nullptr, *uq = nullptr;
     int64_t *nsel = nullptr, *dhoff = nullptr;
-    FJ_CUDA(cudaMallocAsync(&keys, sizeof(uint64_t) * std::max<int64_t>(1, m), st));
-    FJ_CUDA(cudaMallocAsync(&k1, sizeof(uint64_t) * std::max<int64_t>(1, m), st));
-    FJ_CUDA(cudaMallocAsync(&uq, sizeof(uint64_t) * std::max<int64_t>(1, m), st));
-    FJ_CUDA(cudaMallocAsync(&nsel, sizeof(int64_t), st));
-    FJ_CUDA(cudaMallocAsync(&dhoff, sizeof(int64_t) * W, st));
+    FJ_CUDA(ws.alloc(&keys, std::max<int64_t>(1, m)));
+    FJ_CUDA(ws.alloc(&k1, std::max<int64_t>(1, m)));
+    FJ_CUDA(ws.alloc(&uq, std::max<int64_t>(1, m)));
+    FJ_CUDA(ws.alloc(&nsel, 1));
+    FJ_CUDA(ws.alloc(&dhoff, W));
     FJ_CUDA(cudaMemsetAsync(nsel, 0, sizeof(int64_t), st));
     int64_t nu = 0;
     if (m > 0) {
@@ -540,11 +537,10 @@ static fj_status connect_impl(fj_shard **sh, int count) {
       size_t t1 = 0, t2 = 0;
       FJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t1, keys, k1, m, 0, 64, st));
       FJ_CUDA(cub::DeviceSelect::Unique(nullptr, t2, k1, uq, nsel, m, st));
-      void *t = nullptr;
-      FJ_CUDA(cudaMallocAsync(&t, std::max(t1, t2), st));
+      unsigned char *t = nullptr;
+      FJ_CUDA(ws.alloc(&t, std::max(t1, t2)));
       FJ_CUDA(cub::DeviceRadixSort::SortKeys(t, t1, keys, k1, m, 0, 64, st));
       FJ_CUDA(cub::DeviceSelect::Unique(t, t2, k1, uq, nsel, m, st));
-      FJ_CUDA(cudaFreeAsync(t, st));
       FJ_CUDA(cudaMemcpyAsync(&nu, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
       FJ_CUDA(cudaStreamSynchronize(st));
       if (nu > 0) {  // the own-column sentinel sorts last
@@ -569,21 +565,18 @@ static fj_status connect_impl(fj_shard **sh, int count) {
     S->hoff[W - 1] = nu;
     S->nz = S->n_local + nu;
     for (int j = 0; j + 1 < W; j++) need_from[i][(S->rank + 1 + j) % W] = S->hoff[j + 1] - S->hoff[j];
-    for (void *q : {(void *)keys, (void *)k1, (void *)uq, (void *)nsel, (void *)dhoff})
-      cudaFreeAsync(q, st);
   }
   // NCCL: every rank learns what each peer reads from it (its send lists)
   if (!cm->local && W > 1) {
     fj_shard *me = sh[0];
     int64_t *cnt = nullptr;
-    FJ_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * W * (W + 1), st));
+    FJ_CUDA(ws.alloc(&cnt, W * (W + 1)));
     FJ_CUDA(cudaMemcpyAsync(cnt + (int64_t)W * W, need_from[0].data(), sizeof(int64_t) * W,
                             cudaMemcpyHostToDevice, st));
     FJ_NCCL(nccl()->AllGather(cnt + (int64_t)W * W, cnt, (size_t)W, ncclInt64, cm->nc, st));
     std::vector<int64_t> hc((size_t)W * W);  // hc[q·W + r]: what q reads from r
     FJ_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int64_t) * W * W, cudaMemcpyDeviceToHost, st));
     FJ_CUDA(cudaStreamSynchronize(st));
-    cudaFreeAsync(cnt, st);
     me->soff.assign(W + 1, 0);
     for (int q = 0; q < W; q++)
       me->soff[q + 1] = me->soff[q] + (q == me->rank ? 0 : hc[(size_t)q * W + me->rank]);
@@ -604,12 +597,6 @@ static fj_status connect_impl(fj_shard **sh, int count) {
   }
   FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
-  for (int i = 0; i < count; i++) {
-    cudaFreeAsync(pad[i], st);
-    cudaFreeAsync(all[i], st);
-  }
-  cudaFreeAsync(err, st);
-  cudaFreeAsync(dbeg, st);
   FJ_CUDA(cudaStreamSynchronize(st));
   if (herr) {
     set_error("fj_shard_connect: inconsistent partitions across ranks");
@@ -644,42 +631,39 @@ static fj_status shard_solve_impl(fj_shard **sh, int count, const float *const *
   std::vector<ShardWork> wk(count);
   std::vector<void *> red(count);
   std::vector<double *> zb(count);
+  Workspace ws(st);
   cudaEvent_t e0, e1, es0, es1;
-  FJ_CUDA(cudaEventCreate(&e0));
-  FJ_CUDA(cudaEventCreate(&e1));
-  FJ_CUDA(cudaEventCreate(&es0));
-  FJ_CUDA(cudaEventCreate(&es1));
+  for (cudaEvent_t *e : {&e0, &e1, &es0, &es1}) FJ_CUDA(ws.event(e));
   FJ_CUDA(cudaEventRecord(e0, st));
   for (int i = 0; i < count; i++) {
     ShardWork &w = wk[i];
     const Layout &L = sh[i]->g->async_layout;
     const int64_t nl = sh[i]->n_local;
-    FJ_TRY(stage_in(s_in[i], nl, st, w.s));
-    FJ_CUDA(cudaMallocAsync(&w.s_l, sizeof(float) * nl, st));
-    FJ_CUDA(cudaMallocAsync(&w.smm, sizeof(float) * 2, st));
-    FJ_CUDA(cudaMallocAsync(&w.z, sizeof(double) * sh[i]->nz, st));
+    FJ_TRY(stage_in(s_in[i], nl, ws, w.s));
+    FJ_CUDA(ws.alloc(&w.s_l, nl));
+    FJ_CUDA(ws.alloc(&w.smm, 2));
+    FJ_CUDA(ws.alloc(&w.z, sh[i]->nz));
     FJ_CUDA(cudaMemsetAsync(w.z, 0, sizeof(double) * sh[i]->nz, st));
-    FJ_CUDA(cudaMallocAsync(&w.S, sizeof(Scalars), st));
-    FJ_CUDA(cudaMallocAsync(&w.partial, sizeof(double2) * std::max(1, L.npartials), st));
-    FJ_CUDA(cudaMallocAsync(&w.arrive, sizeof(int) * std::max(1, L.npartials), st));
+    FJ_CUDA(ws.alloc(&w.S, 1));
+    FJ_CUDA(ws.alloc(&w.partial, std::max(1, L.npartials)));
+    FJ_CUDA(ws.alloc(&w.arrive, std::max(1, L.npartials)));
     FJ_CUDA(cudaMemsetAsync(w.arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
-    FJ_CUDA(cudaMallocAsync(&w.ctl, sizeof(unsigned) * kCtlWords, st));
-    FJ_CUDA(cudaMallocAsync(&w.cnt, sizeof(SweepCounters) * 3, st));
-    FJ_CUDA(cudaMallocAsync(&w.outv, sizeof(unsigned long long) * (9 + 4 * kSweepBatch), st));
+    FJ_CUDA(ws.alloc(&w.ctl, kCtlWords));
+    FJ_CUDA(ws.alloc(&w.cnt, 3));
+    FJ_CUDA(ws.alloc(&w.outv, (9 + 4 * kSweepBatch)));
     w.stop = w.outv + 8;
     w.agg = w.outv + 9;
-    if (!is_device_ptr(z_out[i])) FJ_CUDA(cudaMallocAsync(&w.zo, sizeof(float) * nl, st));
+    if (!is_device_ptr(z_out[i])) FJ_CUDA(ws.alloc(&w.zo, nl));
     if (zp_out && zp_out[i] && !is_device_ptr(zp_out[i]))
-      FJ_CUDA(cudaMallocAsync(&w.zp, sizeof(double) * nl, st));
+      FJ_CUDA(ws.alloc(&w.zp, nl));
     size_t tmp = 0, tmp2 = 0;
     FJ_CUDA(cub::DeviceReduce::Min(nullptr, tmp, w.s.dev, w.smm, nl, st));
     FJ_CUDA(cub::DeviceReduce::Max(nullptr, tmp2, w.s.dev, w.smm + 1, nl, st));
     tmp = std::max(tmp, tmp2);
-    void *t = nullptr;
-    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    unsigned char *t = nullptr;
+    FJ_CUDA(ws.alloc(&t, tmp));
     FJ_CUDA(cub::DeviceReduce::Min(t, tmp, w.s.dev, w.smm, nl, st));
     FJ_CUDA(cub::DeviceReduce::Max(t, tmp, w.s.dev, w.smm + 1, nl, st));
-    FJ_CUDA(cudaFreeAsync(t, st));
   }
   // a2: global shift from the global min / max of s (Alg. 2)
   {
@@ -845,13 +829,6 @@ static fj_status shard_solve_impl(fj_shard **sh, int count, const float *const *
   stats.c = hs.c;
   stats.eps_prime = hs.eps_p;
   hs.bad_input = bad_input ? 1 : 0;
-  for (ShardWork &w : wk) {
-    for (void *q : {(void *)w.s_l, (void *)w.smm, (void *)w.zo, (void *)w.z, (void *)w.zp,
-                    (void *)w.partial, (void *)w.arrive, (void *)w.S, (void *)w.ctl, (void *)w.cnt,
-                    (void *)w.outv, (void *)w.s.owned})
-      if (q) cudaFreeAsync(q, st);
-  }
-  for (cudaEvent_t e : {e0, e1, es0, es1}) cudaEventDestroy(e);
   FJ_CUDA(cudaStreamSynchronize(st));
   FJ_CUDA(cudaGetLastError());
   fj_status rc = finish_status(hs, stats, o, omega);
@@ -864,19 +841,20 @@ static fj_status shard_measures_impl(fj_shard **sh, int count, const float *cons
   NvtxRange nv("fj_shard_measures");
   fj_comm *cm = sh[0]->comm;
   cudaStream_t st = cm->stream;
+  Workspace ws(st);
   std::vector<Staged> z(count), s(count);
   std::vector<double *> zl(count), sums(count);
   std::vector<void *> red(count);
   std::vector<unsigned *> ctr(count);
   for (int i = 0; i < count; i++) {
     const int64_t nl = sh[i]->n_local;
-    FJ_TRY(stage_in(z_in[i], nl, st, z[i]));
-    if (s_in && s_in[i]) FJ_TRY(stage_in(s_in[i], nl, st, s[i]));
-    FJ_CUDA(cudaMallocAsync(&zl[i], sizeof(double) * sh[i]->nz, st));
+    FJ_TRY(stage_in(z_in[i], nl, ws, z[i]));
+    if (s_in && s_in[i]) FJ_TRY(stage_in(s_in[i], nl, ws, s[i]));
+    FJ_CUDA(ws.alloc(&zl[i], sh[i]->nz));
     FJ_CUDA(cudaMemsetAsync(zl[i], 0, sizeof(double) * sh[i]->nz, st));
-    FJ_CUDA(cudaMallocAsync(&sums[i], sizeof(double) * 5, st));
+    FJ_CUDA(ws.alloc(&sums[i], 5));
     FJ_CUDA(cudaMemsetAsync(sums[i], 0, sizeof(double) * 5, st));
-    FJ_CUDA(cudaMallocAsync(&ctr[i], sizeof(unsigned), st));
+    FJ_CUDA(ws.alloc(&ctr[i], 1));
     FJ_CUDA(cudaMemsetAsync(ctr[i], 0, sizeof(unsigned), st));
     count_launch();
     k_meas_nodes1<<<gridn(nl), kBlock, 0, st>>>(nl, sh[i]->g->async_layout.perm, z[i].dev, zl[i],
@@ -909,11 +887,6 @@ static fj_status shard_measures_impl(fj_shard **sh, int count, const float *cons
   double h[5];
   FJ_CUDA(cudaMemcpyAsync(h, sums[0], sizeof(h), cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
-  for (int i = 0; i < count; i++) {
-    for (void *q : {(void *)zl[i], (void *)sums[i], (void *)ctr[i], (void *)z[i].owned,
-                    (void *)s[i].owned})
-      if (q) cudaFreeAsync(q, st);
-  }
   FJ_CUDA(cudaStreamSynchronize(st));
   FJ_CUDA(cudaGetLastError());
   out->polarization = h[1];

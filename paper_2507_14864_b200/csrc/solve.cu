@@ -479,17 +479,13 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   const Layout &L = (method == FJ_METHOD_COLORED) ? g->color_layout : g->async_layout;
   const bool W = g->weighted != 0;
 
+  Workspace ws(st);
   cudaEvent_t e0, e1, es0, es1, ec0, ec1;
-  FJ_CUDA(cudaEventCreate(&e0));
-  FJ_CUDA(cudaEventCreate(&e1));
-  FJ_CUDA(cudaEventCreate(&es0));
-  FJ_CUDA(cudaEventCreate(&es1));
-  FJ_CUDA(cudaEventCreate(&ec0));
-  FJ_CUDA(cudaEventCreate(&ec1));
+  for (cudaEvent_t *e : {&e0, &e1, &es0, &es1, &ec0, &ec1}) FJ_CUDA(ws.event(e));
   FJ_CUDA(cudaEventRecord(e0, st));
 
   Staged s{};
-  FJ_TRY(stage_in(s_in, n, st, s));
+  FJ_TRY(stage_in(s_in, n, ws, s));
   const bool zdev = is_device_ptr(z_out);
   const bool zpdev = o->zprime_out && is_device_ptr(o->zprime_out);
 
@@ -502,20 +498,20 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   unsigned *ctl = nullptr;  // ctr[3] + bar[2]
   SweepCounters *cnt = nullptr;
   unsigned long long *outv = nullptr, *certbits = nullptr;
-  FJ_CUDA(cudaMallocAsync(&s_l, sizeof(float) * n, st));
-  FJ_CUDA(cudaMallocAsync(&z, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&smin, sizeof(float) * 2, st));
+  FJ_CUDA(ws.alloc(&s_l, n));
+  FJ_CUDA(ws.alloc(&z, n));
+  FJ_CUDA(ws.alloc(&smin, 2));
   smax = smin + 1;
-  FJ_CUDA(cudaMallocAsync(&S, sizeof(Scalars), st));
-  FJ_CUDA(cudaMallocAsync(&partial, sizeof(double2) * std::max(1, L.npartials), st));
-  FJ_CUDA(cudaMallocAsync(&arrive, sizeof(int) * std::max(1, L.npartials), st));
+  FJ_CUDA(ws.alloc(&S, 1));
+  FJ_CUDA(ws.alloc(&partial, std::max(1, L.npartials)));
+  FJ_CUDA(ws.alloc(&arrive, std::max(1, L.npartials)));
   FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
-  FJ_CUDA(cudaMallocAsync(&ctl, sizeof(unsigned) * kCtlWords, st));
-  FJ_CUDA(cudaMallocAsync(&cnt, sizeof(SweepCounters) * 3, st));
-  FJ_CUDA(cudaMallocAsync(&outv, sizeof(unsigned long long) * 8, st));
+  FJ_CUDA(ws.alloc(&ctl, kCtlWords));
+  FJ_CUDA(ws.alloc(&cnt, 3));
+  FJ_CUDA(ws.alloc(&outv, 8));
   certbits = outv + 4;
-  if (!zdev) FJ_CUDA(cudaMallocAsync(&zo, sizeof(float) * n, st));
-  if (o->zprime_out && !zpdev) FJ_CUDA(cudaMallocAsync(&zp, sizeof(double) * n, st));
+  if (!zdev) FJ_CUDA(ws.alloc(&zo, n));
+  if (o->zprime_out && !zpdev) FJ_CUDA(ws.alloc(&zp, n));
 
   // a2: shift and init (Alg. 2)
   {
@@ -524,11 +520,10 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     size_t tmp2 = 0;
     FJ_CUDA(cub::DeviceReduce::Max(nullptr, tmp2, s.dev, smax, n, st));
     tmp = std::max(tmp, tmp2);
-    void *t = nullptr;
-    FJ_CUDA(cudaMallocAsync(&t, tmp, st));
+    unsigned char *t = nullptr;
+    FJ_CUDA(ws.alloc(&t, tmp));
     FJ_CUDA(cub::DeviceReduce::Min(t, tmp, s.dev, smin, n, st));
     FJ_CUDA(cub::DeviceReduce::Max(t, tmp, s.dev, smax, n, st));
-    FJ_CUDA(cudaFreeAsync(t, st));
   }
   fj::count_launch();
   k_scalars<<<1, 1, 0, st>>>(smin, smax, eps, o->sigma, o->c, S);
@@ -538,14 +533,13 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     if (is_device_ptr(o->z_init)) {
       zinit = o->z_init;
     } else {
-      FJ_CUDA(cudaMallocAsync(&zinit_owned, sizeof(double) * n, st));
+      FJ_CUDA(ws.alloc(&zinit_owned, n));
       FJ_CUDA(cudaMemcpyAsync(zinit_owned, o->z_init, sizeof(double) * n, cudaMemcpyHostToDevice, st));
       zinit = zinit_owned;
     }
   }
   fj::count_launch();
   k_init<<<gridn(n), kBlock, 0, st>>>(n, L.perm, L.rp, s.dev, S, s_l, z, zinit);
-  if (zinit_owned) FJ_CUDA(cudaFreeAsync(zinit_owned, st));
 
   KP p = make_kp(g, L);
   p.s = s_l;
@@ -591,7 +585,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   AsyncCtl *actl = nullptr;
   if (barrier_free) {
     FJ_CUDA(cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)async_smem));
-    FJ_CUDA(cudaMallocAsync(&actl, sizeof(AsyncCtl), st));
+    FJ_CUDA(ws.alloc(&actl, 1));
   }
   const int agrid = barrier_free ? persistent_grid(fa, g->num_sms, async_smem) : 0;
   for (;;) {
@@ -648,7 +642,6 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     // the certificate rejects is relaxed again
     p.theta *= 0.5;
   }
-  if (actl) cudaFreeAsync(actl, st);
   stats.cert_rounds = rounds;
   stats.phases = stats.sweeps * L.ncolors;
   stats.rows_read = stats.sweeps * L.active_rows;
@@ -674,19 +667,6 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   stats.c = hs.c;
   stats.eps_prime = hs.eps_p;
 
-  cudaFreeAsync(s_l, st);
-  cudaFreeAsync(z, st);
-  cudaFreeAsync(smin, st);
-  cudaFreeAsync(S, st);
-  cudaFreeAsync(partial, st);
-  cudaFreeAsync(arrive, st);
-  cudaFreeAsync(ctl, st);
-  cudaFreeAsync(cnt, st);
-  cudaFreeAsync(outv, st);
-  if (zo) cudaFreeAsync(zo, st);
-  if (zp) cudaFreeAsync(zp, st);
-  if (s.owned) cudaFreeAsync(s.owned, st);
-  for (cudaEvent_t e : {e0, e1, es0, es1, ec0, ec1}) cudaEventDestroy(e);
   FJ_CUDA(cudaGetLastError());
 
   fj_status rc = finish_status(hs, stats, o, omega);
@@ -699,15 +679,16 @@ fj_status measures_impl(fj_graph *g, const float *z_in, const float *s_in, fj_me
   cudaStream_t st = g->stream;
   const int64_t n = g->n;
   const Layout &L = g->async_layout;
+  Workspace ws(st);
   Staged z{}, s{};
-  FJ_TRY(stage_in(z_in, n, st, z));
-  if (s_in) FJ_TRY(stage_in(s_in, n, st, s));
+  FJ_TRY(stage_in(z_in, n, ws, z));
+  if (s_in) FJ_TRY(stage_in(s_in, n, ws, s));
   double *zl = nullptr, *sums = nullptr;
   unsigned *ctr = nullptr;
-  FJ_CUDA(cudaMallocAsync(&zl, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&sums, sizeof(double) * 5, st));
+  FJ_CUDA(ws.alloc(&zl, n));
+  FJ_CUDA(ws.alloc(&sums, 5));
   FJ_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * 5, st));
-  FJ_CUDA(cudaMallocAsync(&ctr, sizeof(unsigned), st));
+  FJ_CUDA(ws.alloc(&ctr, 1));
   FJ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), st));
   fj::count_launch();
   k_meas_nodes1<<<gridn(n), kBlock, 0, st>>>(n, L.perm, z.dev, zl, sums);
@@ -725,11 +706,6 @@ fj_status measures_impl(fj_graph *g, const float *z_in, const float *s_in, fj_me
   double h[5];
   FJ_CUDA(cudaMemcpyAsync(h, sums, sizeof(h), cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
-  cudaFreeAsync(zl, st);
-  cudaFreeAsync(sums, st);
-  cudaFreeAsync(ctr, st);
-  if (z.owned) cudaFreeAsync(z.owned, st);
-  if (s.owned) cudaFreeAsync(s.owned, st);
   FJ_CUDA(cudaGetLastError());
   out->polarization = h[1];
   // each undirected edge is stored as two arcs (reading R14)
@@ -773,8 +749,9 @@ __global__ void __launch_bounds__(kBlock) k_gather_probe(int64_t m, const int32_
 fj_status gather_probe_impl(fj_graph *g, int reps, double *ms_per_pass) {
   cudaStream_t st = g->stream;
   const Layout &L = g->async_layout;
+  Workspace ws(st);
   double *x = nullptr;
-  FJ_CUDA(cudaMallocAsync(&x, sizeof(double) * (g->n + 1), st));
+  FJ_CUDA(ws.alloc(&x, (size_t)g->n + 1));
   FJ_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (g->n + 1), st));
   const void *fn = L.w ? (const void *)k_gather_probe<true> : (const void *)k_gather_probe<false>;
   const int grid = persistent_grid(fn, g->num_sms);
@@ -784,8 +761,8 @@ fj_status gather_probe_impl(fj_graph *g, int reps, double *ms_per_pass) {
   double *sink = x + g->n;
   void *args[] = {&m, &col, &w, &x, &sink};
   cudaEvent_t a, b;
-  FJ_CUDA(cudaEventCreate(&a));
-  FJ_CUDA(cudaEventCreate(&b));
+  FJ_CUDA(ws.event(&a));
+  FJ_CUDA(ws.event(&b));
   fj::count_launch();
   FJ_CUDA(cudaLaunchKernel(fn, grid, kBlock, args, 0, st));  // warm-up
   FJ_CUDA(cudaEventRecord(a, st));
@@ -797,9 +774,6 @@ fj_status gather_probe_impl(fj_graph *g, int reps, double *ms_per_pass) {
   FJ_CUDA(cudaEventSynchronize(b));
   float ms = 0.f;
   FJ_CUDA(cudaEventElapsedTime(&ms, a, b));
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
-  cudaFreeAsync(x, st);
   FJ_CUDA(cudaStreamSynchronize(st));
   *ms_per_pass = ms / reps;
   return FJ_OK;
@@ -846,10 +820,11 @@ fj_status omega_opt_impl(fj_graph *g, int max_iters, double tol, double *mu_out,
   const int64_t n = g->n;
   double *x = nullptr, *y = nullptr, *sums = nullptr, *partial = nullptr;
   unsigned *ctr = nullptr;
-  FJ_CUDA(cudaMallocAsync(&x, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&y, sizeof(double) * n, st));
-  FJ_CUDA(cudaMallocAsync(&sums, sizeof(double) * 2, st));
-  FJ_CUDA(cudaMallocAsync(&ctr, sizeof(unsigned), st));
+  Workspace ws(st);
+  FJ_CUDA(ws.alloc(&x, (size_t)n));
+  FJ_CUDA(ws.alloc(&y, n));
+  FJ_CUDA(ws.alloc(&sums, 2));
+  FJ_CUDA(ws.alloc(&ctr, 1));
   fj::count_launch();
   k_fill<<<gridn(n), kBlock, 0, st>>>(n, 1.0 / sqrt((double)n), x);
   KP p = make_kp(g, L);
@@ -880,10 +855,6 @@ fj_status omega_opt_impl(fj_graph *g, int max_iters, double tol, double *mu_out,
     if (fabs(mu - prev) <= tol * mu) break;
     prev = mu;
   }
-  cudaFreeAsync(x, st);
-  cudaFreeAsync(y, st);
-  cudaFreeAsync(sums, st);
-  cudaFreeAsync(ctr, st);
   (void)partial;
   FJ_CUDA(cudaStreamSynchronize(st));
   if (mu > 1.0) mu = 1.0;

@@ -620,6 +620,19 @@ struct Staged {
   float *owned = nullptr;
 };
 
+// host data staged into a workspace buffer; device pointers pass through
+static fj_status stage_in(const float *src, int64_t n, Workspace &ws, Staged &out) {
+  if (is_device_ptr(src)) {
+    out.dev = src;
+    return FJ_OK;
+  }
+  float *d = nullptr;
+  FJ_CUDA(ws.alloc(&d, (size_t)n));
+  FJ_CUDA(cudaMemcpyAsync(d, src, sizeof(float) * n, cudaMemcpyHostToDevice, ws.st));
+  out.dev = d;
+  return FJ_OK;
+}
+
 static fj_status stage_in(const float *src, int64_t n, cudaStream_t st, Staged &out) {
   if (is_device_ptr(src)) {
     out.dev = src;
