@@ -161,7 +161,8 @@ struct Workspace {
 };
 
 // graph.cu
-fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **ocol, float **ow);
+fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **ocol, float **ow,
+                           int *err = nullptr);
 // layout.cu: sweep layout from the pull CSR (original ids)
 fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *ocol,
                                 const float *ow, const int32_t *color /* nullable */,

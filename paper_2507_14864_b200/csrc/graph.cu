@@ -2,13 +2,15 @@
 //
 // Steps (all on the graph's stream):
 //   1. stage the caller's in-CSR into library-owned device memory;
-//   2. validate row_ptr, columns, weights (FJ_ERR_INVALID on failure);
-//   3. canonicalise the in-CSR (rows sorted by column) with one radix sort of
-//      (v, u) keys; adjacent equal keys are duplicate arcs, u == v self-loops;
-//   4. transpose to the pull (out-) CSR with a second sort of (u, v) keys and
-//      reduce its rows to d_u = Σ_v a_uv in fp64 (reading R3);
-//   5. undirected input: check the arc set is symmetric with equal weights;
-//   6. build the sweep layout (layout.cu).
+//   2. validate row_ptr (FJ_ERR_INVALID on failure);
+//   3. transpose to the pull (out-) CSR with a stable radix sort on u; the
+//      same pass validates columns (range, self-loops), weights, and notes
+//      rows that are not strictly increasing;
+//   4. only then, canonicalise the in-CSR (rows sorted by column) with a radix
+//      sort of (v, u) keys; adjacent equal keys are duplicate arcs;
+//   5. d_u = Σ_v a_uv over the out-rows in fp64 (reading R3);
+//   6. undirected input: check the arc set is symmetric with equal weights;
+//   7. build the sweep layout (layout.cu).
 // Sorting and scans use CUB (toolkit library primitives); every kernel here
 // is a one-pass O(m) integer/fp64 kernel.
 #include <stdio.h>
@@ -42,31 +44,6 @@ __global__ void k_validate_rowptr(int64_t n, int64_t m, const int64_t *__restric
   if (x < 0 || x > m) atomicOr(err, 1);
 }
 
-// One warp per row of the caller's in-CSR: column range, self-loops, weight
-// validity, and whether the row is already strictly increasing (bit 64: not
-// canonical, the rows must be sorted).
-__global__ void k_check_rows(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                             const float *__restrict__ w, int *__restrict__ err) {
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
-  for (int64_t v = warp; v < n; v += nwarps) {
-    int bad = 0;
-    for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) {
-      const int32_t u = col[e];
-      if (u < 0 || u >= n) bad |= 2;
-      if (u == v) bad |= 4;
-      if (w) {
-        const float x = w[e];
-        if (!(x > 0.0f) || !isfinite(x)) bad |= 8;
-      }
-      if (e > rp[v] && col[e - 1] >= u) bad |= 64;
-    }
-    bad = __reduce_or_sync(0xffffffffu, bad);
-    if (lane == 0 && bad) atomicOr(err, bad);
-  }
-}
-
 // (v, u) keys of the in-CSR arcs (only when rows must be sorted)
 __global__ void k_in_keys(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                           int nb, uint64_t *__restrict__ keys) {
@@ -96,19 +73,35 @@ __global__ void k_unpack_sorted(int64_t m, int nb, const uint64_t *__restrict__ 
   if (w_dst) w_dst[i] = w_src[idx[i]];
 }
 
-// transpose inputs: key u, payload arc index; row of every arc
+// transpose inputs: key u, payload arc index; row of every arc.  With err
+// (graph create) the same pass validates the caller's columns — range (bit 2),
+// self-loop (4) and whether rows are strictly increasing (64: not canonical) —
+// so the input's columns are read once for both
 __global__ void k_out_keys(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                            uint32_t *__restrict__ key, uint32_t *__restrict__ idx,
-                           uint32_t *__restrict__ row) {
+                           uint32_t *__restrict__ row, int *__restrict__ err) {
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
-  for (int64_t v = warp; v < n; v += nwarps)
-    for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) {
-      key[e] = (uint32_t)col[e];
+  for (int64_t v = warp; v < n; v += nwarps) {
+    int bad = 0;
+    const int64_t b = rp[v], e1 = rp[v + 1];
+    for (int64_t e = b + lane; e < e1; e += 32) {
+      const int32_t u = col[e];
+      if (err) {
+        if (u < 0 || u >= n) bad |= 2;
+        if (u == v) bad |= 4;
+        if (e > b && col[e - 1] >= u) bad |= 64;
+      }
+      key[e] = (u >= 0 && u < n) ? (uint32_t)u : 0u;
       idx[e] = (uint32_t)e;
       row[e] = (uint32_t)v;
     }
+    if (err) {
+      bad = __reduce_or_sync(0xffffffffu, bad);
+      if (lane == 0 && bad) atomicOr(err, bad);
+    }
+  }
 }
 
 // row pointers of the out-CSR from the sorted keys (no atomics): ort[u] is
@@ -129,12 +122,16 @@ __global__ void k_bounds(int64_t n, int64_t m, const uint32_t *__restrict__ key,
 // out-CSR entries from the stably sorted arc indices (v ascending within u)
 __global__ void k_out_fill(int64_t m, const uint32_t *__restrict__ idx, const uint32_t *__restrict__ row,
                            const float *__restrict__ w, int32_t *__restrict__ ocol,
-                           float *__restrict__ ow) {
+                           float *__restrict__ ow, int *__restrict__ err) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= m) return;
   const uint32_t e = idx[k];
   ocol[k] = (int32_t)row[e];
-  if (ow) ow[k] = w[e];
+  if (ow) {
+    const float x = w[e];
+    ow[k] = x;
+    if (err && !(x > 0.0f && isfinite(x))) atomicOr(err, 8);  // weight validity
+  }
 }
 
 // d_u = Σ_v a_uv over the out-row u (warp per row, fixed lane order + fixed
@@ -196,7 +193,8 @@ static fj_status sort_pairs(K *&keys, K *&keys_alt, V *&val, V *&val_alt, int64_
 // Transpose the canonical in-CSR into the pull CSR (row u lists v with a_uv),
 // rows sorted: a stable radix sort on u alone keeps the v order of the
 // canonical input.  *ort, *ocol, *ow live in the caller's workspace `ws`.
-fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **ocol, float **ow) {
+fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **ocol, float **ow,
+                           int *err) {
   cudaStream_t st = g->stream;
   const int64_t n = g->n, m = g->m;
   Workspace tmp(st);  // sort keys and payloads
@@ -211,11 +209,11 @@ fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **
   *ow = nullptr;
   if (g->in_w) FJ_CUDA(ws.alloc(ow, (size_t)m + 8));
   fj::count_launch();
-  k_out_keys<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, k0, i0, row);
+  k_out_keys<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, k0, i0, row, err);
   FJ_TRY(sort_pairs(k0, k1, i0, i1, m, bits_for(n), tmp));
   if (m > 0) {
     fj::count_launch();
-    k_out_fill<<<grid_for(m), kBlock, 0, st>>>(m, i0, row, g->in_w, *ocol, *ow);
+    k_out_fill<<<grid_for(m), kBlock, 0, st>>>(m, i0, row, g->in_w, *ocol, *ow, err);
   }
   fj::count_launch();
   k_bounds<<<grid_for(n + 1), kBlock, 0, st>>>(n, m, k0, *ort);
@@ -286,13 +284,21 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
     set_error("fj_graph_create: in_row_ptr must start at 0, be non-decreasing and end at nnz");
     return FJ_ERR_INVALID;
   }
-  fj::count_launch();
-  k_check_rows<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, g->in_w, err);
+  mark("validate row_ptr");
+
+  // 3. pull CSR; the transpose pass also validates columns and weights.  Its
+  // result does not depend on the order inside the caller's rows (stable sort
+  // on u with the arc index as payload), so unsorted input only needs the
+  // in-CSR itself canonicalised below
+  int64_t *ort = nullptr;
+  int32_t *ocol = nullptr;
+  float *ow = nullptr;
+  FJ_TRY(transpose_in_csr(g, ws, &ort, &ocol, &ow, err));
   FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
-  mark("validate");
+  mark("transpose + validate");
 
-  // 3. canonical in-CSR: sort rows only if some row is not strictly increasing
+  // 4. canonical in-CSR: sort rows only if some row is not strictly increasing
   if ((herr & ~64) == 0 && (herr & 64)) {
     uint64_t *k0 = nullptr, *k1 = nullptr;
     uint32_t *i0 = nullptr, *i1 = nullptr;
@@ -330,17 +336,13 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
     return FJ_ERR_INVALID;
   }
 
-  // 4. pull CSR + degrees
-  int64_t *ort = nullptr;
-  int32_t *ocol = nullptr;
-  float *ow = nullptr;
-  FJ_TRY(transpose_in_csr(g, ws, &ort, &ocol, &ow));
+  // 5. degrees
   FJ_CUDA(cudaMallocAsync(&g->deg, sizeof(double) * n, st));
   fj::count_launch();
   k_row_sums<<<grid_warps(n), kBlock, 0, st>>>(n, ort, ow, g->deg);
-  mark("transpose + degrees");
+  mark("degrees");
 
-  // 5. symmetry of undirected input
+  // 6. symmetry of undirected input
   if (!g->directed && m > 0) {
     fj::count_launch();
     k_neq<int64_t><<<grid_for(n + 1), kBlock, 0, st>>>(n + 1, ort, g->in_rp, err, 32);
@@ -359,7 +361,7 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
     mark("symmetry check");
   }
 
-  // 6. sweep layout (1 color)
+  // 7. sweep layout (1 color)
   fj_status s = build_layout_from_out(g, ort, ocol, ow, nullptr, 1, &g->async_layout);
   if (s != FJ_OK) return s;
   FJ_CUDA(cudaStreamSynchronize(st));
