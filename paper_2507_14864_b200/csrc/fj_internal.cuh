@@ -122,6 +122,7 @@ struct fj_graph {
   int ncolors = 0;           // phases of a colored sweep (tail merged)
   int ncolors_raw = 0;       // colors of the distance-1 coloring before the merge
   int tail_color = -1;       // merged tail phase (−1: none)
+  cudaEvent_t w_ready = nullptr;  // during create only: host weights staged on a side stream
 };
 
 namespace fj {

@@ -212,6 +212,7 @@ fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **
   k_out_keys<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, k0, i0, row, err);
   FJ_TRY(sort_pairs(k0, k1, i0, i1, m, bits_for(n), tmp));
   if (m > 0) {
+    if (g->w_ready) FJ_CUDA(cudaStreamWaitEvent(st, g->w_ready, 0));  // weights staged
     fj::count_launch();
     k_out_fill<<<grid_for(m), kBlock, 0, st>>>(m, i0, row, g->in_w, *ocol, *ow, err);
   }
@@ -264,9 +265,35 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
   if (w_in) FJ_CUDA(cudaMallocAsync(&g->in_w, sizeof(float) * (m + 8), st));
   mark("alloc");
   FJ_CUDA(cudaMemcpyAsync(g->in_rp, rp_in, sizeof(int64_t) * (n + 1), cudaMemcpyDefault, st));
+  // host weights travel on a side stream: the copy engine moves them while the
+  // column checks, keys and sort of the transpose run (it waits only before
+  // the weights are first read)
+  cudaStream_t wst = nullptr;
+  struct SideStream {
+    cudaStream_t &s;
+    cudaEvent_t &e;
+    ~SideStream() {  // also on early error returns: the copy must not outlive in_w
+      if (s) cudaStreamSynchronize(s);
+      if (e) cudaEventDestroy(e);
+      if (s) cudaStreamDestroy(s);
+      e = nullptr;
+    }
+  } side{wst, g->w_ready};
   if (m > 0) {
     FJ_CUDA(cudaMemcpyAsync(g->in_col, col_in, sizeof(int32_t) * m, cudaMemcpyDefault, st));
-    if (w_in) FJ_CUDA(cudaMemcpyAsync(g->in_w, w_in, sizeof(float) * m, cudaMemcpyDefault, st));
+    if (w_in && !is_device_ptr(w_in)) {
+      FJ_CUDA(cudaStreamCreateWithFlags(&wst, cudaStreamNonBlocking));
+      FJ_CUDA(cudaEventCreateWithFlags(&g->w_ready, cudaEventDisableTiming));
+      cudaEvent_t staged;  // the buffer exists on st before the side copy starts
+      FJ_CUDA(cudaEventCreateWithFlags(&staged, cudaEventDisableTiming));
+      FJ_CUDA(cudaEventRecord(staged, st));
+      FJ_CUDA(cudaStreamWaitEvent(wst, staged, 0));
+      cudaEventDestroy(staged);
+      FJ_CUDA(cudaMemcpyAsync(g->in_w, w_in, sizeof(float) * m, cudaMemcpyDefault, wst));
+      FJ_CUDA(cudaEventRecord(g->w_ready, wst));
+    } else if (w_in) {
+      FJ_CUDA(cudaMemcpyAsync(g->in_w, w_in, sizeof(float) * m, cudaMemcpyDefault, st));
+    }
   }
   mark("stage");
 
