@@ -1,4 +1,9 @@
 """Active-set tail (k_sweep_tail) settings on full configs (diagnostics).
+
+The kernel this drove (FJ_TAIL_EU / FJ_TAIL_INNER) was measured and removed
+(DESIGN.md §8 tuning log, profiles/r01_sweep_profile.txt); kept as the record
+of the experiment.  Against the current library every setting runs the same
+code.
 usage: python tools/tail_ab.py CID [CID ...]"""
 import os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
