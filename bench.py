@@ -288,6 +288,24 @@ def run_ours(args, prob, world, rank, local):
                        "one fp64 gathered per arc; frac = probe / sweep time (1 = at the gather "
                        "ceiling)"}
 
+    # f2: the same graph with k = 4 opinion vectors in one batched solve
+    batched = None
+    if not args.no_sweep:
+        import fjgen
+        g = fj.Graph(prob.n, rp, col, w, directed=prob.directed)
+        cols = [prob.s, fjgen.exponential(prob.n, 21), fjgen.pareto(prob.n, 22),
+                fjgen.uniform(prob.n, 23)]
+        S = torch.from_numpy(np.ascontiguousarray(np.stack(cols, 1).astype(np.float32)).ravel()).to(dev)
+        Z = torch.empty(prob.n * 4, dtype=torch.float32, device=dev)
+        fj.solve_batch(g, S, Z, 4, args.eps, args.omega)
+        stb = fj.solve_batch(g, S, Z, 4, args.eps, args.omega)
+        g.close()
+        batched = {"k": 4, "opinions": "Beta(2,5), Exp, Pareto, U[0,1]",
+                   "time_to_eps_s": stb.solve_ms / 1e3, "sweeps": stb.sweeps,
+                   "edge_updates": stb.edge_updates,
+                   "edge_updates_per_s": stb.edge_updates / (stb.solve_ms / 1e3),
+                   "cert_ratio": stb.cert_ratio}
+
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, prob, fj, torch, dev, stream, world)
@@ -312,6 +330,7 @@ def run_ours(args, prob, world, rank, local):
                          "kernel": "k_sweep (persistent)",
                          "algorithmic_bytes_per_launch": ab},
             "gather_ceiling": ceiling,
+            "batched": batched,
             "omega_sweep": omega_table,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
