@@ -249,6 +249,24 @@ def test_tail_merge_complete_graph(dev, monkeypatch, omega):
     g.close()
 
 
+@pytest.mark.parametrize("knob", ["FJ_TMA", "FJ_ASYNC_FREE", "FJ_DYN", "FJ_SYMM", "FJ_MIX"])
+@pytest.mark.parametrize("name", ["rmat12w", "chunglu4k", "lattice64"])
+def test_diagnostic_schedules(dev, monkeypatch, knob, name):
+    """The opt-in sweep variants of the tuning log (TMA-staged stream,
+    barrier-free epochs, dynamic claims, symmetric order, forced interleave)
+    stay correct: certified and equal to the oracle's z."""
+    monkeypatch.setenv(knob, "1")
+    rp, col, w, s, directed = TINY[name]()
+    check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async")
+
+
+def test_small_hub_pieces(dev, monkeypatch):
+    """FJ_PIECE: hub rows split into many 64-arc pieces (the combine path)."""
+    monkeypatch.setenv("FJ_PIECE", "64")
+    rp, col, w, s, directed = TINY["rmat12w"]()
+    check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async")
+
+
 def test_gather_probe(dev):
     """fj_gather_probe runs on the layout and reports a positive time."""
     rp, col, w, s, directed = TINY["rmat12w"]()
