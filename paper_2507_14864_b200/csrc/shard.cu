@@ -45,6 +45,10 @@ __global__ void k_meas_nodes1(int64_t n, const int32_t *__restrict__ perm,
 struct fj_comm {
   int world = 1, rank = 0;
   bool local = true;
+  // in-process transport that runs the NCCL path's bookkeeping (send lists,
+  // pack kernel, per-peer segments) with device copies in place of
+  // ncclSend/ncclRecv: FJ_LOOPBACK=1 at fj_comm_create_local (tests)
+  bool loopback = false;
   ncclComm_t nc = nullptr;
   cudaStream_t stream = nullptr;
   int num_sms = 0;
@@ -379,6 +383,29 @@ static fj_status exchange(fj_shard **sh, int count, double **buf) {
     FJ_NCCL(nccl()->GroupEnd());
     return FJ_OK;
   }
+  if (cm->loopback) {  // the NCCL path with copies: pack on every rank, then move
+    for (int q = 0; q < count; q++) {
+      const int64_t ns = sh[q]->soff[W];
+      if (ns > 0) {
+        count_launch();
+        k_halo_gather<<<gridn(ns), kBlock, 0, st>>>(ns, sh[q]->sendidx, buf[q], sh[q]->sendbuf);
+      }
+    }
+    for (int r = 0; r < count; r++)
+      for (int j = 0; j + 1 < W; j++) {
+        const int q = (r + 1 + j) % W;
+        const int64_t c = sh[r]->hoff[j + 1] - sh[r]->hoff[j];
+        if (c == 0) continue;
+        if (sh[q]->soff[r + 1] - sh[q]->soff[r] != c) {
+          set_error("fj_shard: loopback send/receive counts disagree (%d -> %d)", q, r);
+          return FJ_ERR_CUDA;
+        }
+        FJ_CUDA(cudaMemcpyAsync(buf[r] + sh[r]->n_local + sh[r]->hoff[j],
+                                sh[q]->sendbuf + sh[q]->soff[r], sizeof(double) * c,
+                                cudaMemcpyDeviceToDevice, st));
+      }
+    return FJ_OK;
+  }
   for (int r = 0; r < count; r++)
     for (int j = 0; j + 1 < W; j++) {
       const int q = (r + 1 + j) % W;
@@ -566,34 +593,54 @@ static fj_status connect_impl(fj_shard **sh, int count) {
     S->nz = S->n_local + nu;
     for (int j = 0; j + 1 < W; j++) need_from[i][(S->rank + 1 + j) % W] = S->hoff[j + 1] - S->hoff[j];
   }
-  // NCCL: every rank learns what each peer reads from it (its send lists)
-  if (!cm->local && W > 1) {
-    fj_shard *me = sh[0];
-    int64_t *cnt = nullptr;
-    FJ_CUDA(ws.alloc(&cnt, W * (W + 1)));
-    FJ_CUDA(cudaMemcpyAsync(cnt + (int64_t)W * W, need_from[0].data(), sizeof(int64_t) * W,
-                            cudaMemcpyHostToDevice, st));
-    FJ_NCCL(nccl()->AllGather(cnt + (int64_t)W * W, cnt, (size_t)W, ncclInt64, cm->nc, st));
-    std::vector<int64_t> hc((size_t)W * W);  // hc[q·W + r]: what q reads from r
-    FJ_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int64_t) * W * W, cudaMemcpyDeviceToHost, st));
-    FJ_CUDA(cudaStreamSynchronize(st));
-    me->soff.assign(W + 1, 0);
-    for (int q = 0; q < W; q++)
-      me->soff[q + 1] = me->soff[q] + (q == me->rank ? 0 : hc[(size_t)q * W + me->rank]);
-    const int64_t ns = me->soff[W];
-    FJ_CUDA(cudaMallocAsync(&me->sendidx, sizeof(int32_t) * std::max<int64_t>(1, ns), st));
-    FJ_CUDA(cudaMallocAsync(&me->sendbuf, sizeof(double) * std::max<int64_t>(1, ns), st));
-    FJ_NCCL(nccl()->GroupStart());
-    for (int q = 0; q < W; q++) {
-      if (q == me->rank) continue;
-      const int j = (q - me->rank - 1 + W) % W;
-      const int64_t rc = me->hoff[j + 1] - me->hoff[j], sc = me->soff[q + 1] - me->soff[q];
-      if (rc > 0)
-        FJ_NCCL(nccl()->Send(me->need + me->hoff[j], (size_t)rc, ncclInt32, q, cm->nc, st));
-      if (sc > 0)
-        FJ_NCCL(nccl()->Recv(me->sendidx + me->soff[q], (size_t)sc, ncclInt32, q, cm->nc, st));
+  // NCCL (and loopback): every rank learns what each peer reads from it — its
+  // send lists; hc[q·W + r] = how many values rank q reads from rank r
+  if ((!cm->local || cm->loopback) && W > 1) {
+    std::vector<int64_t> hc((size_t)W * W, 0);
+    if (!cm->local) {
+      int64_t *cnt = nullptr;
+      FJ_CUDA(ws.alloc(&cnt, W * (W + 1)));
+      FJ_CUDA(cudaMemcpyAsync(cnt + (int64_t)W * W, need_from[0].data(), sizeof(int64_t) * W,
+                              cudaMemcpyHostToDevice, st));
+      FJ_NCCL(nccl()->AllGather(cnt + (int64_t)W * W, cnt, (size_t)W, ncclInt64, cm->nc, st));
+      FJ_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int64_t) * W * W, cudaMemcpyDeviceToHost, st));
+      FJ_CUDA(cudaStreamSynchronize(st));
+    } else {
+      for (int i = 0; i < count; i++)
+        for (int q = 0; q < W; q++) hc[(size_t)i * W + q] = need_from[i][q];
     }
-    FJ_NCCL(nccl()->GroupEnd());
+    for (int i = 0; i < count; i++) {
+      fj_shard *me = sh[i];
+      me->soff.assign(W + 1, 0);
+      for (int q = 0; q < W; q++)
+        me->soff[q + 1] = me->soff[q] + (q == me->rank ? 0 : hc[(size_t)q * W + me->rank]);
+      const int64_t ns = me->soff[W];
+      FJ_CUDA(cudaMallocAsync(&me->sendidx, sizeof(int32_t) * std::max<int64_t>(1, ns), st));
+      FJ_CUDA(cudaMallocAsync(&me->sendbuf, sizeof(double) * std::max<int64_t>(1, ns), st));
+    }
+    if (!cm->local) {
+      fj_shard *me = sh[0];
+      FJ_NCCL(nccl()->GroupStart());
+      for (int q = 0; q < W; q++) {
+        if (q == me->rank) continue;
+        const int j = (q - me->rank - 1 + W) % W;
+        const int64_t rc = me->hoff[j + 1] - me->hoff[j], sc = me->soff[q + 1] - me->soff[q];
+        if (rc > 0)
+          FJ_NCCL(nccl()->Send(me->need + me->hoff[j], (size_t)rc, ncclInt32, q, cm->nc, st));
+        if (sc > 0)
+          FJ_NCCL(nccl()->Recv(me->sendidx + me->soff[q], (size_t)sc, ncclInt32, q, cm->nc, st));
+      }
+      FJ_NCCL(nccl()->GroupEnd());
+    } else {  // loopback: reader r's need list for q becomes q's send list for r
+      for (int r = 0; r < count; r++)
+        for (int j = 0; j + 1 < W; j++) {
+          const int q = (r + 1 + j) % W;
+          const int64_t rc = sh[r]->hoff[j + 1] - sh[r]->hoff[j];
+          if (rc > 0)
+            FJ_CUDA(cudaMemcpyAsync(sh[q]->sendidx + sh[q]->soff[r], sh[r]->need + sh[r]->hoff[j],
+                                    sizeof(int32_t) * rc, cudaMemcpyDeviceToDevice, st));
+        }
+    }
   }
   FJ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
@@ -999,6 +1046,7 @@ fj_status fj_comm_create_local(int world, fj_comm_t *out) {
   fj_comm *c = new fj_comm();
   c->world = world;
   c->local = true;
+  c->loopback = getenv("FJ_LOOPBACK") && atoi(getenv("FJ_LOOPBACK"));
   fj_status s = comm_base(c);
   if (s != FJ_OK) {
     fj_comm_destroy(c);
