@@ -136,6 +136,18 @@ def max_over_ranks(value: float, world: int, device=None) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(value: float, world: int, device=None) -> float:
+    """Sum of `value` over all ranks (work units every rank processed)."""
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64,
+                     device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def config_dict(prob, args, extra=None):
     d = {"workload": f"config{args.config}:{prob.name}", "n": prob.n, "m": prob.m,
          "eps": args.eps, "omega": args.omega, "directed": prob.directed,
@@ -258,7 +270,7 @@ def run_ours(args, prob, world, rank, local):
     launches = fj.lib().fj_kernel_launches() - launches0
     ms = max_over_ranks(ev0.elapsed_time(ev1), world, dev)
     eu_rank = sum(st.edge_updates for st, _ in stats)
-    value = eu_rank * world / (ms / 1e3)
+    value = sum_over_ranks(eu_rank, world, dev) / (ms / 1e3)
     st0, m0 = stats[-1]
     solve_ms = statistics.median(st.solve_ms for st, _ in stats)
     sweep_ms = statistics.median(st.sweep_ms for st, _ in stats)
@@ -485,7 +497,9 @@ def run_e2e(args, prob, fj, torch, dev, stream, world):
     h2d = prob.row_ptr.nbytes + prob.col.nbytes + (0 if prob.w is None else prob.w.nbytes) + \
         prob.s.nbytes
     d2h = 4 * prob.n + 32
-    return {"value": eu * world / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+    dt = max_over_ranks(dt, world, dev)
+    return {"value": sum_over_ranks(eu, world, dev) / dt, "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": k,
             "note": "wall clock around blocking C-ABI calls with pinned host buffers"}
 
