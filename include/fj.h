@@ -210,8 +210,9 @@ fj_status fj_measures_ex(fj_graph_t g, const float *z, const float *s, fj_measur
  * (I+L)z = s (Lemma 1) reads a_uv along u's OUT-arcs u→v — and the
  * estimate ẑ_u.  Every sweep each rank relaxes its own rows exactly as
  * fj_solve's ASYNC schedule does (|r_u| > h_u), reading the other
- * ranks' ẑ from the last exchange; then the ranks exchange their ẑ segments
- * and reduce (relaxations, divergence flag).  A sweep in which no rank
+ * ranks' ẑ from the last exchange; then every rank receives the current ẑ of
+ * exactly the remote nodes its rows read (its halo) and the ranks reduce
+ * (relaxations, divergence flag).  A sweep in which no rank
  * relaxes anything read only final values, so the loop ends on the paper's
  * rule (Q = ∅) exactly as on one GPU; the fp64 certificate (Lemma 3,
  * P:231) then runs on every rank and its maximum decides, with the same
@@ -221,7 +222,7 @@ fj_status fj_measures_ex(fj_graph_t g, const float *z, const float *s, fj_measur
  * the certificate decide.
  *
  * Transport (fj_comm): NCCL (one rank per process and GPU; ranks exchange
- * segments with grouped ncclSend/ncclRecv and reduce with ncclAllReduce over
+ * halos with grouped ncclSend/ncclRecv and reduce with ncclAllReduce over
  * NVLink/NVSwitch; libnccl.so.2 is loaded on first use), or an in-process
  * transport that holds all `world` shards of one process on the current
  * device and exchanges with device copies (single-GPU use and tests).
