@@ -13,7 +13,9 @@
 //        ẑ_v ← ẑ_v + ω r_v / (1 + d_v)                      (equ:sor1)
 // ASYNC: one phase per sweep, rows updated in place (later rows see earlier
 // updates, as in Gauss–Seidel).  COLORED: one phase per color; rows of one
-// color share no arc, so each phase equals sequential SOR over that color.
+// color share no arc, so each phase equals sequential SOR over that color
+// (the tiny tail colors of power-law graphs are merged into one asynchronous
+// phase with a per-row bound on ω, reading R23, color.cu).
 // The loop ends on the first sweep that relaxes nothing: every residual was
 // then evaluated on the final ẑ and is ≤ h — the paper's "Q = ∅".
 // A separate compensated fp64 pass (certificate) re-checks max |r_v|/h_v.
