@@ -2,7 +2,7 @@
 sweeps for several FJ_TAIL_FRAC settings against ASYNC ω = 1 (diagnostics).
 
 usage: python tools/tail_exp.py CID [CID ...]
-env: TAIL_FRACS (comma list, default 0,0.002,0.01,0.03), FJ_TAIL_OMEGA passes through
+env: TAIL_FRACS (comma list, default 0,0.002,0.01,0.03)
 """
 import os, sys, subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -31,5 +31,5 @@ for cid in sys.argv[1:]:
         oms = "1.0,1.2,1.4,1.6" if frac == "0" else "1.2,1.4,1.6"
         out = subprocess.run([sys.executable, "-c", code, cid, eps, oms], env=env,
                              capture_output=True, text=True, timeout=900)
-        print(f"config {cid} FJ_TAIL_FRAC={frac} FJ_TAIL_OMEGA={os.environ.get('FJ_TAIL_OMEGA', '1')}", flush=True)
+        print(f"config {cid} FJ_TAIL_FRAC={frac}", flush=True)
         print(out.stdout.rstrip(), out.stderr[-400:] if out.returncode else "", flush=True)
