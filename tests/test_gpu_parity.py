@@ -267,6 +267,25 @@ def test_small_hub_pieces(dev, monkeypatch):
     check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async")
 
 
+@pytest.mark.parametrize("name", ["er2000", "rmat12w", "lattice64"])
+@pytest.mark.parametrize("eps", [1e-2, 1e-4])
+def test_accuracy_protocol(dev, name, eps):
+    """The paper's accuracy protocol (tab:measure_li): against the exact
+    z of a dense solve, the maximum relative opinion error stays within ε
+    (with σ, reading R5) and every measure's relative error within 2ε."""
+    rp, col, w, s, directed = TINY[name]()
+    zref = oracle.dense_solve(rp, col, w, s)
+    mref = oracle.measures(rp, col, w, zref, directed=directed, s=np.asarray(s, np.float64))
+    for omega in (1.0, 1.3 if not directed else 1.2):
+        g, z, zp, st = gpu_solve(dev, rp, col, w, s, eps, omega, directed)
+        m = fj.measures(g, torch.from_numpy(z.astype(np.float32)).to(dev),
+                        torch.from_numpy(np.asarray(s, np.float32)).to(dev))
+        g.close()
+        assert np.max(np.abs(z - zref) / np.maximum(np.abs(zref), SIG)) <= eps
+        for k in "CDIP":
+            assert abs(m[k] - mref[k]) <= 2 * eps * abs(mref[k]) + 1e-12, (k, m[k], mref[k])
+
+
 def test_gather_probe(dev):
     """fj_gather_probe runs on the layout and reports a positive time."""
     rp, col, w, s, directed = TINY["rmat12w"]()
