@@ -72,10 +72,18 @@ CASES = list(range(1, 301))
 
 
 @pytest.mark.parametrize("seed", CASES)
-def test_fuzz_case(dev, seed):
+def test_fuzz_case(dev, monkeypatch, seed):
     fam, rp, col, w, s, directed, eps, rng = draw(seed)
     n = len(rp) - 1
     sched = ["async", "colored", "push", "batch", "sharded"][(seed // 5) % 5]
+    # opt-in paths ride along: the loopback transport (the NCCL path's
+    # bookkeeping) for half the sharded cases, the compacted frontier for half
+    # the PUSH cases
+    if sched == "sharded" and seed % 2:
+        monkeypatch.setenv("FJ_LOOPBACK", "1")
+    if sched == "push" and seed % 2:
+        monkeypatch.setenv("FJ_PUSH_COMPACT", "1")
+        monkeypatch.setenv("FJ_PUSH_SPARSE_DIV", str(int(rng.integers(1, 64))))
     omega = 1.0 if sched in ("batch", "sharded") or rng.random() < 0.4 else \
         float(rng.uniform(1.05, 1.9))
     ref = oracle.solve(rp, col, w, s, eps, 1.0)
