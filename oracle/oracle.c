@@ -7,7 +7,7 @@
  * (paper_2507_14864_b200/) and does not import it.
  *
  * Citations: P:n = /root/reference/PAPER.md line n (section / equation /
- * algorithm named beside it); readings R1..R19 are listed in DESIGN.md §3.
+ * algorithm named beside it); readings R1..R23 are listed in DESIGN.md §2.
  *
  * Graph input is the C-ABI in-CSR (reading R1/R2): row v lists the u with an
  * arc u→v (u listens to v) and weight a_uv (NULL = unit weights).

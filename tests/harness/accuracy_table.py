@@ -10,7 +10,7 @@ reference is independent of the GPU path: a sparse direct solve of
 solve (CG for undirected, BiCGSTAB for directed, relative residual 1e-13)
 for the larger ones, with the measures of that z computed by the oracle.
 
-usage: python tools/accuracy_table.py [CID ...]   (default 1 2 5)
+usage: python tests/harness/accuracy_table.py [CID ...]   (default 1 2 5)
 """
 import json
 import os
@@ -22,7 +22,7 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import fjgen  # noqa: E402
 import oracle  # noqa: E402

@@ -1,8 +1,8 @@
 """Time the oracle (paper's FIFO ImprovedBLISOR, fp64, one host core) at a given
 ω on full configs — the CPU baseline SURVEY §8(d) asks for at the best ω.
-usage: python tools/oracle_sor_time.py CID:OMEGA [CID:OMEGA ...]"""
+usage: python tests/harness/oracle_sor_time.py CID:OMEGA [CID:OMEGA ...]"""
 import json, os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import fjgen  # noqa: E402
 import oracle  # noqa: E402
 for arg in sys.argv[1:]:

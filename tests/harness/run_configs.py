@@ -4,7 +4,7 @@ GPU, for a list of ω and methods, and record per-solve stats.  With --certify
 the oracle's compensated fp64 certificate (oracle/, test infrastructure) is
 applied to every GPU ẑ' and the oracle measures are computed on the GPU z.
 
-    python tools/run_configs.py --configs 1,2,3,4,5 --certify --out gpurun_out/configs.jsonl
+    python tests/harness/run_configs.py --configs 1,2,3,4,5 --certify --out gpurun_out/configs.jsonl
 """
 from __future__ import annotations
 
@@ -14,7 +14,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
