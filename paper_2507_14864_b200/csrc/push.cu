@@ -170,46 +170,17 @@ __global__ void __launch_bounds__(kBlock, 4) k_push(PP p) {
       }
       grid_sync(p.bar);
     }
-    unsigned long long u = t.upd, e = t.eu, b = t.bad;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      u += __shfl_xor_sync(0xffffffffu, u, off);
-      e += __shfl_xor_sync(0xffffffffu, e, off);
-      b |= __shfl_xor_sync(0xffffffffu, b, off);
-    }
-    SweepCounters *c = p.cnt + sw % 3;
-    if (lane == 0 && (u | e | b)) {
-      atomicAdd(&c->upd, u);
-      atomicAdd(&c->eu, e);
-      if (b) atomicOr(&c->bad, b);
-    }
-    t.upd = t.eu = t.bad = 0;
-    grid_sync(p.bar);
-    if (threadIdx.x == 0) {
-      s_dec[0] = __ldcg(&c->upd);
-      s_dec[1] = __ldcg(&c->eu);
-      s_dec[2] = __ldcg(&c->bad);
-      if (blockIdx.x == 0) {
-        SweepCounters *zc = p.cnt + (sw + 2) % 3;
-        zc->upd = zc->eu = zc->bad = 0;
-      }
-    }
-    __syncthreads();
-    tot_upd += s_dec[0];
-    tot_eu += s_dec[1];
-    last_upd = s_dec[0];
+    unsigned long long dec[3];
+    sweep_totals(p.cnt, p.bar, sw, t, s_dec, dec);
+    tot_upd += dec[0];
+    tot_eu += dec[1];
+    last_upd = dec[0];
     sweeps = sw + 1;
-    const bool bad = s_dec[2] != 0, done = s_dec[0] == 0;
-    __syncthreads();
+    const bool bad = dec[2] != 0, done = dec[0] == 0;
     if (bad) { reason = 2; break; }
     if (done) { reason = 0; break; }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    p.out[0] = (unsigned long long)sweeps;
-    p.out[1] = tot_upd;
-    p.out[2] = tot_eu;
-    p.out[3] = (unsigned long long)reason;
-  }
+  sweep_result(p.out, sweeps, tot_upd, tot_eu, reason);
 }
 
 // push-layout init: s in push order, ẑ' = 0, r = s' (Alg. 1 init)

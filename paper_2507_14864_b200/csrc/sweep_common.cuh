@@ -472,6 +472,57 @@ __device__ __forceinline__ void grid_sync(unsigned *bar) {
   __syncthreads();
 }
 
+// End of a sweep: every thread's (relaxations, edge updates, sentinel flag)
+// go into the ring slot of sweep `sw` by warp-aggregated atomics; one grid
+// barrier; then every thread of every block reads the grid totals into dec.
+// The slot two sweeps ahead is cleared for reuse (3-slot ring: no second
+// barrier needed between reading a slot and clearing it).
+__device__ __forceinline__ void sweep_totals(SweepCounters *cnt, unsigned *bar, int sw, TAcc &t,
+                                             unsigned long long *s_dec,
+                                             unsigned long long (&dec)[3]) {
+  unsigned long long u = t.upd, e = t.eu, b = t.bad;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    u += __shfl_xor_sync(0xffffffffu, u, off);
+    e += __shfl_xor_sync(0xffffffffu, e, off);
+    b |= __shfl_xor_sync(0xffffffffu, b, off);
+  }
+  SweepCounters *c = cnt + sw % 3;
+  if ((threadIdx.x & 31) == 0 && (u | e | b)) {
+    atomicAdd(&c->upd, u);
+    atomicAdd(&c->eu, e);
+    if (b) atomicOr(&c->bad, b);
+  }
+  t.upd = t.eu = t.bad = 0;
+  grid_sync(bar);
+  if (threadIdx.x == 0) {
+    s_dec[0] = __ldcg(&c->upd);
+    s_dec[1] = __ldcg(&c->eu);
+    s_dec[2] = __ldcg(&c->bad);
+    if (blockIdx.x == 0) {
+      SweepCounters *zc = cnt + (sw + 2) % 3;
+      zc->upd = zc->eu = zc->bad = 0;
+    }
+  }
+  __syncthreads();
+  dec[0] = s_dec[0];
+  dec[1] = s_dec[1];
+  dec[2] = s_dec[2];
+  __syncthreads();
+}
+
+// the loop's outcome for the host: sweeps, relaxations, edge updates, reason
+__device__ __forceinline__ void sweep_result(unsigned long long *out, int sweeps,
+                                             unsigned long long upd, unsigned long long eu,
+                                             int reason) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[0] = (unsigned long long)sweeps;
+    out[1] = upd;
+    out[2] = eu;
+    out[3] = (unsigned long long)reason;
+  }
+}
+
 #ifndef FJ_MINB
 #define FJ_MINB 4
 #endif
