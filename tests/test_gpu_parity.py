@@ -260,6 +260,19 @@ def test_diagnostic_schedules(dev, monkeypatch, knob, name):
     check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async")
 
 
+@pytest.mark.parametrize("coloring", ["spec", "jp"])
+@pytest.mark.parametrize("name", ["chunglu4k", "rmat12w"])
+def test_colorings(dev, monkeypatch, coloring, name):
+    """Both colorings (default speculative largest-first, FJ_COLORING=jp) give
+    valid colored solves; the colors are a proper coloring (checked through the
+    sequential-SOR parity of the COLORED schedule without the tail merge)."""
+    monkeypatch.setenv("FJ_COLORING", coloring)
+    monkeypatch.setenv("FJ_TAIL_FRAC", "0")
+    rp, col, w, s, directed = TINY[name]()
+    check_parity(dev, rp, col, w, s, 1e-6, 1.3, directed, method="colored",
+                 ref_omega=1.0 if directed else None)
+
+
 def test_small_hub_pieces(dev, monkeypatch):
     """FJ_PIECE: hub rows split into many 64-arc pieces (the combine path)."""
     monkeypatch.setenv("FJ_PIECE", "64")
