@@ -75,6 +75,7 @@ struct KP {
   int dyn;                       // dynamic work claiming in k_sweep (env FJ_DYN)
   int symm;                      // alternate sweep direction (env FJ_SYMM)
   const unsigned long long *stop;  // sharded solve: nonzero = the loop has ended (k_sweep)
+  int64_t empty0, empty1;  // rows with no arcs (the layout's last group): CERT covers them too
 };
 
 // CSR streams are read once per sweep: read-only path, no L1 allocation, so
@@ -594,6 +595,13 @@ __global__ void __launch_bounds__(kBlock, 4) k_pass(KP p) {
   for (int ti = blockIdx.x; ti < p.ntasks_all; ti += gridDim.x)
     dispatch_tile<MODE, W>(p, S, p.tasks[ti], t);
   if constexpr (MODE == CERT) {
+    // rows without arcs: r = s' − ẑ' (exactly 0 after the pull solvers' init,
+    // R20; PUSH relaxes them like any other row, so they are certified too)
+    for (int64_t row = p.empty0 + blockIdx.x * (int64_t)kBlock + threadIdx.x; row < p.empty1;
+         row += (int64_t)gridDim.x * kBlock)
+      cert_row<W>(p, S, (int)row, 0, dd{0.0, 0.0}, t);
+  }
+  if constexpr (MODE == CERT) {
     double m = t.certmax;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
@@ -714,6 +722,8 @@ static KP make_kp(const fj_graph *g, const Layout &L) {
   p.tail_beta = L.tail_beta;
   p.ntasks_all = L.ntasks;
   p.nwtasks_all = L.nwtasks;
+  p.empty0 = L.n - L.empty_rows;
+  p.empty1 = L.n;
   return p;
 }
 

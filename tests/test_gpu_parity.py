@@ -273,6 +273,37 @@ def test_colorings(dev, monkeypatch, coloring, name):
                  ref_omega=1.0 if directed else None)
 
 
+@pytest.mark.parametrize("compact", ["0", "1"])
+@pytest.mark.parametrize("omega", [1.0, 1.197, 1.6])
+def test_push_certifies_rows_without_arcs(dev, monkeypatch, compact, omega):
+    """Rows with d_v = 0 are exact after the pull solvers' init (R20) but PUSH
+    relaxes them like any other row, so the certificate (and the residual it
+    hands back on a resume) must cover them: the GPU ratio is at least the
+    oracle's ratio over those rows, and the result meets the ε bound.  (A
+    directed R-MAT graph with isolated nodes and sinks.)"""
+    monkeypatch.setenv("FJ_PUSH_COMPACT", compact)
+    monkeypatch.setenv("FJ_PUSH_SPARSE_DIV", "15")
+    rp, col = fjgen.rmat_graph(11, 8, 161)
+    n = len(rp) - 1
+    s = fjgen.uniform(n, 161)
+    eps = 6e-7
+    d = oracle.degrees(rp, col, None)
+    E = np.nonzero(d == 0)[0]
+    assert len(E) > 0
+    ref = oracle.solve(rp, col, None, s, eps, 1.0)
+    g = fj.Graph(n, rp, col, None, directed=True)
+    for rep in range(3):
+        z = np.empty(n, np.float32)
+        zp = np.empty(n, np.float64)
+        st = fj.solve(g, s, z, eps, omega, method="push", zprime_out=zp)
+        ratio, R = oracle.certificate(rp, col, None, s, zp, eps)
+        _, h, _, _ = oracle.thresholds(s, eps)
+        assert ratio <= 1.0 and st.cert_ratio <= 1.0
+        assert st.cert_ratio >= (np.abs(R[E]) / h[E]).max() * (1 - 1e-6)
+        assert rel_err(z.astype(np.float64), ref.z) <= 2 * eps + 1e-6
+    g.close()
+
+
 def test_small_hub_pieces(dev, monkeypatch):
     """FJ_PIECE: hub rows split into many 64-arc pieces (the combine path)."""
     monkeypatch.setenv("FJ_PIECE", "64")
