@@ -104,6 +104,53 @@ __global__ void k_out_keys(int64_t n, const int64_t *__restrict__ rp, const int3
   }
 }
 
+// packed transpose (inputs already on the device): key u, payload the source
+// row v — with the weight's bits in the high word when weighted — so the
+// sorted payload is the out-CSR itself (no index gather afterwards).  Same
+// validation bits as k_out_keys, plus the weight check (8)
+template <bool WT>
+__global__ void k_out_pack(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                           const float *__restrict__ w, uint32_t *__restrict__ key,
+                           uint32_t *__restrict__ v32, uint64_t *__restrict__ v64,
+                           int *__restrict__ err) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    int bad = 0;
+    const int64_t b = rp[v], e1 = rp[v + 1];
+    for (int64_t e = b + lane; e < e1; e += 32) {
+      const int32_t u = col[e];
+      if (err) {
+        if (u < 0 || u >= n) bad |= 2;
+        if (u == v) bad |= 4;
+        if (e > b && col[e - 1] >= u) bad |= 64;
+      }
+      key[e] = (u >= 0 && u < n) ? (uint32_t)u : 0u;
+      if constexpr (WT) {
+        const float x = w[e];
+        if (err && !(x > 0.0f && isfinite(x))) bad |= 8;
+        v64[e] = (uint64_t)(uint32_t)v | ((uint64_t)__float_as_uint(x) << 32);
+      } else {
+        v32[e] = (uint32_t)v;
+      }
+    }
+    if (err) {
+      bad = __reduce_or_sync(0xffffffffu, bad);
+      if (lane == 0 && bad) atomicOr(err, bad);
+    }
+  }
+}
+
+__global__ void k_out_unpack(int64_t m, const uint64_t *__restrict__ v64, int32_t *__restrict__ ocol,
+                             float *__restrict__ ow) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const uint64_t x = v64[k];
+  ocol[k] = (int32_t)(uint32_t)x;
+  ow[k] = __uint_as_float((uint32_t)(x >> 32));
+}
+
 // row pointers of the out-CSR from the sorted keys (no atomics): ort[u] is
 // the first position whose key is >= u (binary search)
 __global__ void k_bounds(int64_t n, int64_t m, const uint32_t *__restrict__ key,
@@ -201,13 +248,45 @@ fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **
   uint32_t *k0 = nullptr, *k1 = nullptr, *i0 = nullptr, *i1 = nullptr, *row = nullptr;
   FJ_CUDA(tmp.alloc(&k0, (size_t)m + 1));
   FJ_CUDA(tmp.alloc(&k1, (size_t)m + 1));
-  FJ_CUDA(tmp.alloc(&i0, (size_t)m + 1));
-  FJ_CUDA(tmp.alloc(&i1, (size_t)m + 1));
-  FJ_CUDA(tmp.alloc(&row, (size_t)m + 1));
   FJ_CUDA(ws.alloc(ort, (size_t)n + 1));
   FJ_CUDA(ws.alloc(ocol, (size_t)m + 8));
   *ow = nullptr;
   if (g->in_w) FJ_CUDA(ws.alloc(ow, (size_t)m + 8));
+  if (!g->w_ready) {
+    // weights (if any) are on the device already: sort the out-CSR payload
+    // itself (radix passes move 8 or 12 bytes per arc, every access coalesced)
+    if (g->in_w) {
+      uint64_t *p0 = nullptr, *p1 = nullptr;
+      FJ_CUDA(tmp.alloc(&p0, (size_t)m + 1));
+      FJ_CUDA(tmp.alloc(&p1, (size_t)m + 1));
+      fj::count_launch();
+      k_out_pack<true><<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, g->in_w, k0,
+                                                          nullptr, p0, err);
+      FJ_TRY(sort_pairs(k0, k1, p0, p1, m, bits_for(n), tmp));
+      if (m > 0) {
+        fj::count_launch();
+        k_out_unpack<<<grid_for(m), kBlock, 0, st>>>(m, p0, *ocol, *ow);
+      }
+    } else {
+      uint32_t *v0 = nullptr, *v1 = reinterpret_cast<uint32_t *>(*ocol);
+      FJ_CUDA(tmp.alloc(&v0, (size_t)m + 1));
+      fj::count_launch();
+      k_out_pack<false><<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, nullptr, k0,
+                                                           v0, nullptr, err);
+      FJ_TRY(sort_pairs(k0, k1, v0, v1, m, bits_for(n), tmp));
+      if (m > 0 && v0 != reinterpret_cast<uint32_t *>(*ocol))
+        FJ_CUDA(cudaMemcpyAsync(*ocol, v0, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, st));
+    }
+    fj::count_launch();
+    k_bounds<<<grid_for(n + 1), kBlock, 0, st>>>(n, m, k0, *ort);
+    FJ_CUDA(cudaGetLastError());
+    return FJ_OK;
+  }
+  // host weights still in flight on the side stream: sort arc indices now and
+  // gather the weights once they have landed
+  FJ_CUDA(tmp.alloc(&i0, (size_t)m + 1));
+  FJ_CUDA(tmp.alloc(&i1, (size_t)m + 1));
+  FJ_CUDA(tmp.alloc(&row, (size_t)m + 1));
   fj::count_launch();
   k_out_keys<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, k0, i0, row, err);
   FJ_TRY(sort_pairs(k0, k1, i0, i1, m, bits_for(n), tmp));
