@@ -69,25 +69,101 @@ __global__ void k_perm(int64_t n, const uint64_t *__restrict__ keys, const int64
   len[i] = ort[u + 1] - ort[u];
 }
 
-// warp per new row: copy the out-row of perm[i] with relabelled columns
-__global__ void k_copy_rows(int64_t n, const int32_t *__restrict__ perm,
+// warp per 32 consecutive new rows (rows of one length class sit together):
+// the warp walks the rows' concatenated arc range 32 arcs at a time, each lane
+// finding its arc's row among the 32 row starts by a shuffle binary search
+// (all lanes busy even for 1–4-arc rows).  Chunks holding more than
+// kLongChunk arcs (hub rows) are cut into kLongChunk-arc pieces listed for
+// k_copy_long, a warp per piece, so no warp walks a whole hub row alone.
+constexpr int64_t kLongChunk = 2048;
+
+// the 32-row walk over arcs [k0, k1) of the chunk starting at row i0 (lane l
+// holds the chunk's row start my_rp and source start my_src of row i0 + l)
+__device__ __forceinline__ void copy_walk(int64_t n, int nr, int64_t my_rp, int64_t my_src,
+                                          int64_t k0, int64_t k1, const int32_t *__restrict__ iperm,
+                                          const int32_t *__restrict__ ocol,
+                                          const float *__restrict__ ow, int32_t *__restrict__ col,
+                                          float *__restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t k = k0 + lane; k - lane < k1; k += 32) {
+    // largest r < nr with rp[i0 + r] <= k (rows may be empty: take the last)
+    int r = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int q = r + step;
+      const int64_t v = __shfl_sync(0xffffffffu, my_rp, q < nr ? q : 0);
+      if (q < nr && v <= k) r = q;
+    }
+    const int64_t rs = __shfl_sync(0xffffffffu, my_rp, r);
+    const int64_t src = __shfl_sync(0xffffffffu, my_src, r);
+    if (k < k1) {
+      const int64_t sk = src + (k - rs);
+      const int32_t c = ocol[sk];
+      col[k] = c < n ? iperm[c] : c;  // c ≥ n: a shard's remote column (shard.cu)
+      if (w) w[k] = ow[sk];
+    }
+  }
+}
+__global__ void k_copy_rows32(int64_t n, const int32_t *__restrict__ perm,
+                              const int32_t *__restrict__ iperm, const int64_t *__restrict__ ort,
+                              const int32_t *__restrict__ ocol, const float *__restrict__ ow,
+                              const double *__restrict__ deg, const int64_t *__restrict__ rp,
+                              int32_t *__restrict__ col, float *__restrict__ w,
+                              double *__restrict__ d1, unsigned *__restrict__ long_cnt,
+                              int2 *__restrict__ long_list) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t i0 = warp * 32; i0 < n; i0 += nwarps * 32) {
+    const int64_t i = i0 + lane;
+    const int nr = (int)(n - i0 < 32 ? n - i0 : 32);
+    int64_t my_rp = 0, my_src = 0;
+    if (i < n) {
+      const int32_t u = perm[i];
+      my_rp = rp[i];
+      my_src = ort[u];
+      if (d1) d1[i] = 1.0 + deg[u];
+    }
+    const int64_t a0 = __shfl_sync(0xffffffffu, my_rp, 0);
+    const int64_t a1 = rp[i0 + nr];
+    if (a1 - a0 > kLongChunk) {
+      const int np = (int)((a1 - a0 + kLongChunk - 1) / kLongChunk);
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(long_cnt, (unsigned)np);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      for (int q = lane; q < np; q += 32) long_list[base + q] = make_int2((int)(i0 >> 5), q);
+      continue;
+    }
+    copy_walk(n, nr, my_rp, my_src, a0, a1, iperm, ocol, ow, col, w);
+  }
+}
+
+// the listed pieces of long chunks, a warp per piece (grid-stride over the
+// device-side piece count)
+__global__ void k_copy_long(int64_t n, const unsigned *__restrict__ long_cnt,
+                            const int2 *__restrict__ long_list, const int32_t *__restrict__ perm,
                             const int32_t *__restrict__ iperm, const int64_t *__restrict__ ort,
                             const int32_t *__restrict__ ocol, const float *__restrict__ ow,
-                            const double *__restrict__ deg, const int64_t *__restrict__ rp,
-                            int32_t *__restrict__ col, float *__restrict__ w,
-                            double *__restrict__ d1) {
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
-  for (int64_t i = warp; i < n; i += nwarps) {
-    int32_t u = perm[i];
-    int64_t b = ort[u], e = ort[u + 1], o = rp[i];
-    for (int64_t k = lane; k < e - b; k += 32) {
-      const int32_t c = ocol[b + k];
-      col[o + k] = c < n ? iperm[c] : c;  // c ≥ n: a shard's remote column (shard.cu)
-      if (w) w[o + k] = ow[b + k];
+                            const int64_t *__restrict__ rp, int32_t *__restrict__ col,
+                            float *__restrict__ w) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  const int64_t items = (int64_t)*long_cnt;
+  for (int64_t it = warp; it < items; it += nwarps) {
+    const int2 pc = long_list[it];
+    const int64_t i0 = 32 * (int64_t)pc.x;
+    const int nr = (int)(n - i0 < 32 ? n - i0 : 32);
+    int64_t my_rp = 0, my_src = 0;
+    if (lane < nr) {
+      my_rp = rp[i0 + lane];
+      my_src = ort[perm[i0 + lane]];
     }
-    if (lane == 0 && d1) d1[i] = 1.0 + deg[u];
+    const int64_t a0 = __shfl_sync(0xffffffffu, my_rp, 0);
+    const int64_t a1 = rp[i0 + nr];
+    const int64_t k0 = a0 + (int64_t)pc.y * kLongChunk;
+    const int64_t k1 = k0 + kLongChunk < a1 ? k0 + kLongChunk : a1;
+    copy_walk(n, nr, my_rp, my_src, k0, k1, iperm, ocol, ow, col, w);
   }
 }
 
@@ -224,8 +300,18 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   }
   fj::count_launch();
   mark("keys+sort+perm+scan");
-  k_copy_rows<<<gridn(n * 32), kBlock, 0, st>>>(n, L->perm, L->iperm, ort, ocol, ow, g->deg, L->rp,
-                                                L->col, L->w, L->d1);
+  {
+    unsigned *long_cnt = nullptr;
+    int2 *long_list = nullptr;
+    FJ_CUDA(ws.alloc(&long_cnt, 1));
+    FJ_CUDA(ws.alloc(&long_list, (size_t)(m / kLongChunk + n / 32 + 2)));
+    FJ_CUDA(cudaMemsetAsync(long_cnt, 0, sizeof(unsigned), st));
+    k_copy_rows32<<<gridn(n), kBlock, 0, st>>>(n, L->perm, L->iperm, ort, ocol, ow, g->deg, L->rp,
+                                               L->col, L->w, L->d1, long_cnt, long_list);
+    fj::count_launch();
+    k_copy_long<<<g->num_sms * 8, kBlock, 0, st>>>(n, long_cnt, long_list, L->perm, L->iperm, ort,
+                                                   ocol, ow, L->rp, L->col, L->w);
+  }
 
   int64_t *dmax = nullptr;
   int64_t hmax = 0;
