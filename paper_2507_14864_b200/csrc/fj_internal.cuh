@@ -36,6 +36,23 @@ constexpr int kTileArcs = 2048;       // max arcs of one CTA tile task (smem pro
 #endif
 constexpr int kWarpTileArcs = FJ_WT_ARCS;  // max arcs of one warp tile (8 per lane)
 constexpr int kNumClasses = 8;        // row-length classes of the layout
+constexpr int64_t kChunkArcs = 2048;  // chunked row walks: pieces of long 32-row chunks
+
+// Chunked row walks (graph build, layout copy): a warp owns 32 consecutive
+// rows, lane l holding the start my_rp of row i0 + l (nr ≤ 32 rows).  For an
+// arc position k in the chunk, the row is the largest r < nr with
+// rp[i0 + r] ≤ k (empty rows share a start: the last of them is the owner).
+// Five shuffles; every lane of the warp must call it.
+__device__ __forceinline__ int chunk_row_of(int nr, int64_t my_rp, int64_t k) {
+  int r = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1) {
+    const int q = r + step;
+    const int64_t v = __shfl_sync(0xffffffffu, my_rp, q < nr ? q : 0);
+    if (q < nr && v <= k) r = q;
+  }
+  return r;
+}
 
 // Row-length classes (out-degree L of the pull CSR).  Rows with L == 0 are
 // solved exactly at init (z_v = s_v, Eq. (1) with d_v = 0) and never enter a

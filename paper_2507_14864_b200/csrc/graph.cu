@@ -73,72 +73,100 @@ __global__ void k_unpack_sorted(int64_t m, int nb, const uint64_t *__restrict__ 
   if (w_dst) w_dst[i] = w_src[idx[i]];
 }
 
-// transpose inputs: key u, payload arc index; row of every arc.  With err
-// (graph create) the same pass validates the caller's columns — range (bit 2),
-// self-loop (4) and whether rows are strictly increasing (64: not canonical) —
-// so the input's columns are read once for both
-__global__ void k_out_keys(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                           uint32_t *__restrict__ key, uint32_t *__restrict__ idx,
-                           uint32_t *__restrict__ row, int *__restrict__ err) {
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
-  for (int64_t v = warp; v < n; v += nwarps) {
-    int bad = 0;
-    const int64_t b = rp[v], e1 = rp[v + 1];
-    for (int64_t e = b + lane; e < e1; e += 32) {
-      const int32_t u = col[e];
-      if (err) {
-        if (u < 0 || u >= n) bad |= 2;
-        if (u == v) bad |= 4;
-        if (e > b && col[e - 1] >= u) bad |= 64;
-      }
-      key[e] = (u >= 0 && u < n) ? (uint32_t)u : 0u;
-      idx[e] = (uint32_t)e;
-      row[e] = (uint32_t)v;
-    }
+// Transpose inputs, one pass over the in-CSR that also validates the
+// caller's columns — range (bit 2), self-loop (4), rows not strictly
+// increasing (64: not canonical) and, packed with weights, the weight (8).
+//   KIdx:  key u, payload arc index e, row v of every arc (host weights still
+//          in flight: they are gathered by index after the sort);
+//   KV32:  key u, payload v (unweighted: the sorted payload is the out-CSR);
+//   KV64:  key u, payload v | bits(w) << 32 (weights on the device).
+// Chunked: a warp walks the concatenated arcs of 32 consecutive rows (all
+// lanes busy for short rows); chunks above kChunkArcs arcs are cut into
+// pieces for k_out_keys_long (hub rows spread over many warps).
+enum KeyMode { KIdx = 0, KV32 = 1, KV64 = 2 };
+struct KeyOut {
+  uint32_t *key, *idx, *row, *v32;
+  uint64_t *v64;
+};
+
+template <int KM>
+__device__ __forceinline__ void keys_walk(int64_t n, int64_t i0, int nr, int64_t my_rp,
+                                          int64_t k0, int64_t k1, const int32_t *__restrict__ col,
+                                          const float *__restrict__ w, KeyOut o, int *err) {
+  const int lane = threadIdx.x & 31;
+  int bad = 0;
+  for (int64_t k = k0 + lane; k - lane < k1; k += 32) {
+    const int r = chunk_row_of(nr, my_rp, k);
+    const int64_t rs = __shfl_sync(0xffffffffu, my_rp, r);
+    if (k >= k1) continue;
+    const int64_t v = i0 + r;
+    const int32_t u = col[k];
     if (err) {
-      bad = __reduce_or_sync(0xffffffffu, bad);
-      if (lane == 0 && bad) atomicOr(err, bad);
+      if (u < 0 || u >= n) bad |= 2;
+      if (u == v) bad |= 4;
+      if (k > rs && col[k - 1] >= u) bad |= 64;
     }
+    o.key[k] = (u >= 0 && u < n) ? (uint32_t)u : 0u;
+    if constexpr (KM == KIdx) {
+      o.idx[k] = (uint32_t)k;
+      o.row[k] = (uint32_t)v;
+    } else if constexpr (KM == KV32) {
+      o.v32[k] = (uint32_t)v;
+    } else {
+      const float x = w[k];
+      if (err && !(x > 0.0f && isfinite(x))) bad |= 8;
+      o.v64[k] = (uint64_t)(uint32_t)v | ((uint64_t)__float_as_uint(x) << 32);
+    }
+  }
+  if (err) {
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0 && bad) atomicOr(err, bad);
   }
 }
 
-// packed transpose (inputs already on the device): key u, payload the source
-// row v — with the weight's bits in the high word when weighted — so the
-// sorted payload is the out-CSR itself (no index gather afterwards).  Same
-// validation bits as k_out_keys, plus the weight check (8)
-template <bool WT>
-__global__ void k_out_pack(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                           const float *__restrict__ w, uint32_t *__restrict__ key,
-                           uint32_t *__restrict__ v32, uint64_t *__restrict__ v64,
-                           int *__restrict__ err) {
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
-  for (int64_t v = warp; v < n; v += nwarps) {
-    int bad = 0;
-    const int64_t b = rp[v], e1 = rp[v + 1];
-    for (int64_t e = b + lane; e < e1; e += 32) {
-      const int32_t u = col[e];
-      if (err) {
-        if (u < 0 || u >= n) bad |= 2;
-        if (u == v) bad |= 4;
-        if (e > b && col[e - 1] >= u) bad |= 64;
-      }
-      key[e] = (u >= 0 && u < n) ? (uint32_t)u : 0u;
-      if constexpr (WT) {
-        const float x = w[e];
-        if (err && !(x > 0.0f && isfinite(x))) bad |= 8;
-        v64[e] = (uint64_t)(uint32_t)v | ((uint64_t)__float_as_uint(x) << 32);
-      } else {
-        v32[e] = (uint32_t)v;
-      }
+template <int KM>
+__global__ void k_out_keys(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                           const float *__restrict__ w, KeyOut o, int *err, unsigned *long_cnt,
+                           int2 *long_list) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t i0 = warp * 32; i0 < n; i0 += nwarps * 32) {
+    const int nr = (int)(n - i0 < 32 ? n - i0 : 32);
+    const int64_t my_rp = lane < nr ? rp[i0 + lane] : 0;
+    const int64_t a0 = __shfl_sync(0xffffffffu, my_rp, 0);
+    const int64_t a1 = rp[i0 + nr];
+    if (a1 - a0 > kChunkArcs) {
+      const int np = (int)((a1 - a0 + kChunkArcs - 1) / kChunkArcs);
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(long_cnt, (unsigned)np);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      for (int q = lane; q < np; q += 32) long_list[base + q] = make_int2((int)(i0 >> 5), q);
+      continue;
     }
-    if (err) {
-      bad = __reduce_or_sync(0xffffffffu, bad);
-      if (lane == 0 && bad) atomicOr(err, bad);
-    }
+    keys_walk<KM>(n, i0, nr, my_rp, a0, a1, col, w, o, err);
+  }
+}
+
+template <int KM>
+__global__ void k_out_keys_long(int64_t n, const int64_t *__restrict__ rp,
+                                const int32_t *__restrict__ col, const float *__restrict__ w,
+                                KeyOut o, int *err, const unsigned *long_cnt,
+                                const int2 *long_list) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  const int64_t items = (int64_t)*long_cnt;
+  for (int64_t it = warp; it < items; it += nwarps) {
+    const int2 pc = long_list[it];
+    const int64_t i0 = 32 * (int64_t)pc.x;
+    const int nr = (int)(n - i0 < 32 ? n - i0 : 32);
+    const int64_t my_rp = lane < nr ? rp[i0 + lane] : 0;
+    const int64_t a0 = __shfl_sync(0xffffffffu, my_rp, 0);
+    const int64_t a1 = rp[i0 + nr];
+    const int64_t k0 = a0 + (int64_t)pc.y * kChunkArcs;
+    const int64_t k1 = k0 + kChunkArcs < a1 ? k0 + kChunkArcs : a1;
+    keys_walk<KM>(n, i0, nr, my_rp, k0, k1, col, w, o, err);
   }
 }
 
@@ -237,6 +265,24 @@ static fj_status sort_pairs(K *&keys, K *&keys_alt, V *&val, V *&val_alt, int64_
   return FJ_OK;
 }
 
+template <int KM>
+static fj_status launch_out_keys(fj_graph *g, Workspace &tmp, const float *w, KeyOut o, int *err) {
+  const int64_t n = g->n, m = g->m;
+  cudaStream_t st = g->stream;
+  unsigned *long_cnt = nullptr;
+  int2 *long_list = nullptr;
+  FJ_CUDA(tmp.alloc(&long_cnt, 1));
+  FJ_CUDA(tmp.alloc(&long_list, (size_t)(m / kChunkArcs + n / 32 + 2)));
+  FJ_CUDA(cudaMemsetAsync(long_cnt, 0, sizeof(unsigned), st));
+  fj::count_launch();
+  k_out_keys<KM><<<grid_for(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, w, o, err, long_cnt,
+                                                 long_list);
+  fj::count_launch();
+  k_out_keys_long<KM><<<g->num_sms * 8, kBlock, 0, st>>>(n, g->in_rp, g->in_col, w, o, err,
+                                                         long_cnt, long_list);
+  return FJ_OK;
+}
+
 // Transpose the canonical in-CSR into the pull CSR (row u lists v with a_uv),
 // rows sorted: a stable radix sort on u alone keeps the v order of the
 // canonical input.  *ort, *ocol, *ow live in the caller's workspace `ws`.
@@ -259,9 +305,8 @@ fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **
       uint64_t *p0 = nullptr, *p1 = nullptr;
       FJ_CUDA(tmp.alloc(&p0, (size_t)m + 1));
       FJ_CUDA(tmp.alloc(&p1, (size_t)m + 1));
-      fj::count_launch();
-      k_out_pack<true><<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, g->in_w, k0,
-                                                          nullptr, p0, err);
+      KeyOut o{k0, nullptr, nullptr, nullptr, p0};
+      FJ_TRY(launch_out_keys<KV64>(g, tmp, g->in_w, o, err));
       FJ_TRY(sort_pairs(k0, k1, p0, p1, m, bits_for(n), tmp));
       if (m > 0) {
         fj::count_launch();
@@ -270,9 +315,8 @@ fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **
     } else {
       uint32_t *v0 = nullptr, *v1 = reinterpret_cast<uint32_t *>(*ocol);
       FJ_CUDA(tmp.alloc(&v0, (size_t)m + 1));
-      fj::count_launch();
-      k_out_pack<false><<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, nullptr, k0,
-                                                           v0, nullptr, err);
+      KeyOut o{k0, nullptr, nullptr, v0, nullptr};
+      FJ_TRY(launch_out_keys<KV32>(g, tmp, nullptr, o, err));
       FJ_TRY(sort_pairs(k0, k1, v0, v1, m, bits_for(n), tmp));
       if (m > 0 && v0 != reinterpret_cast<uint32_t *>(*ocol))
         FJ_CUDA(cudaMemcpyAsync(*ocol, v0, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, st));
@@ -287,8 +331,10 @@ fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **
   FJ_CUDA(tmp.alloc(&i0, (size_t)m + 1));
   FJ_CUDA(tmp.alloc(&i1, (size_t)m + 1));
   FJ_CUDA(tmp.alloc(&row, (size_t)m + 1));
-  fj::count_launch();
-  k_out_keys<<<grid_warps(n), kBlock, 0, st>>>(n, g->in_rp, g->in_col, k0, i0, row, err);
+  {
+    KeyOut o{k0, i0, row, nullptr, nullptr};
+    FJ_TRY(launch_out_keys<KIdx>(g, tmp, nullptr, o, err));
+  }
   FJ_TRY(sort_pairs(k0, k1, i0, i1, m, bits_for(n), tmp));
   if (m > 0) {
     if (g->w_ready) FJ_CUDA(cudaStreamWaitEvent(st, g->w_ready, 0));  // weights staged

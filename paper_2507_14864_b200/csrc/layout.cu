@@ -75,7 +75,7 @@ __global__ void k_perm(int64_t n, const uint64_t *__restrict__ keys, const int64
 // (all lanes busy even for 1–4-arc rows).  Chunks holding more than
 // kLongChunk arcs (hub rows) are cut into kLongChunk-arc pieces listed for
 // k_copy_long, a warp per piece, so no warp walks a whole hub row alone.
-constexpr int64_t kLongChunk = 2048;
+constexpr int64_t kLongChunk = kChunkArcs;
 
 // the 32-row walk over arcs [k0, k1) of the chunk starting at row i0 (lane l
 // holds the chunk's row start my_rp and source start my_src of row i0 + l)
@@ -86,14 +86,7 @@ __device__ __forceinline__ void copy_walk(int64_t n, int nr, int64_t my_rp, int6
                                           float *__restrict__ w) {
   const int lane = threadIdx.x & 31;
   for (int64_t k = k0 + lane; k - lane < k1; k += 32) {
-    // largest r < nr with rp[i0 + r] <= k (rows may be empty: take the last)
-    int r = 0;
-#pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-      const int q = r + step;
-      const int64_t v = __shfl_sync(0xffffffffu, my_rp, q < nr ? q : 0);
-      if (q < nr && v <= k) r = q;
-    }
+    const int r = chunk_row_of(nr, my_rp, k);
     const int64_t rs = __shfl_sync(0xffffffffu, my_rp, r);
     const int64_t src = __shfl_sync(0xffffffffu, my_src, r);
     if (k < k1) {
