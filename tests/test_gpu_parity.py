@@ -304,6 +304,53 @@ def test_push_certifies_rows_without_arcs(dev, monkeypatch, compact, omega):
     g.close()
 
 
+def mixed_hub_graph(weighted, seed=17):
+    """Directed graph whose in-rows mix hubs around the 2048-arc chunk size
+    (2047, 2048, 2049, 4096, 5000, 7000 arcs), empty rows and short rows, so
+    32-row chunks of the build's chunked walks hold several pieces, rows that
+    cross piece boundaries and empty rows between them."""
+    rng = np.random.default_rng(seed)
+    n = 9000
+    lens = rng.integers(0, 6, n)
+    lens[rng.random(n) < 0.2] = 0
+    hubs = {3: 2047, 4: 2048, 5: 2049, 6: 0, 7: 5000, 9: 7000, 10: 1, 11: 0, 40: 4096,
+            41: 300, 8000: 6000}
+    for v, L in hubs.items():
+        lens[v] = L
+    rows = []
+    for v in range(n):
+        c = rng.choice(n - 1, lens[v], replace=False)
+        c[c >= v] += 1                       # no self-loops
+        # popular columns: long rows on the transposed (pull) side as well
+        for hub, p in ((100, 0.5), (101, 0.25), (102, 0.23)):
+            if v != hub and rng.random() < p:
+                c = np.append(c, hub)
+        rows.append(np.unique(c))
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum([len(c) for c in rows])
+    col = np.concatenate(rows).astype(np.int32)
+    w = fjgen.arc_weights(rp, col, seed) if weighted else None
+    return rp, col, w
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_chunked_build_mixed_hubs(dev, weighted):
+    """Graph build from device tensors (packed transpose) and from host arrays
+    (index transpose, weights staged on the side stream) give the same layout:
+    COLORED results agree bit for bit; both pass the oracle's parity bar."""
+    rp, col, w = mixed_hub_graph(weighted)
+    s = fjgen.uniform(len(rp) - 1, 23)
+    check_parity(dev, rp, col, w, s, 1e-6, 1.0, True, method="async")
+    outs = []
+    for host in (False, True):
+        g, z, zp, st = gpu_solve(dev, rp, col, w, s, 1e-6, 1.0, True, method="colored", host=host)
+        assert st.status == 0
+        outs.append(zp)
+        g.close()
+    assert np.array_equal(outs[0], outs[1])
+    assert oracle.certificate(rp, col, w, s, outs[0], 1e-6)[0] <= 1.0
+
+
 def test_small_hub_pieces(dev, monkeypatch):
     """FJ_PIECE: hub rows split into many 64-arc pieces (the combine path)."""
     monkeypatch.setenv("FJ_PIECE", "64")
