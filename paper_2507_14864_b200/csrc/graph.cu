@@ -209,22 +209,72 @@ __global__ void k_out_fill(int64_t m, const uint32_t *__restrict__ idx, const ui
   }
 }
 
-// d_u = Σ_v a_uv over the out-row u (warp per row, fixed lane order + fixed
-// shuffle tree ⇒ deterministic fp64 sums)
+// d_u = Σ_v a_uv over the out-rows, fp64, deterministic (the order of
+// the additions depends only on the graph).  Unweighted: d_u = row length.
+// Weighted, chunked like the transpose: a warp walks the arcs of 32
+// consecutive rows 32 at a time; a segmented lane scan sums each row's arcs
+// of the step and the row's owner lane adds its segment total.  Chunks above
+// kChunkArcs arcs go to k_row_sums_long (a warp per row, lane-strided sums
+// and a fixed shuffle tree).
 __global__ void k_row_sums(int64_t n, const int64_t *__restrict__ rp, const float *__restrict__ w,
-                           double *__restrict__ d) {
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
-  for (int64_t u = warp; u < n; u += nwarps) {
-    int64_t b = rp[u], e = rp[u + 1];
-    double s = 0.0;
-    if (w) {
-      for (int64_t k = b + lane; k < e; k += 32) s += (double)w[k];
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    } else {
-      s = (double)(e - b);
+                           double *__restrict__ d, unsigned *__restrict__ long_cnt,
+                           int32_t *__restrict__ long_list) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t i0 = warp * 32; i0 < n; i0 += nwarps * 32) {
+    const int nr = (int)(n - i0 < 32 ? n - i0 : 32);
+    int64_t my_b = 0, my_e = 0;
+    if (lane < nr) {
+      my_b = rp[i0 + lane];
+      my_e = rp[i0 + lane + 1];
     }
+    if (!w) {
+      if (lane < nr) d[i0 + lane] = (double)(my_e - my_b);
+      continue;
+    }
+    const int64_t a0 = __shfl_sync(0xffffffffu, my_b, 0);
+    const int64_t a1 = __shfl_sync(0xffffffffu, my_e, nr - 1);
+    if (a1 - a0 > kChunkArcs) {
+      if (lane == 0) long_list[atomicAdd(long_cnt, 1u)] = (int32_t)(i0 >> 5);
+      continue;
+    }
+    double acc = 0.0;
+    for (int64_t base = a0; base < a1; base += 32) {
+      const int64_t k = base + lane;
+      const int r = chunk_row_of(nr, my_b, k);
+      double v = k < a1 ? (double)w[k] : 0.0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {  // segmented inclusive scan by row
+        const double y = __shfl_up_sync(0xffffffffu, v, off);
+        const int ry = __shfl_up_sync(0xffffffffu, r, off);
+        if (lane >= off && ry == r) v += y;
+      }
+      const int64_t hi = my_e < base + 32 ? my_e : base + 32;  // my row ∩ this step
+      const int64_t lo = my_b > base ? my_b : base;
+      const bool has = lane < nr && hi > lo;
+      const double seg = __shfl_sync(0xffffffffu, v, has ? (int)(hi - 1 - base) : 0);
+      if (has) acc += seg;
+    }
+    if (lane < nr) d[i0 + lane] = acc;
+  }
+}
+
+__global__ void k_row_sums_long(int64_t n, const int64_t *__restrict__ rp,
+                                const float *__restrict__ w, double *__restrict__ d,
+                                const unsigned *__restrict__ long_cnt,
+                                const int32_t *__restrict__ long_list) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  const int64_t items = 32 * (int64_t)*long_cnt;
+  for (int64_t it = warp; it < items; it += nwarps) {
+    const int64_t u = 32 * (int64_t)long_list[it >> 5] + (it & 31);
+    if (u >= n) continue;
+    const int64_t b = rp[u], e = rp[u + 1];
+    double s = 0.0;
+    for (int64_t k = b + lane; k < e; k += 32) s += (double)w[k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) d[u] = s;
   }
 }
@@ -490,8 +540,19 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
 
   // 5. degrees
   FJ_CUDA(cudaMallocAsync(&g->deg, sizeof(double) * n, st));
-  fj::count_launch();
-  k_row_sums<<<grid_warps(n), kBlock, 0, st>>>(n, ort, ow, g->deg);
+  {
+    unsigned *long_cnt = nullptr;
+    int32_t *long_list = nullptr;
+    FJ_CUDA(ws.alloc(&long_cnt, 1));
+    FJ_CUDA(ws.alloc(&long_list, (size_t)(n / 32 + 1)));
+    FJ_CUDA(cudaMemsetAsync(long_cnt, 0, sizeof(unsigned), st));
+    fj::count_launch();
+    k_row_sums<<<grid_for(n), kBlock, 0, st>>>(n, ort, ow, g->deg, long_cnt, long_list);
+    if (ow) {
+      fj::count_launch();
+      k_row_sums_long<<<g->num_sms * 8, kBlock, 0, st>>>(n, ort, ow, g->deg, long_cnt, long_list);
+    }
+  }
   mark("degrees");
 
   // 6. symmetry of undirected input
