@@ -284,7 +284,9 @@ def run_ours(args, prob, world, rank, local):
     prof = os.path.join(ROOT, "profiles", "ncu_sweep_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            # ncu's dram bytes per sweep of its captured launch × this launch's
+            # sweeps (a launch runs as many sweeps as ASYNC needs: 246–253 on C4)
+            traffic = json.load(open(prof))["dram_bytes_per_sweep"] * st0.sweeps
         except Exception:
             traffic = None
 
