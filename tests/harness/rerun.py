@@ -1,5 +1,5 @@
 """Call one GPU test function many times in one process and report failures
-(diagnostics for rare flakes).  usage: test_rep.py module func param reps"""
+(diagnostics for rare flakes).  usage: rerun.py module func param reps"""
 import sys, os, traceback, inspect
 sys.path.insert(0, os.getcwd())
 import importlib, torch
