@@ -256,8 +256,10 @@ __device__ __forceinline__ A block_reduce(A a, A *sm) {
 }
 
 // Warp unit (rows above 256 arcs): one warp accumulates a whole row or one
-// kWarpPiece-arc piece of it in registers — 8 independent col/w loads, then 8
-// ẑ gathers per lane per step — and reduces with shuffles (no block barrier).
+// kWarpPiece-arc piece of it in registers — U = 4 independent col/w loads, then
+// 4 ẑ gathers per lane per step (U = 4 measured best with the warp tiles in the
+// same kernel: C3 −5 %, C5 −7 %, C4 −1 % per sweep against U = 8) — and reduces
+// with shuffles (no block barrier).
 // Pieces of one row are combined by the last-arriving warp in piece order
 // (deterministic).
 template <int MODE, bool W>
@@ -265,7 +267,7 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
   // rows above 256 arcs accumulate in double-double for RELAX and CERT
   using A = typename std::conditional<MODE == DIS || MODE == SPMV, double, dd>::type;
 #ifndef FJ_WU
-#define FJ_WU 8
+#define FJ_WU 4
 #endif
   constexpr int U = FJ_WU;  // arcs per lane per step (loads in flight)
   const int lane = threadIdx.x & 31;
