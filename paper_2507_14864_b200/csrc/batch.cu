@@ -46,9 +46,12 @@ __device__ __forceinline__ void relax_rowK(const KP &p, const Scalars *SK, int r
 }
 
 // warp unit (row > kWarpTileArcs arcs, or a piece of one), K right-hand sides
+#ifndef FJ_BWU
+#define FJ_BWU 4
+#endif
 template <bool W, int K>
 __device__ __forceinline__ void do_warpK(const KP &p, const Scalars *SK, const Task &tk, TAcc &t) {
-  constexpr int U = 4;
+  constexpr int U = FJ_BWU;  // arcs per lane per step (diagnostic build flag FJ_BWU)
   const int lane = threadIdx.x & 31;
   const int row = tk.a, piece = tk.b, np = tk.kind >> 8, slot = tk.slot;
   const int64_t a0 = tk.a0, a1 = tk.a1;
@@ -179,8 +182,11 @@ __device__ __forceinline__ void tileK(const KP &p, const Scalars *SK, const Task
 // barrier per sweep, counters reduced on the device) around the K-wide units
 // and tiles above.  The loop ends after a sweep in which no right-hand side
 // relaxed any row (Q = ∅ for all of them).
+#ifndef FJ_BMINB
+#define FJ_BMINB 4  // CTAs per SM (diagnostic build flag; 3 and 2 measured slower per sweep)
+#endif
 template <bool W, int K>
-__global__ void __launch_bounds__(kBlock, 4) k_sweep_batch_bar(KP p) {
+__global__ void __launch_bounds__(kBlock, FJ_BMINB) k_sweep_batch_bar(KP p) {
   __shared__ Scalars sk[K];
   __shared__ unsigned long long s_dec[3];
   if (threadIdx.x < K) sk[threadIdx.x] = p.sc[threadIdx.x];
