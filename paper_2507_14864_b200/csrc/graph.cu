@@ -3,12 +3,15 @@
 // Steps (all on the graph's stream):
 //   1. stage the caller's in-CSR into library-owned device memory;
 //   2. validate row_ptr (FJ_ERR_INVALID on failure);
-//   3. transpose to the pull (out-) CSR with a stable radix sort on u; the
-//      same pass validates columns (range, self-loops), weights, and notes
-//      rows that are not strictly increasing;
+//   3. transpose to the pull (out-) CSR with a stable radix sort on u whose
+//      payload is the out-CSR entry itself (v, or v | weight bits; arc
+//      indices only while host weights are still being copied); the keys
+//      pass validates columns (range, self-loops), weights, and notes rows
+//      that are not strictly increasing;
 //   4. only then, canonicalise the in-CSR (rows sorted by column) with a radix
 //      sort of (v, u) keys; adjacent equal keys are duplicate arcs;
-//   5. d_u = Σ_v a_uv over the out-rows in fp64 (reading R3);
+//   5. d_u = Σ_v a_uv over the out-rows in fp64, deterministic order (P:78,
+//      reading R3);
 //   6. undirected input: check the arc set is symmetric with equal weights;
 //   7. build the sweep layout (layout.cu).
 // Sorting and scans use CUB (toolkit library primitives); every kernel here
