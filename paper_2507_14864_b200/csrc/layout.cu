@@ -1,7 +1,9 @@
 // layout.cu — the sweep layout (§8 row a1, K3): rows of the pull CSR
 // permuted to (color, length class, id) order so that every task handles rows
 // of one color and of similar length, and the work list (tasks) that the
-// persistent sweep kernel claims dynamically.
+// persistent sweep kernel walks (static round-robin by default).  The row
+// copy into layout order is chunked: a warp per 32 consecutive new rows
+// (which share a length class), hub chunks cut into 2048-arc pieces.
 //
 // Permuted ids make the per-row state (s, ẑ, 1+d) streams coalesced; within
 // one class the original id order is kept (stable), so R-MAT hubs (low ids)
