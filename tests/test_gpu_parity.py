@@ -653,7 +653,7 @@ def test_warm_start_resume(dev, name):
     """Resume from an earlier estimate (Lemma 3: any ẑ is a valid state): a
     solve warm-started from a converged z needs ≤ 2 sweeps and still passes
     the oracle's certificate; one warm-started from a loose (ε = 1e-2) z
-    converges in fewer sweeps than a cold start."""
+    needs less work (edge updates) than a cold start."""
     rp, col, w, s, directed = TINY[name]()
     n = len(rp) - 1
     g = fj.Graph(n, _t(rp, dev), _t(col, dev), _t(w, dev), directed=directed)
@@ -662,7 +662,10 @@ def test_warm_start_resume(dev, name):
     cold = fj.solve(g, _t(s, dev), z, 1e-6, 1.0)
     fj.solve(g, _t(s, dev), z, 1e-2, 1.0)
     warm = fj.solve(g, _t(s, dev), z, 1e-6, 1.0, z_init=z.double(), zprime_out=zp)
-    assert warm.sweeps < cold.sweeps
+    # less work, not necessarily fewer sweeps: the sweep count is set by the
+    # slowest component, which a loose start barely advances (rmat12w: 227 vs
+    # 226 sweeps once in ~40 runs, with 5.7 M vs 9.0 M edge updates)
+    assert warm.edge_updates < 0.8 * cold.edge_updates
     assert oracle.certificate(rp, col, w, s, zp.cpu().numpy(), 1e-6)[0] <= 1.0
     again = fj.solve(g, _t(s, dev), z, 1e-6, 1.0, z_init=(zp - warm.c).contiguous())
     assert again.sweeps <= 2
