@@ -201,6 +201,39 @@ def omega_opt(mu: float) -> float:
     return 1.0 + (mu / (1.0 + np.sqrt(1.0 - mu * mu))) ** 2
 
 
+def omega_grid(lo=1.0, hi=1.95, step=0.05):
+    """The ω grid of the heuristic, visited from ω → 2⁻ down to 1 (P:488);
+    step 0.05 per reading R10 (P:625's 'step size of 0.5' read as garbled)."""
+    k = int(round((hi - lo) / step))
+    return [round(hi - i * step, 10) for i in range(k + 1)]
+
+
+def omega_sweep(rp, col, w, s, eps, lo=1.0, hi=1.95, step=0.05, sigma=SIGMA, prune=True):
+    """The paper's ω heuristic, verbatim on the oracle: "begin with
+    ω → 2⁻ and iteratively reduce ω by a fixed step size until it reaches 1;
+    the ω that achieves the minimum number of updates" — updates = pops of Q
+    of ImprovedBLISOR (Alg. 2 + Alg. 3, FIFO, fp64).  Reading R10: grid
+    1.95:−0.05:1.00, a diverging or unterminated ω costs +∞, ties go to the
+    smaller ω (the later point of the downward walk).
+
+    With ``prune`` a run is stopped once it exceeds the best count so far (it
+    can no longer win; its cost is recorded as +∞ with status "pruned").
+    Returns (best_omega, table) with table rows (ω, pushes or inf, status)."""
+    best, best_cost, table = None, None, []
+    for om in omega_grid(lo, hi, step):
+        cap = best_cost if (prune and best_cost is not None) else -1
+        res = solve(rp, col, w, s, eps, om, sigma=sigma, alg=3, max_pushes=cap)
+        if res.status == 0 and res.cert_ratio <= 1.0:
+            cost, status = res.pushes, "ok"
+        else:
+            cost = float("inf")
+            status = "pruned" if (cap >= 0 and res.pushes >= cap) else "diverged"
+        table.append((om, cost, status))
+        if cost != float("inf") and (best_cost is None or cost <= best_cost):
+            best, best_cost = om, cost           # ≤: ties go to the smaller ω
+    return best, table
+
+
 def jacobi_mu_dense(rp, col, w):
     """μ = ρ((I+D)^{-1}A) by dense eigenvalues (small n only)."""
     M = dense_system(rp, col, w)

@@ -693,3 +693,93 @@ def test_unsorted_rows_canonicalised(dev):
         outs.append(zp)
         g.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+# ------------------------- full BASELINE sizes against the oracle (round 2)
+_CFG = {}
+
+
+def _config(cid):
+    """Full-size config `cid` (fjgen), generated once per test process."""
+    if cid not in _CFG:
+        _CFG.clear() if len(_CFG) >= 2 else None   # keep host memory bounded
+        _CFG[cid] = fjgen.config(cid)
+    return _CFG[cid]
+
+
+def _full_solve(dev, p, omega, raise_on_numeric=True):
+    g = fj.Graph(p.n, _t(p.row_ptr, dev), _t(p.col, dev), _t(p.w, dev), directed=p.directed)
+    z = torch.empty(p.n, dtype=torch.float32, device=dev)
+    zp = torch.empty(p.n, dtype=torch.float64, device=dev)
+    st = fj.solve(g, _t(p.s, dev), z, p_eps(p), omega, zprime_out=zp,
+                  raise_on_numeric=raise_on_numeric)
+    m = fj.measures(g, z)
+    torch.cuda.synchronize()
+    out = z.cpu().numpy().astype(np.float64), zp.cpu().numpy(), st, m
+    g.close()
+    return out
+
+
+def p_eps(p):
+    return 1e-6   # every config (BASELINE.json configs; fjgen.CONFIG_SOLVE)
+
+
+# (config, ω): the oracle's FIFO solve at the same ω and ε finishes in seconds
+# to ~30 s on one host core (profiles/r01f_full_parity.md)
+FULL_VS_ORACLE = [(1, 1.0), (1, 1.5), (2, 1.0), (5, 1.0), (5, 1.25)]
+
+
+@pytest.mark.parametrize("cid,omega", FULL_VS_ORACLE, ids=[f"C{c}-w{o}" for c, o in FULL_VS_ORACLE])
+def test_full_size_vs_oracle_z(dev, cid, omega):
+    """The north_star parity bar at the full BASELINE size, in the launch
+    configuration bench.py times (AUTO schedule; ε = 1e-6): the GPU z against
+    the oracle's converged z (ImprovedBLI / ImprovedBLISOR, FIFO, fp64; Alg. 2
+    + Alg. 1/3, P:204–228, P:436–463) element by element, max rel ≤ 1e-4;
+    the oracle's own certificate of the GPU ẑ' ≤ 1 (Lemma 6); P and D
+    (tab:measures P:105–106) within 1e-5 of the oracle's measures of its z."""
+    p = _config(cid)
+    z, zp, st, m = _full_solve(dev, p, omega)
+    assert st.status == 0 and st.cert_ratio <= 1.0, st
+    ratio, _ = oracle.certificate(p.row_ptr, p.col, p.w, p.s, zp, 1e-6)
+    assert ratio <= 1.0, ratio
+    ref = oracle.solve(p.row_ptr, p.col, p.w, p.s, 1e-6, omega)
+    assert ref.status == 0
+    assert rel_err(z, ref.z) <= 1e-4
+    om = oracle.measures(p.row_ptr, p.col, p.w, ref.z, directed=p.directed)
+    for k in ("P", "D"):
+        assert abs(m[k] - om[k]) <= 1e-5 * abs(om[k]), (k, m[k], om[k])
+
+
+# (config, ω) whose oracle FIFO solve takes minutes (C3 ω = 1.6: 64 s, C4: 221–1000 s):
+# certified by the oracle's compensated certificate (any size), measures of the same z
+FULL_CERTIFIED = [(3, 1.6), (4, 1.2), (4, 1.4), (4, 1.6)]
+
+
+@pytest.mark.parametrize("cid,omega", FULL_CERTIFIED, ids=[f"C{c}-w{o}" for c, o in FULL_CERTIFIED])
+def test_full_size_sor_certified(dev, cid, omega):
+    """BLISOR at full size (Alg. 3): C3 at ω = 1.6 runs the
+    COLORED schedule with the merged tail (reading R23), C4 the ASYNC directed
+    schedule (R11).  The oracle's compensated certificate of the GPU ẑ' is ≤ 1
+    (⇒ |ẑ − z| ≤ ε·max(|z|, σ), Lemma 6 P:474 + R5); the GPU measures equal the
+    oracle's measures of the same z (≤ 1e-9); min s ≤ z ≤ max s."""
+    p = _config(cid)
+    z, zp, st, m = _full_solve(dev, p, omega)
+    assert st.status == 0 and st.cert_ratio <= 1.0, st
+    if cid == 3:
+        assert st.colors > 1   # AUTO picked the multicolor schedule
+    ratio, _ = oracle.certificate(p.row_ptr, p.col, p.w, p.s, zp, 1e-6)
+    assert ratio <= 1.0, ratio
+    om = oracle.measures(p.row_ptr, p.col, p.w, z, directed=p.directed)
+    for k in ("P", "D"):
+        assert abs(m[k] - om[k]) <= 1e-9 * abs(om[k]), (k, m[k], om[k])
+    s64 = p.s.astype(np.float64)
+    assert z.min() >= s64.min() - 1e-6 and z.max() <= s64.max() + 1e-6
+
+
+def test_full_size_c4_omega18_numeric(dev):
+    """C4 at ω = 1.8 (BASELINE.json's ω list): asynchronous over-relaxation of
+    the directed R-MAT-24 system diverges; the library reports FJ_ERR_NUMERIC
+    (divergence sentinel S:339 / watchdog) instead of a wrong answer (R11)."""
+    p = _config(4)
+    z, zp, st, m = _full_solve(dev, p, 1.8, raise_on_numeric=False)
+    assert st.status == fj.FJ_ERR_NUMERIC and st.reason in (1, 2), st

@@ -195,7 +195,49 @@ def test_zero_opinions_terminate():
     eps = 1e-2
     res = oracle.solve(rp, col, w, s, eps, 1.0)
     assert res.status == 0
-    assert np.all(res.z <= 1e-18) and np.all(res.z >= -res.eps_prime * res.c - 1e-18)
+    # s_min = 0 ⇒ c = σ (Alg. 2 with reading R5) and ε' = σε/(c+σ) = ε/2
+    # (P:337), computed here and not taken from the oracle's own result
+    sig = oracle.SIGMA
+    c = sig
+    eps_p = sig * eps / (c + sig)
+    assert res.c == c and res.eps_prime == pytest.approx(eps_p, rel=1e-15)
+    assert np.all(res.z <= 1e-18) and np.all(res.z >= -eps_p * c - 1e-18)
+
+
+def _sources_near_sigma(n=300, seed=21):
+    """Opinions spread log-uniformly over [σ, 100σ] plus a third exact zeros:
+    most z_v lie in (σ, 100σ), where ε' = σε/(c+σ) and ε' = ε give different
+    bands (Lemma 5)."""
+    rp, col, w = G.random_undirected(n, 0.02, seed)
+    rng = np.random.default_rng(seed)
+    s = (oracle.SIGMA * 10 ** rng.uniform(0, 2, n)).astype(np.float32)
+    s[rng.choice(n, n // 3, replace=False)] = 0.0
+    return rp, col, w, s
+
+
+@pytest.mark.parametrize("eps", [1e-2, 1e-4])
+def test_lemma5_relative_bound_near_sigma(eps):
+    """Lemma 5: ImprovedBLI with c = σ and ε' = σε/(c+σ)
+    gives (1−ε)z ≤ ẑ ≤ z for every z_v ≥ σ, against dense GE.  The shifted
+    system's residual at termination is ≤ h = ε'·s' (Alg. 1 stops when no
+    r_u > h_u; h per Alg. 2, P:340 with reading R4), checked with
+    the dense matrix and ε' computed here — a slip to ε' = ε leaves residuals
+    up to 2h (the realized max is ≈ 0.99h) and fails this test."""
+    rp, col, w, s = _sources_near_sigma()
+    sig = oracle.SIGMA
+    z = oracle.dense_solve(rp, col, w, s)
+    res = oracle.solve(rp, col, w, s, eps, 1.0)
+    assert res.status == 0
+    big = z >= sig
+    assert big.sum() > 150
+    assert np.all(res.z[big] <= z[big] + 1e-18)
+    assert np.all(z[big] - res.z[big] <= eps * z[big])
+    c = sig                                       # s ≥ 0: c = σ (P:625)
+    sp = s.astype(np.float64) + c                 # s' = s + c (P:339)
+    h = sig * eps / (c + sig) * sp                # ε' s' (P:337, P:340)
+    R = sp - oracle.dense_system(rp, col, w) @ res.zprime
+    assert R.max() <= h.max() and np.all(R <= h * (1 + 1e-9) + 1e-18)
+    assert np.all(R >= -1e-16)    # Lemma 4: r stays ≥ 0 at ω = 1 (dense matvec rounding ≈ 1e-18)
 
 
 @pytest.mark.parametrize("omega", [1.0, 1.5])
@@ -284,3 +326,83 @@ def test_measures_directed_arc_once():
     assert oracle.measures(rp, col, w, z, directed=True)["D"] == pytest.approx(2 * 1 + 1 * 9)
     rp, col, w = G.in_csr_from_edges(2, [(0, 1)])
     assert oracle.measures(rp, col, w, np.array([1.0, 0.0]), directed=False)["D"] == 1.0
+
+
+# ------------------------------------------------------ ω heuristic
+def _mu_numpy(rp, col, w):
+    """μ = ρ((I+D)^{-1}A) with numpy's eigenvalue routine on A built
+    here from the arcs (independent of oracle.dense_system)."""
+    n = len(rp) - 1
+    A = np.zeros((n, n))
+    for v in range(n):
+        for e in range(rp[v], rp[v + 1]):
+            A[col[e], v] = 1.0 if w is None else float(w[e])
+    J = A / (1.0 + A.sum(axis=1))[:, None]
+    return float(np.max(np.abs(np.linalg.eigvals(J))))
+
+
+OMEGA_CASES = [  # (name, graph, speed-up over ω = 1 the SOR theory leaves room for)
+    ("grid24", lambda: G.in_csr_from_edges(576, G.grid_edges(24)), 1.5),
+    ("path200", lambda: G.in_csr_from_edges(200, [(i, i + 1) for i in range(199)]), 1.3),
+    ("er400", lambda: G.random_undirected(400, 0.025, 15), 3.0),
+]
+
+
+@pytest.mark.parametrize("name,mk,gain", OMEGA_CASES, ids=[c[0] for c in OMEGA_CASES])
+def test_omega_sweep_near_omega_opt(name, mk, gain):
+    """The fewest-updates heuristic lands next to the SOR optimum
+    ω_opt = 1 + (μ/(1+√(1−μ²)))² (Eq. optimal-omega; Young's theorem
+    for consistently ordered SPD systems) with μ from numpy's eigenvalues —
+    grid 1.25, path 1.15, ER 1.41 — and beats ω = 1 (by ≥ 3× on the random
+    graph, P:488's "more than approximately three times"; the path's small μ
+    leaves SOR less room)."""
+    rp, col, w = mk()
+    n = len(rp) - 1
+    s = np.random.default_rng(1).random(n).astype(np.float32)
+    best, table = oracle.omega_sweep(rp, col, w, s, 1e-6, prune=False)
+    mu = _mu_numpy(rp, col, w)
+    w_opt = 1.0 + (mu / (1.0 + np.sqrt(1.0 - mu * mu))) ** 2
+    assert abs(best - w_opt) <= 0.1, (best, w_opt)
+    cost = {om: c for om, c, _ in table}
+    assert [om for om, _, _ in table] == oracle.omega_grid()          # 1.95 → 1.00
+    assert cost[1.0] >= gain * cost[best]
+    assert cost[best] == min(cost.values())
+    # pruning only drops runs that cannot win: same pick, same winning count
+    best2, table2 = oracle.omega_sweep(rp, col, w, s, 1e-6, prune=True)
+    assert best2 == best and dict((o, c) for o, c, _ in table2)[best] == cost[best]
+
+
+def test_omega_sweep_skips_divergence():
+    """Directed graphs: SOR over-relaxation may diverge (P:484 covers only
+    the symmetric case; reading R11); the heuristic gives such ω cost +∞
+    and picks a converging ω, which still meets the ε band against dense GE."""
+    rp, col, w = G.random_directed(200, 0.03, 4)
+    s = np.random.default_rng(1).random(200).astype(np.float32)
+    best, table = oracle.omega_sweep(rp, col, w, s, 1e-6, prune=False)
+    diverged = [om for om, c, st in table if st == "diverged"]
+    assert 1.95 in diverged and best not in diverged
+    res = oracle.solve(rp, col, w, s, 1e-6, best)
+    z = oracle.dense_solve(rp, col, w, s)
+    assert res.status == 0
+    assert np.all(np.abs(res.z - z) <= 1e-6 * np.maximum(np.abs(z), oracle.SIGMA))
+    mu = _mu_numpy(rp, col, w)
+    assert abs(best - (1.0 + (mu / (1.0 + np.sqrt(1.0 - mu * mu))) ** 2)) <= 0.1
+
+
+def test_omega_sweep_ties_to_smaller():
+    """Ties go to the smaller ω (reading R10): with an empty graph every
+    node is its own component, z = s, and one push at ω = 1 is exact while any
+    other ω needs more — so the pick is 1.0 on a grid whose every other point
+    costs more, and a single-point grid returns that point."""
+    rp = np.zeros(6, np.int64)
+    col = np.zeros(0, np.int32)
+    s = np.array([0.1, 0.2, 0.3, 0.4, 0.5], np.float32)
+    best, table = oracle.omega_sweep(rp, col, None, s, 1e-6, prune=False)
+    cost = {om: c for om, c, _ in table}
+    assert best == 1.0 and cost[1.0] == 5
+    assert all(c > 5 for om, c in cost.items() if om != 1.0)
+    # a symmetric pair: |1 − ω| equal for ω = 0.9 and 1.1 ⇒ equal pop counts
+    best, table = oracle.omega_sweep(rp, col, None, s, 1e-6, lo=0.9, hi=1.1, step=0.2,
+                                     prune=False)
+    assert [om for om, _, _ in table] == [1.1, 0.9]
+    assert table[0][1] == table[1][1] and best == 0.9

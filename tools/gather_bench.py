@@ -1,0 +1,55 @@
+"""Gather ceilings on config 4's pull CSR (diagnostics): scalar vs 128-bit
+stream loads, and the H most popular columns served from shared memory.
+usage: python tools/gather_bench.py [CID]"""
+import ctypes, os, subprocess, sys
+import numpy as np, torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import fjgen  # noqa: E402
+so = os.path.join(ROOT, "build", "libgb.so")
+src = os.path.join(ROOT, "tools", "gather_bench.cu")
+os.makedirs(os.path.dirname(so), exist_ok=True)
+if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+    subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a",
+                           "-O3", "-shared", "-Xcompiler", "-fPIC", "-o", so, src])
+L = ctypes.CDLL(so)
+L.gb_run.restype = ctypes.c_float
+L.gb_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 3 + \
+    [ctypes.c_int] * 5
+cid = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+p = fjgen.config(cid)
+dev = torch.device("cuda:0")
+col = torch.from_numpy(p.col).to(dev)
+rows = torch.repeat_interleave(torch.arange(p.n, device=dev, dtype=torch.int32),
+                               torch.from_numpy(np.diff(p.row_ptr)).to(dev))
+key, idx = torch.sort(col, stable=True)
+ocol = rows[idx].contiguous()            # pull-CSR columns, rows by u
+w = None if p.w is None else torch.from_numpy(p.w).to(dev)[idx].contiguous()
+m = (p.m // 4) * 4
+cnt = torch.bincount(ocol.long(), minlength=p.n)
+order = torch.argsort(cnt, descending=True, stable=True)
+newid = torch.empty_like(order)
+newid[order] = torch.arange(p.n, device=dev)
+rcol = newid[ocol.long()].int().contiguous()          # columns relabelled by popularity
+x = torch.rand(p.n, dtype=torch.float64, device=dev)
+cum = torch.cumsum(cnt[order].double(), 0) / p.m
+wp = 0 if w is None else w.data_ptr()
+
+
+def run(vec, hot, c, H=0, thr=256, carve=-1, extra=0, reps=10):
+    return L.gb_run(vec, hot, m, c.data_ptr(), wp, x.data_ptr(), H, thr, carve, reps, extra)
+
+
+print(f"{p.name}: m={p.m}")
+for name, c in (("raw ids", ocol), ("popularity ids", rcol)):
+    for vec in (1, 4):
+        print(f"  {name:15s} vec{vec} no hot 4x256       {run(vec, 0, c):.3f} ms", flush=True)
+for extra in (0, 32768, 65536):
+    for H in (4096, 8192, 12288, 16384, 20480, 24576):
+        if H * 8 + extra > 227 * 1024:
+            continue
+        cov = float(cum[H - 1])
+        for thr in (1024, 512):
+            t = run(4, 1, rcol, H, thr, -1, extra)
+            print(f"  hot H={H:6d} ({cov:.3f} of arcs) extra={extra // 1024:3d}KB thr={thr:4d}: "
+                  f"{t:.3f} ms", flush=True)
