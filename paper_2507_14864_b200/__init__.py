@@ -133,12 +133,23 @@ def _ptr(a):
     return ctypes.c_void_p(a.ctypes.data)
 
 
-def _dtype_ok(a, name: str, kind: str):
+def _dtype_ok(a, name: str, kind: str, numel: int | None = None):
+    """dtype check, and (``numel``) the element count the library will read or
+    write through the pointer: a short buffer would be overrun on the device
+    or, for host outputs, by the device→host copy."""
     if a is None:
         return
     dt = str(a.dtype)
     if kind not in dt:
         raise TypeError(f"{name} must be {kind}, got {dt}")
+    if numel is not None:
+        got = int(a.numel()) if hasattr(a, "numel") else int(a.size)
+        if got < numel:
+            raise ValueError(f"{name} has {got} elements, the call needs {numel}")
+        if hasattr(a, "is_contiguous") and not a.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if hasattr(a, "flags") and not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name} must be C-contiguous")
 
 
 def _stream_of(*arrays):
@@ -176,11 +187,11 @@ class Graph:
     in-CSR (row v lists the u with an arc u→v, u listens to v)."""
 
     def __init__(self, n, row_ptr, col, w=None, directed=True, stream=None):
-        _dtype_ok(row_ptr, "row_ptr", "int64")
-        _dtype_ok(col, "col", "int32")
-        _dtype_ok(w, "w", "float32")
+        _dtype_ok(row_ptr, "row_ptr", "int64", int(n) + 1)
+        nnz = int(row_ptr[int(n)])
+        _dtype_ok(col, "col", "int32", nnz)
+        _dtype_ok(w, "w", "float32", nnz)
         self._h = ctypes.c_void_p()
-        nnz = int(row_ptr[-1])
         st = stream if stream is not None else _stream_of(row_ptr, col, w)
         _check(lib().fj_graph_create(int(n), nnz, _ptr(row_ptr), _ptr(col), _ptr(w),
                                      1 if directed else 0, st, ctypes.byref(self._h)))
@@ -216,16 +227,16 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
           z_init=None) -> SolveStats:
     """fj_solve_ex: writes z into ``z_out`` (float32[n]); returns the stats.
     ``z_init`` (float64[n], optional): warm start / resume from an earlier z."""
-    _dtype_ok(s, "s", "float32")
-    _dtype_ok(z_out, "z_out", "float32")
-    _dtype_ok(zprime_out, "zprime_out", "float64")
+    _dtype_ok(s, "s", "float32", g.n)
+    _dtype_ok(z_out, "z_out", "float32", g.n)
+    _dtype_ok(zprime_out, "zprime_out", "float64", g.n)
     o = _Opts()
     lib().fj_opts_default(ctypes.byref(o))
     o.sigma, o.c, o.method = sigma, c, METHODS[method]
     o.max_sweeps, o.cert_rounds, o.certify = max_sweeps, cert_rounds, int(certify)
     zp = _ptr(zprime_out)
     o.zprime_out = zp.value if zp is not None else None
-    _dtype_ok(z_init, "z_init", "float64")
+    _dtype_ok(z_init, "z_init", "float64", g.n)
     zi = _ptr(z_init)
     o.z_init = zi.value if zi is not None else None
     st = _Stats()
@@ -241,8 +252,8 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
 def solve_batch(g: Graph, S, Z_out, k: int, eps: float, omega: float = 1.0,
                 sigma: float = 1e-5, max_sweeps: int = 0, raise_on_numeric: bool = True) -> SolveStats:
     """fj_solve_batch: k opinion vectors (node-major fp32[n*k]) in one solve."""
-    _dtype_ok(S, "S", "float32")
-    _dtype_ok(Z_out, "Z_out", "float32")
+    _dtype_ok(S, "S", "float32", g.n * int(k))
+    _dtype_ok(Z_out, "Z_out", "float32", g.n * int(k))
     o = _Opts()
     lib().fj_opts_default(ctypes.byref(o))
     o.sigma, o.max_sweeps = sigma, max_sweeps
@@ -263,8 +274,8 @@ def solve_simple(g: Graph, s, z_out, eps: float, omega: float = 1.0):
 
 def measures(g: Graph, z, s=None) -> dict:
     """fj_measures_ex: P, D (and I, C) of Table tab:measures."""
-    _dtype_ok(z, "z", "float32")
-    _dtype_ok(s, "s", "float32")
+    _dtype_ok(z, "z", "float32", g.n)
+    _dtype_ok(s, "s", "float32", g.n)
     m = _Measures()
     _check(lib().fj_measures_ex(g._h, _ptr(z), _ptr(s), ctypes.byref(m)))
     return dict(P=m.polarization, D=m.disagreement, I=m.internal_conflict, C=m.controversy)
@@ -272,6 +283,7 @@ def measures(g: Graph, z, s=None) -> dict:
 
 def measures_pd(g: Graph, z):
     """The plain ABI call fj_measures(graph, z, &P, &D)."""
+    _dtype_ok(z, "z", "float32", g.n)
     P, D = ctypes.c_double(), ctypes.c_double()
     _check(lib().fj_measures(g._h, _ptr(z), ctypes.byref(P), ctypes.byref(D)))
     return P.value, D.value

@@ -73,7 +73,8 @@ __device__ __forceinline__ void do_warpK(const KP &p, const Scalars *SK, const T
       const int64_t k = k0 + 32 * u;
       const bool ok = k < a1;
       j[u] = ld_stream(p.col + (ok ? k : a0));
-      wv[u] = ok ? (W ? ld_stream(p.w + k) : 1.0f) : 0.0f;
+      wv[u] = W ? ld_stream(p.w + (ok ? k : a0)) : 1.0f;  // clamped: never speculate past the row
+      if (!ok) wv[u] = 0.0f;
     }
     double zj[U][K];
 #pragma unroll
@@ -103,16 +104,14 @@ __device__ __forceinline__ void do_warpK(const KP &p, const Scalars *SK, const T
 #pragma unroll
     for (int r = 0; r < K; r++)
       __stcg(p.partial + ((int64_t)slot + piece) * K + r, make_double2(a[r].hi, a[r].lo));
-    __threadfence();
-    const int old = atomicAdd(p.arrive + slot, 1);
+    const int old = arrive_release(p.arrive + slot);  // no L1 flush (sweep_common.cuh)
     if ((old + 1) % np != 0) return;
-    __threadfence();
 #pragma unroll
     for (int r = 0; r < K; r++) a[r] = dd{0.0, 0.0};
     for (int q = 0; q < np; q++)
 #pragma unroll
       for (int r = 0; r < K; r++) {
-        const double2 x = __ldcg(p.partial + ((int64_t)slot + q) * K + r);
+        const double2 x = ld_partial(p.partial + ((int64_t)slot + q) * K + r);
         acc_merge(a[r], dd{x.x, x.y});
       }
   }

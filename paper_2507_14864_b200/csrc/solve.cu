@@ -229,13 +229,11 @@ __device__ __forceinline__ void relax_stream(const KP &p, const Scalars &S, int 
           bool finish = true;
           if (np > 1) {
             __stcg(p.partial + T.slot + T.b, make_double2(acc.hi, acc.lo));
-            __threadfence();
-            finish = (atomicAdd(p.arrive + T.slot, 1) + 1) % np == 0;
+            finish = (arrive_release(p.arrive + T.slot) + 1) % np == 0;
             if (finish) {
-              __threadfence();
               acc = dd{0.0, 0.0};
               for (int q = 0; q < np; q++) {
-                const double2 x = __ldcg(p.partial + T.slot + q);
+                const double2 x = ld_partial(p.partial + T.slot + q);
                 acc_merge(acc, dd{x.x, x.y});
               }
             }
@@ -478,7 +476,6 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   FJ_CUDA(ws.alloc(&S, 1));
   FJ_CUDA(ws.alloc(&partial, std::max(1, L.npartials)));
   FJ_CUDA(ws.alloc(&arrive, std::max(1, L.npartials)));
-  FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
   FJ_CUDA(ws.alloc(&ctl, kCtlWords));
   FJ_CUDA(ws.alloc(&cnt, 3));
   FJ_CUDA(ws.alloc(&outv, 8));
@@ -566,6 +563,9 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     FJ_CUDA(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * kCtlWords, st));
     FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(SweepCounters) * 3, st));
     FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 8, st));
+    // hub-piece arrival counters start at 0 for every launch (a resumed
+    // sweep or the certificate never inherits a half-finished count)
+    FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
     FJ_CUDA(cudaEventRecord(es0, st));
     if (barrier_free) {
       FJ_CUDA(cudaMemsetAsync(actl, 0, sizeof(AsyncCtl), st));
@@ -584,6 +584,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     if (o->certify) {
       KP q = p;
       q.ctr = ctl + 5;
+      FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
       FJ_CUDA(cudaEventRecord(ec0, st));
       const void *cf = W ? (const void *)k_pass<CERT, true> : (const void *)k_pass<CERT, false>;
       void *cargs[] = {&q};

@@ -101,6 +101,31 @@ __device__ __forceinline__ float ld_stream(const float *q) {
 // (weak loads: the compiler may batch them; __ldca compiles to a strong load)
 __device__ __forceinline__ double ld_z(const double *q) { return *q; }
 
+// Hub-row pieces (see do_warp): a piece's partial sum is stored, then its
+// arrival is counted with release semantics (MEMBAR.ALL.GPU orders the store
+// before the atomic; unlike __threadfence / acquire operations it emits no
+// CCTL.IVALL, so L1 keeps its cached ẑ lines).  The last-arriving warp reads
+// the partials with gpu-scope strong loads, which are served by L2 — the point
+// of coherence the releasing stores have reached — never by a stale L1 line.
+__device__ __forceinline__ int arrive_release(int *q) {
+#ifdef FJ_OLD_FENCE
+  __threadfence();
+  const int old = atomicAdd(q, 1);
+  __threadfence();
+  return old;
+#else
+  int old;
+  asm volatile("atom.add.release.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(q) : "memory");
+  return old;
+#endif
+}
+__device__ __forceinline__ double2 ld_partial(const double2 *q) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(q)
+               : "memory");
+  return v;
+}
+
 struct dd {
   double hi, lo;
 };
@@ -342,17 +367,18 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
   } else {
     if (np > 1) {
       __stcg(p.partial + slot + piece, make_double2(a.hi, a.lo));
-      __threadfence();
       // cumulative arrival count: the np-th, 2np-th, ... arrival finishes the
       // row (no reset, so overlapping sweeps of the barrier-free kernel can
       // never lose an arrival; mixing partials of two sweeps is still a
-      // valid relaxation amount by Lemma 3 and the certificate decides)
-      const int old = atomicAdd(p.arrive + slot, 1);
+      // valid relaxation amount by Lemma 3 and the certificate decides).
+      // Release arrival + L2 (gpu-scope) reads of the partials: no
+      // __threadfence, whose CCTL.IVALL would wipe this SM's L1 — the home of
+      // the hub ẑ gathers — once per hub piece.
+      const int old = arrive_release(p.arrive + slot);
       if ((old + 1) % np != 0) return;
-      __threadfence();
       acc_zero(a);
       for (int q = 0; q < np; q++) {  // fixed order ⇒ deterministic row sum
-        const double2 x = __ldcg(p.partial + slot + q);
+        const double2 x = ld_partial(p.partial + slot + q);
         acc_merge(a, dd{x.x, x.y});
       }
     }
@@ -604,10 +630,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_pass(KP p) {
       cert_row<W>(p, S, (int)row, 0, dd{0.0, 0.0}, t);
   }
   if constexpr (MODE == CERT) {
+    // NaN-propagating warp max: a non-finite residual in any lane must fail
+    // the certificate (fmax would drop it)
     double m = t.certmax;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if (isnan(t.certmax)) m = t.certmax;
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, m, off);
+      m = (isnan(o) || o > m) ? o : m;
+    }
     if ((threadIdx.x & 31) == 0 && m != 0.0)
       atomicMax(p.cert_max, (unsigned long long)__double_as_longlong(m));
   } else if constexpr (MODE == DIS) {

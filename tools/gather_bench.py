@@ -44,12 +44,19 @@ print(f"{p.name}: m={p.m}")
 for name, c in (("raw ids", ocol), ("popularity ids", rcol)):
     for vec in (1, 4):
         print(f"  {name:15s} vec{vec} no hot 4x256       {run(vec, 0, c):.3f} ms", flush=True)
-for extra in (0, 32768, 65536):
-    for H in (4096, 8192, 12288, 16384, 20480, 24576):
-        if H * 8 + extra > 227 * 1024:
-            continue
+import math
+for extra in (0, 32768):
+    for H in (4096, 8192, 12288, 16384, 20480):
+        need = H * 8 + extra
         cov = float(cum[H - 1])
-        for thr in (1024, 512):
-            t = run(4, 1, rcol, H, thr, -1, extra)
-            print(f"  hot H={H:6d} ({cov:.3f} of arcs) extra={extra // 1024:3d}KB thr={thr:4d}: "
-                  f"{t:.3f} ms", flush=True)
+        for carve in (math.ceil(100 * (need + 2048) / (228 * 1024)), 100):
+            if carve > 100:
+                continue
+            ts = [run(4, 1, rcol, H, 1024, carve, extra) for _ in range(3)]
+            print(f"  hot H={H:6d} ({cov:.3f} of arcs) extra={extra // 1024:3d}KB carve={carve:3d}%: "
+                  + " ".join(f"{t:.3f}" for t in ts) + " ms", flush=True)
+for carve in (0, 25, 50, 75, 100):
+    ts = [run(4, 0, rcol, 0, 256, carve, 0) for _ in range(3)]
+    print(f"  no hot 4x256 carve={carve:3d}%: " + " ".join(f"{t:.3f}" for t in ts) + " ms", flush=True)
+    ts = [run(4, 0, rcol, 0, 1024, carve, 0) for _ in range(3)]
+    print(f"  no hot 1x1024 carve={carve:3d}%: " + " ".join(f"{t:.3f}" for t in ts) + " ms", flush=True)
