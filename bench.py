@@ -219,15 +219,34 @@ def cpu_baseline(prob, args):
 
 
 # ----------------------------------------------------------------- our arm
-def algorithmic_bytes(st, weighted: bool):
-    """Bytes the sweep kernel must move: per arc read col (4)
-    + w (4, weighted); per evaluated row rp (8) + s (4) + ẑ (8) + 1+d (8,
-    weighted); per relaxation an 8-byte ẑ write.  ẑ gathers are not counted
-    (L2-resident), which makes `achieved` a lower bound."""
-    per_arc = 8 if weighted else 4
-    per_row = 28 if weighted else 20
-    swept_relax = st.relaxations  # includes init-solved empty rows (no bytes in the sweep)
-    return st.arcs_read * per_arc + st.rows_read * per_row + 8 * swept_relax
+def algorithmic_bytes(st, weighted: bool, empty_rows: int):
+    """SURVEY §8(d)'s algorithmic bytes of the sweep kernel:
+    per edge-update (an arc of a relaxed row, P:488's "updates" × their arcs)
+    col 4 + gathered ẑ_j 4 (+ w 4 weighted) = 8 / 12 B; per relaxation the
+    row's state: row_ptr 8 + s 4 + ẑ_i read 8 + ẑ_i write 8 (+ 1+d 8
+    weighted) = 28 / 36 B.  Rows solved exactly at init (no arcs) move nothing."""
+    per_eu = 12 if weighted else 8
+    per_relax = 36 if weighted else 28
+    swept_relax = st.relaxations - empty_rows
+    return st.edge_updates * per_eu + swept_relax * per_relax
+
+
+def streamed_bytes(st, weighted: bool, empty_rows: int):
+    """What the window sweep actually streams per launch: every arc of every
+    sweep (col 4 + w 4 weighted), one gathered fp64 ẑ_j per arc (8, counted at
+    its useful size), every evaluated row's state (s 4 + ẑ_i 8 + 1+d 8
+    weighted) and one 8-byte write per relaxation."""
+    per_arc = 16 if weighted else 12
+    per_row = 20 if weighted else 12
+    return st.arcs_read * per_arc + st.rows_read * per_row + 8 * (st.relaxations - empty_rows)
+
+
+def lib_fingerprint():
+    """sha256 (16 hex) of the loaded libfj.so: ties an ncu capture to its build."""
+    import hashlib
+    import paper_2507_14864_b200 as fj
+    with open(fj.LIB_PATH, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()[:16]
 
 
 def run_ours(args, prob, world, rank, local):
@@ -278,15 +297,23 @@ def run_ours(args, prob, world, rank, local):
     # roofline of the dominant kernel (k_sweep), CUDA events on the graph stream
     pk = peaks()
     peak = pk["hbm_gbs"] if pk else 6650.0
-    ab = algorithmic_bytes(st0, prob.w is not None)
+    g = fj.Graph(prob.n, rp, col, w, directed=prob.directed)
+    empty_rows = g.info()["empty_rows"]
+    g.close()
+    ab = algorithmic_bytes(st0, prob.w is not None, empty_rows)
+    sb = streamed_bytes(st0, prob.w is not None, empty_rows)
     achieved = ab / (st0.sweep_ms / 1e3) / 1e9
     traffic = None
+    traffic_src = None
     prof = os.path.join(ROOT, "profiles", "ncu_sweep_traffic.json")
     if os.path.exists(prof):
         try:
             # ncu's dram bytes per sweep of its captured launch × this launch's
-            # sweeps (a launch runs as many sweeps as ASYNC needs: 246–253 on C4)
-            traffic = json.load(open(prof))["dram_bytes_per_sweep"] * st0.sweeps
+            # sweeps — only if the capture was taken on this very build
+            tj = json.load(open(prof))
+            if tj.get("lib_sha16") == lib_fingerprint() and args.config == tj.get("config", 4):
+                traffic = tj["dram_bytes_per_sweep"] * st0.sweeps
+                traffic_src = tj.get("source")
         except Exception:
             traffic = None
 
@@ -341,8 +368,13 @@ def run_ours(args, prob, world, rank, local):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
-                         "kernel": "k_sweep (persistent)",
-                         "algorithmic_bytes_per_launch": ab},
+                         "kernel": "k_sweep (persistent window sweep)",
+                         "algorithmic_bytes_per_launch": ab,
+                         "bytes_model": "SURVEY 8(d): 12 B per edge-update (col, w, gathered z_j) "
+                                        "+ 36 B per relaxation (row_ptr, s, z_i r/w, 1+d)",
+                         "streamed_bytes_per_launch": sb,
+                         "streamed_gbs": sb / (st0.sweep_ms / 1e3) / 1e9,
+                         "traffic_source": traffic_src, "lib_sha16": lib_fingerprint()},
             "gather_ceiling": ceiling,
             "batched": batched,
             "omega_sweep": omega_table,
@@ -422,9 +454,9 @@ def run_sharded(args, prob, world, rank, local):
     st0, m0 = stats[-1]
     pk = peaks()
     peak = pk["hbm_gbs"] if pk else 6650.0
-    per_arc = 8 if prob.w is not None else 4
-    per_row = 28 if prob.w is not None else 20
-    ab = st0.arcs_read * per_arc + st0.rows_read * per_row + 8 * st0.relaxations / world
+    # §8(d) bytes of this rank's share (edge updates and relaxations are
+    # all-reduced totals; rows without arcs are ignored here)
+    ab = algorithmic_bytes(st0, prob.w is not None, 0) / world
     achieved = ab / (st0.sweep_ms / 1e3) / 1e9
     comm.close()
     return {"metric": METRIC, "value": eu / (ms / 1e3), "unit": UNIT, "n_gpus": world,

@@ -178,13 +178,16 @@ def zero_mask(s, count, seed):
 # ----------------------------------------------------------------- configs
 CONFIG_SEEDS = {1: 101, 2: 202, 3: 303, 4: 404, 5: 505}
 
-#: solve parameters per config (BASELINE.json configs)
+#: solve parameters per config (BASELINE.json configs).  `tuned`
+#: is reading R10's tuned ω: the paper's fewest-updates heuristic run by
+#: the ORACLE (tests/harness/omega_tune.py → profiles/r02_oracle_omega_tune.jsonl;
+#: values copied from there, no arithmetic here).  C4's ω list is BASELINE's own.
 CONFIG_SOLVE = {
-    1: dict(eps=1e-6, omegas=[1.0, 1.5]),
-    2: dict(eps=1e-6, omegas=[1.0]),
-    3: dict(eps=1e-6, omegas=[1.0]),
-    4: dict(eps=1e-6, omegas=[1.0, 1.2, 1.4, 1.6, 1.8]),
-    5: dict(eps=1e-6, omegas=[1.0, 1.25]),
+    1: dict(eps=1e-6, omegas=[1.0, 1.5], tuned=1.5),
+    2: dict(eps=1e-6, omegas=[1.0, 1.55], tuned=1.55),
+    3: dict(eps=1e-6, omegas=[1.0, 1.6], tuned=1.6),
+    4: dict(eps=1e-6, omegas=[1.0, 1.2, 1.4, 1.6, 1.8], tuned=None),
+    5: dict(eps=1e-6, omegas=[1.0, 1.25, 1.3], tuned=1.3),
 }
 
 

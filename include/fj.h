@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define FJ_ABI_VERSION 1
+#define FJ_ABI_VERSION 2
 
 typedef struct fj_graph *fj_graph_t;
 
@@ -83,6 +83,18 @@ typedef struct {
                         recomputed from ẑ); the ε rule and certificate are unchanged.
                         ASYNC/COLORED only (FJ_ERR_INVALID with PUSH).  NULL = start at 0
                         as Alg. 1 does                                           */
+  /* Schedule options (defaults from fj_opts_default; none changes what is computed,
+     only the order of relaxations, which Lemma 3 leaves free): */
+  double tail_frac;  /* COLORED: colors after the first K whose rows total ≤ tail_frac·n
+                        are merged into one bounded asynchronous phase (reading R23);
+                        < 0 → 0.01, 0 → no merge (exact multicolor SOR)                 */
+  int coloring;      /* COLORED: 0 = speculative first-fit in largest-first degree
+                        buckets (default), 1 = Jones–Plassmann (degree priority)        */
+  int push_compact;  /* PUSH: 1 = compacted frontier (ballot + slots), 0 = dense (default)*/
+  int push_sparse_div; /* PUSH compacted: walk the list once the last sweep relaxed
+                        < n / push_sparse_div rows; <= 0 → 8                            */
+  /* The coloring and tail merge are built at the first COLORED solve of a graph and
+     rebuilt if a later solve asks for a different coloring or tail_frac. */
 } fj_opts;
 
 typedef struct {
@@ -248,6 +260,11 @@ fj_status fj_comm_create(const void *id128, int rank, int world, fj_comm_t *out)
 /* In-process transport: all `world` ranks are shards of this process on the
    current device. */
 fj_status fj_comm_create_local(int world, fj_comm_t *out);
+/* As fj_comm_create_local, but the exchange runs the NCCL path's own bookkeeping
+   (count matrix, send lists, pack kernel, per-peer segments) and only replaces
+   each ncclSend/ncclRecv pair by a device copy: the multi-rank path minus NCCL
+   itself, testable on one GPU. */
+fj_status fj_comm_create_loopback(int world, fj_comm_t *out);
 /* Destroy a comm after every shard created on it. */
 fj_status fj_comm_destroy(fj_comm_t c);
 

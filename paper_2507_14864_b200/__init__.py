@@ -26,7 +26,8 @@ EXPORTS = ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve
            "fj_measures", "fj_measures_ex", "fj_opts_default", "fj_last_error",
            "fj_abi_version", "fj_kernel_launches", "fj_omega_opt", "fj_omega_sweep",
            "fj_solve_batch", "fj_shard_plan", "fj_comm_unique_id", "fj_comm_create",
-           "fj_comm_create_local", "fj_comm_destroy", "fj_shard_create", "fj_shard_connect",
+           "fj_comm_create_local", "fj_comm_create_loopback", "fj_comm_destroy", "fj_shard_create",
+           "fj_shard_connect",
            "fj_shard_solve", "fj_shard_measures", "fj_shard_destroy", "fj_shard_info", "fj_gather_probe")
 
 
@@ -40,7 +41,9 @@ class _Opts(ctypes.Structure):
     _fields_ = [("sigma", ctypes.c_double), ("c", ctypes.c_double), ("method", ctypes.c_int),
                 ("max_sweeps", ctypes.c_int), ("cert_rounds", ctypes.c_int),
                 ("certify", ctypes.c_int), ("zprime_out", ctypes.c_void_p),
-                ("z_init", ctypes.c_void_p)]
+                ("z_init", ctypes.c_void_p), ("tail_frac", ctypes.c_double),
+                ("coloring", ctypes.c_int), ("push_compact", ctypes.c_int),
+                ("push_sparse_div", ctypes.c_int)]
 
 
 class _Stats(ctypes.Structure):
@@ -95,6 +98,7 @@ def lib():
         L.fj_comm_unique_id.argtypes = [P]
         L.fj_comm_create.argtypes = [P, i, i, PP]
         L.fj_comm_create_local.argtypes = [i, PP]
+        L.fj_comm_create_loopback.argtypes = [i, PP]
         L.fj_comm_destroy.argtypes = [P]
         L.fj_shard_create.argtypes = [P, i, i64, P, P, P, P, i, PP]
         L.fj_shard_connect.argtypes = [PP, i]
@@ -107,7 +111,8 @@ def lib():
         for f in ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve",
                   "fj_solve_ex", "fj_measures", "fj_measures_ex", "fj_omega_opt",
                   "fj_omega_sweep", "fj_solve_batch", "fj_shard_plan", "fj_comm_unique_id",
-                  "fj_comm_create", "fj_comm_create_local", "fj_comm_destroy",
+                  "fj_comm_create", "fj_comm_create_local", "fj_comm_create_loopback",
+                  "fj_comm_destroy",
                   "fj_shard_create", "fj_shard_connect", "fj_shard_solve",
                   "fj_shard_measures", "fj_shard_destroy", "fj_gather_probe", "fj_shard_info"):
             getattr(L, f).restype = i
@@ -224,9 +229,13 @@ class Graph:
 def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "auto",
           sigma: float = 1e-5, c: float = 0.0, max_sweeps: int = 0, cert_rounds: int = -1,
           certify: bool = True, zprime_out=None, raise_on_numeric: bool = True,
-          z_init=None) -> SolveStats:
+          z_init=None, tail_frac: float = -1.0, coloring: str = "spec",
+          push_compact: bool = False, push_sparse_div: int = 8) -> SolveStats:
     """fj_solve_ex: writes z into ``z_out`` (float32[n]); returns the stats.
-    ``z_init`` (float64[n], optional): warm start / resume from an earlier z."""
+    ``z_init`` (float64[n], optional): warm start / resume from an earlier z.
+    Schedule options (fj_opts): ``tail_frac`` (COLORED tail merge, R23; 0 =
+    exact multicolor SOR), ``coloring`` ("spec" or "jp"), ``push_compact`` /
+    ``push_sparse_div`` (PUSH frontier)."""
     _dtype_ok(s, "s", "float32", g.n)
     _dtype_ok(z_out, "z_out", "float32", g.n)
     _dtype_ok(zprime_out, "zprime_out", "float64", g.n)
@@ -234,6 +243,8 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
     lib().fj_opts_default(ctypes.byref(o))
     o.sigma, o.c, o.method = sigma, c, METHODS[method]
     o.max_sweeps, o.cert_rounds, o.certify = max_sweeps, cert_rounds, int(certify)
+    o.tail_frac, o.coloring = float(tail_frac), {"spec": 0, "jp": 1}[coloring]
+    o.push_compact, o.push_sparse_div = int(bool(push_compact)), int(push_sparse_div)
     zp = _ptr(zprime_out)
     o.zprime_out = zp.value if zp is not None else None
     _dtype_ok(z_init, "z_init", "float64", g.n)
@@ -344,9 +355,12 @@ class Comm:
         self._h, self.world, self.rank, self.in_process_ = h, world, rank, in_process
 
     @classmethod
-    def in_process(cls, world: int) -> "Comm":
+    def in_process(cls, world: int, loopback: bool = False) -> "Comm":
+        """All shards in this process.  ``loopback``: run the NCCL path's send
+        lists and pack kernel with device copies in place of NCCL (tests)."""
         h = ctypes.c_void_p()
-        _check(lib().fj_comm_create_local(int(world), ctypes.byref(h)))
+        fn = lib().fj_comm_create_loopback if loopback else lib().fj_comm_create_local
+        _check(fn(int(world), ctypes.byref(h)))
         return cls(h, int(world), 0, True)
 
     @classmethod

@@ -77,6 +77,10 @@ void fj_opts_default(fj_opts *o) {
   o->certify = 1;
   o->zprime_out = nullptr;
   o->z_init = nullptr;
+  o->tail_frac = -1.0;
+  o->coloring = 0;
+  o->push_compact = 0;
+  o->push_sparse_div = 8;
 }
 
 fj_status fj_graph_get_info(fj_graph_t g, fj_graph_info *info) {

@@ -113,14 +113,12 @@ __global__ void k_color_clamp(int64_t n, int32_t *__restrict__ c, int K) {
 // |1−ω_i| + ω_i β_i < 1, i.e. ‖T‖_∞ < 1, the Chazan–Miranker condition under
 // which asynchronous relaxation of the block converges whatever the update
 // order and staleness.  K = the smallest index whose tail holds at most
-// FJ_TAIL_FRAC (default 1%) of the rows; 0 disables the merge.
-static fj_status merge_tail_colors(fj_graph *g) {
+// fj_opts.tail_frac (default 1%) of the rows; 0 disables the merge.
+static fj_status merge_tail_colors(fj_graph *g, double frac) {
   cudaStream_t st = g->stream;
   const int nc = g->ncolors;
   g->ncolors_raw = nc;
   g->tail_color = -1;
-  double frac = 0.01;
-  if (const char *e = getenv("FJ_TAIL_FRAC")) frac = atof(e);
   if (!(frac > 0.0) || nc <= 2 || nc > 6000) return FJ_OK;
   Workspace ws(st);
   unsigned long long *cnt = nullptr;
@@ -362,9 +360,20 @@ static fj_status spec_coloring(fj_graph *g, Workspace &ws, const int64_t *orp, c
   return FJ_OK;
 }
 
-fj_status build_coloring(fj_graph *g) {
+fj_status build_coloring(fj_graph *g, const fj_opts *o) {
+  const double frac = o->tail_frac < 0 ? 0.01 : o->tail_frac;
+  const int algo = o->coloring == 1 ? 1 : 0;
+  if (g->colors && g->color_tail_frac == frac && g->color_algo == algo) return FJ_OK;
   cudaStream_t st = g->stream;
   const int64_t n = g->n;
+  if (g->colors) {  // other options: drop the old coloring and its layouts
+    cudaFreeAsync(g->colors, st);
+    g->colors = nullptr;
+    g->color_layout.release(st);
+    g->push_color_layout.release(st);
+  }
+  g->color_tail_frac = frac;
+  g->color_algo = algo;
   Workspace ws(st);  // the pull CSR and the round buffers; the colors go to g
   // the pull CSR: for an undirected graph it IS the canonical in-CSR (graph
   // create checked the symmetry), so only directed graphs transpose again
@@ -380,7 +389,7 @@ fj_status build_coloring(fj_graph *g) {
     ocol = t_col;
     ow = t_w;
   }
-  const bool jp = getenv("FJ_COLORING") && !strcmp(getenv("FJ_COLORING"), "jp");
+  const bool jp = algo == 1;
   if (!jp) {
     int32_t *cs = nullptr;
     FJ_CUDA(ws.alloc(&cs, (size_t)n));
@@ -389,12 +398,13 @@ fj_status build_coloring(fj_graph *g) {
     // undirected: the in-CSR already holds both directions of every edge
     FJ_TRY(spec_coloring(g, ws, g->directed ? ort : nullptr, g->directed ? ocol : nullptr, cs, &nc,
                          &rounds));
-    if (getenv("FJ_DEBUG")) fprintf(stderr, "fj coloring: %d speculative rounds, %d colors\n",
-                                    rounds, nc);
+#ifdef FJ_DIAG
+    fprintf(stderr, "fj coloring: %d speculative rounds, %d colors\n", rounds, nc);
+#endif
     ws.keep(cs);
     g->ncolors = nc;
     g->colors = cs;
-    FJ_TRY(merge_tail_colors(g));
+    FJ_TRY(merge_tail_colors(g, frac));
     fj_status s = build_layout_from_out(g, ort, ocol, ow, g->colors, g->ncolors, &g->color_layout);
     if (s == FJ_OK) s = tail_bounds(g, &g->color_layout);
     FJ_CUDA(cudaStreamSynchronize(st));
@@ -421,21 +431,24 @@ fj_status build_coloring(fj_graph *g) {
     FJ_CUDA(cudaMemcpyAsync(c0, c1, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
     FJ_CUDA(cudaMemcpyAsync(&left, rem, sizeof(left), cudaMemcpyDeviceToHost, st));
     FJ_CUDA(cudaStreamSynchronize(st));
-    if (getenv("FJ_DEBUG") && (rounds < 64 || rounds % 100 == 0))
-      fprintf(stderr, "fj JP round %d: %llu vertices left\n", rounds, left);
+#ifdef FJ_DIAG
+    if (rounds < 64 || rounds % 100 == 0) fprintf(stderr, "fj JP round %d: %llu vertices left\n", rounds, left);
+#endif
     if (++rounds > 1000000) {
       set_error("coloring did not terminate");
       return FJ_ERR_CUDA;
     }
   }
-  if (getenv("FJ_DEBUG")) fprintf(stderr, "fj coloring: %d JP rounds\n", rounds);
+#ifdef FJ_DIAG
+  fprintf(stderr, "fj coloring: %d JP rounds\n", rounds);
+#endif
   int hmax = 0;
   FJ_CUDA(cudaMemcpyAsync(&hmax, maxc, sizeof(int), cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));
   ws.keep(c0);
   g->ncolors = hmax + 1;
   g->colors = c0;
-  FJ_TRY(merge_tail_colors(g));
+  FJ_TRY(merge_tail_colors(g, frac));
   fj_status s = build_layout_from_out(g, ort, ocol, ow, g->colors, g->ncolors, &g->color_layout);
   if (s == FJ_OK) s = tail_bounds(g, &g->color_layout);
   FJ_CUDA(cudaStreamSynchronize(st));

@@ -36,6 +36,8 @@ constexpr int kTileArcs = 2048;       // max arcs of one CTA tile task (smem pro
 #endif
 constexpr int kWarpTileArcs = FJ_WT_ARCS;  // max arcs of one warp tile (8 per lane)
 constexpr int kNumClasses = 8;        // row-length classes of the layout
+constexpr int64_t kStreamPad = 264;   // zero-filled col/w slots after the last arc (16-byte
+                                      // sweep loads may run up to 259 slots past a tile start)
 constexpr int64_t kChunkArcs = 2048;  // chunked row walks: pieces of long 32-row chunks
 
 // Chunked row walks (graph build, layout copy): a warp owns 32 consecutive
@@ -113,7 +115,6 @@ struct Layout {
   int64_t active_rows = 0;        // rows with L > 0
   int64_t max_len = 0;
   int64_t warp_unit_arcs = 0;     // arcs in rows handled by warp units (> kWarpTileArcs)
-  bool stream_tma = false;        // sweep streams arcs with TMA (see solve.cu)
   int piece = kWarpPiece;         // arcs per warp piece of a hub row
   void release(cudaStream_t st);
 };
@@ -139,6 +140,8 @@ struct fj_graph {
   int ncolors = 0;           // phases of a colored sweep (tail merged)
   int ncolors_raw = 0;       // colors of the distance-1 coloring before the merge
   int tail_color = -1;       // merged tail phase (−1: none)
+  double color_tail_frac = -2.0;  // fj_opts.tail_frac / .coloring the coloring was built with
+  int color_algo = -1;
   cudaEvent_t w_ready = nullptr;  // during create only: host weights staged on a side stream
 };
 
@@ -186,7 +189,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
                                 const float *ow, const int32_t *color /* nullable */,
                                 int ncolors, Layout *L, bool need_d1 = false);
 // color.cu
-fj_status build_coloring(fj_graph *g);
+fj_status build_coloring(fj_graph *g, const fj_opts *o);  // (re)builds if o asks for other options
 // memory helpers (api.cu)
 bool is_device_ptr(const void *p);
 // every kernel launch issued by this library is counted (fj_kernel_launches)

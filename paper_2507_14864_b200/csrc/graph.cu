@@ -408,7 +408,11 @@ static double wall() {
 
 static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const int32_t *col_in,
                              const float *w_in, int directed, cudaStream_t st, fj_graph *g) {
-  const bool dbg = getenv("FJ_DEBUG") != nullptr;
+#ifdef FJ_DIAG
+  const bool dbg = true;   // diagnostic build: phase timings on stderr
+#else
+  const bool dbg = false;
+#endif
   double t0 = wall();
   auto mark = [&](const char *what) {
     if (!dbg) return;

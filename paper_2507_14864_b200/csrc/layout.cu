@@ -235,7 +235,11 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
                                 bool need_d1) {
   cudaStream_t st = g->stream;
   const int64_t n = g->n, m = g->m;
-  const bool dbg = getenv("FJ_DEBUG") != nullptr;
+#ifdef FJ_DIAG
+  const bool dbg = true;   // diagnostic build: phase timings on stderr
+#else
+  const bool dbg = false;
+#endif
   timespec tt0;
   clock_gettime(CLOCK_MONOTONIC, &tt0);
   auto mark = [&](const char *what) {
@@ -281,8 +285,12 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   FJ_CUDA(cudaMallocAsync(&L->perm, sizeof(int32_t) * n, st));
   FJ_CUDA(cudaMallocAsync(&L->iperm, sizeof(int32_t) * n, st));
   FJ_CUDA(cudaMallocAsync(&L->rp, sizeof(int64_t) * (n + 2), st));
-  FJ_CUDA(cudaMallocAsync(&L->col, sizeof(int32_t) * (m + 8), st));
-  if (ow) FJ_CUDA(cudaMallocAsync(&L->w, sizeof(float) * (m + 8), st));
+  FJ_CUDA(cudaMallocAsync(&L->col, sizeof(int32_t) * (m + kStreamPad), st));
+  FJ_CUDA(cudaMemsetAsync(L->col + m, 0, sizeof(int32_t) * kStreamPad, st));
+  if (ow) {
+    FJ_CUDA(cudaMallocAsync(&L->w, sizeof(float) * (m + kStreamPad), st));
+    FJ_CUDA(cudaMemsetAsync(L->w + m, 0, sizeof(float) * kStreamPad, st));
+  }
   if (g->weighted || need_d1) FJ_CUDA(cudaMallocAsync(&L->d1, sizeof(double) * n, st));
   fj::count_launch();
   k_perm<<<gridn(n), kBlock, 0, st>>>(n, k0, ort, L->perm, L->iperm, len);
@@ -345,9 +353,12 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   fj::count_launch();
   // hub rows are split in warp pieces: long pieces (fewer partial combines)
   // for one-phase sweeps; short ones for colored sweeps, where every phase
-  // waits for its slowest warp (FJ_PIECE overrides, diagnostics)
+  // waits for its slowest warp (a diagnostic build may force -DFJ_PIECE=…)
+#ifdef FJ_PIECE
+  int piece = FJ_PIECE;
+#else
   int piece = ncolors > 1 ? 256 : kWarpPiece;
-  if (getenv("FJ_PIECE")) piece = std::max(32, atoi(getenv("FJ_PIECE")));
+#endif
   L->piece = piece;
   k_piece_counts<<<gridn(n + 1), kBlock, 0, st>>>(n, L->rp, piece, npc);
   {
@@ -445,9 +456,8 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   // on the counts) so every SM works on a mix of both at any time.  Measured:
   // C3 (Chung–Lu, few hub rows) 0.477 → 0.450 ms per sweep; C4 (R-MAT-24, 65 %
   // of the arcs in hub rows) 1.386 → 1.40, so only graphs whose warp units hold
-  // under half the arcs get it (FJ_MIX=0/1 forces it off/on).
-  const bool mix = getenv("FJ_MIX") ? atoi(getenv("FJ_MIX")) != 0
-                                    : 2 * L->warp_unit_arcs < m;
+  // under half the arcs get it.
+  const bool mix = 2 * L->warp_unit_arcs < m;
   if (ncolors == 1 && mix && nrt > 0) {
     const int64_t U = L->wphase_begin[1] - L->wphase_begin[0], N = nrt, T = N - U;
     std::vector<int32_t> hp(N);
@@ -468,11 +478,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   }
   FJ_CUDA(cudaStreamSynchronize(st));  // host vectors above are stack-owned
   mark("task lists");
-  // measured on all five configs: direct loads beat the TMA-staged stream
-  // once short rows run as warp tiles (the stage buffers take L1 away from
-  // the ẑ gathers); the TMA path stays selectable with FJ_TMA=1
-  L->stream_tma = false;
-  if (getenv("FJ_DEBUG")) {  // per-color layout summary (diagnostics)
+  if (dbg) {  // per-color layout summary (diagnostic build)
     std::vector<int64_t> cut(ncolors + 1);
     for (int c = 0; c <= ncolors; c++) cut[c] = gstart[c * kClasses];
     std::vector<int64_t> arc(ncolors + 1);

@@ -216,7 +216,7 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   cudaStream_t st = g->stream;
   const int64_t n = g->n;
   const bool colored = omega != 1.0;
-  if (colored && !g->colors) FJ_TRY(build_coloring(g));
+  if (colored) FJ_TRY(build_coloring(g, o));
   Layout &P = colored ? g->push_color_layout : g->push_layout;
   if (!P.tasks) {
     FJ_TRY(build_layout_from_out(g, g->in_rp, g->in_col, g->in_w, colored ? g->colors : nullptr,
@@ -302,7 +302,7 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   FJ_CUDA(ws.alloc(&front, n));
   pp.front = front;
   pp.fcount = reinterpret_cast<unsigned long long *>(ctl + 16);  // zeroed with ctl
-  pp.sparse_div = getenv("FJ_PUSH_SPARSE_DIV") ? atoi(getenv("FJ_PUSH_SPARSE_DIV")) : 8;
+  pp.sparse_div = o->push_sparse_div > 0 ? o->push_sparse_div : 8;
   KP kq = make_kp(g, L);
   kq.s = sL;
   kq.z = zL;
@@ -318,7 +318,7 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   kq.partial = partial;
   kq.arrive = arrive;
 
-  const bool compact = getenv("FJ_PUSH_COMPACT") && atoi(getenv("FJ_PUSH_COMPACT"));
+  const bool compact = o->push_compact != 0;
   const void *fn = W ? (compact ? (const void *)k_push<true, true> : (const void *)k_push<true, false>)
                      : (compact ? (const void *)k_push<false, true> : (const void *)k_push<false, false>);
   const int grid = persistent_grid(fn, g->num_sms);

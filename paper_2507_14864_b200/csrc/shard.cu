@@ -47,7 +47,7 @@ struct fj_comm {
   bool local = true;
   // in-process transport that runs the NCCL path's bookkeeping (send lists,
   // pack kernel, per-peer segments) with device copies in place of
-  // ncclSend/ncclRecv: FJ_LOOPBACK=1 at fj_comm_create_local (tests)
+  // ncclSend/ncclRecv: fj_comm_create_loopback (tests)
   bool loopback = false;
   ncclComm_t nc = nullptr;
   cudaStream_t stream = nullptr;
@@ -1037,7 +1037,7 @@ fj_status fj_comm_create(const void *id128, int rank, int world, fj_comm_t *out)
   return FJ_OK;
 }
 
-fj_status fj_comm_create_local(int world, fj_comm_t *out) {
+static fj_status comm_create_local(int world, bool loopback, fj_comm_t *out) {
   if (!out || world < 1 || world > fj::kMaxLocal) {
     fj::set_error("fj_comm_create_local: need 1 <= world <= %d and out", fj::kMaxLocal);
     return FJ_ERR_INVALID;
@@ -1046,7 +1046,7 @@ fj_status fj_comm_create_local(int world, fj_comm_t *out) {
   fj_comm *c = new fj_comm();
   c->world = world;
   c->local = true;
-  c->loopback = getenv("FJ_LOOPBACK") && atoi(getenv("FJ_LOOPBACK"));
+  c->loopback = loopback;
   fj_status s = comm_base(c);
   if (s != FJ_OK) {
     fj_comm_destroy(c);
@@ -1055,6 +1055,10 @@ fj_status fj_comm_create_local(int world, fj_comm_t *out) {
   *out = c;
   return FJ_OK;
 }
+
+fj_status fj_comm_create_local(int world, fj_comm_t *out) { return comm_create_local(world, false, out); }
+
+fj_status fj_comm_create_loopback(int world, fj_comm_t *out) { return comm_create_local(world, true, out); }
 
 fj_status fj_comm_destroy(fj_comm_t c) {
   if (!c) return FJ_OK;

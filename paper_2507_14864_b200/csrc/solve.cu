@@ -26,296 +26,41 @@
 
 namespace fj {
 
-// ------------------------------------------------ TMA-pipelined warp stream
-// Each warp walks its work items (hub-row warp units, then short-row warp
-// tiles) as a stream of <= 256-arc chunks.  The column indices (and weights)
-// of chunk i+1 are fetched into the warp's shared-memory stage by a TMA bulk
-// copy (cp.async.bulk, completion on an mbarrier) while chunk i is gathered and
-// reduced, so the HBM stream runs behind the dependent ẑ gathers without
-// holding registers.
-constexpr int kChunk = kWarpTileArcs;                       // arcs per chunk
-constexpr int kStageElems = kChunk + 8;                     // + 16-byte alignment slack
-struct WarpSmem {
-  int32_t col[2][kStageElems];
-  float w[2][kStageElems];
-  double prod[kChunk];
-  unsigned long long bar[2];
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void *q) {
-  return (uint32_t)__cvta_generic_to_shared(q);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long *b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(unsigned long long *b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P1;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
-                                            unsigned long long *b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
-}
-
-// lane 0: fetch arcs [c0, c1) of the layout CSR into stage st (16-byte
-// aligned superset; the arrays are padded by >= 8 elements)
-template <bool W>
-__device__ __forceinline__ void chunk_issue(const KP &p, WarpSmem *ws, int st, int64_t c0,
-                                            int64_t c1) {
-  const int64_t al = c0 & ~(int64_t)3;
-  const uint32_t nb = (uint32_t)((((c1 + 3) & ~(int64_t)3) - al) * 4);
-  // the stage was last read through the generic proxy (after __syncwarp)
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  mbar_expect(&ws->bar[st], W ? 2 * nb : nb);
-  tma_load_1d(ws->col[st], p.col + al, nb, &ws->bar[st]);
-  if (W) tma_load_1d(ws->w[st], p.w + al, nb, &ws->bar[st]);
-}
-
-// relax the rows of a warp tile from a staged chunk
-template <bool W>
-__device__ __forceinline__ void tile_from_stage(const KP &p, const Scalars &S, const Task &tk,
-                                                TAcc &t, WarpSmem *ws, int st, uint32_t par) {
-  constexpr int U = kChunk / 32;
-  const int lane = threadIdx.x & 31;
-  const int cls = tk.kind & 0xff;
-  const int G = 1 << cls;
-  const int gl = lane & (G - 1);
-  const int ng = 32 >> cls;
-  int64_t rb[2], re[2];
-  float sv[2];
-  double zi[2], d1[2];
-#pragma unroll
-  for (int q = 0; q < 2; q++) {  // row state first: independent of the chunk
-    const int row = tk.a + q * ng + (lane >> cls);
-    rb[q] = re[q] = 0;
-    sv[q] = 0.f;
-    zi[q] = d1[q] = 0.0;
-    if (row < tk.b) {
-      rb[q] = __ldg(p.rp + row);
-      re[q] = __ldg(p.rp + row + 1);
-      if (gl == 0) {
-        sv[q] = __ldg(p.s + row);
-        zi[q] = __ldcg(p.z + row);
-        if (W) d1[q] = __ldg(p.d1 + row);
-      }
-    }
-  }
-  const int64_t a0 = tk.a0;
-  const int na = (int)(tk.a1 - a0);
-  const int off = (int)(a0 & 3);
-  mbar_wait(&ws->bar[st], par);
-  int j[U];
-#pragma unroll
-  for (int u = 0; u < U; u++) {
-    const int e = u * 32 + lane;
-    j[u] = e < na ? ws->col[st][off + e] : -1;
-  }
-  double zj[U];
-#pragma unroll
-  for (int u = 0; u < U; u++) zj[u] = j[u] >= 0 ? ld_z(p.z + j[u]) : 0.0;
-#pragma unroll
-  for (int u = 0; u < U; u++) {
-    const int e = u * 32 + lane;
-    if (e < na) ws->prod[e] = (W ? (double)ws->w[st][off + e] : 1.0) * zj[u];
-  }
-  __syncwarp();
-#pragma unroll
-  for (int q = 0; q < 2; q++) {
-    double a = 0.0;
-    const int kb = (int)(rb[q] - a0), ke = (int)(re[q] - a0);
-    for (int k = kb + gl; k < ke; k += G) a += ws->prod[k];
-    for (int o = G >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    const int row = tk.a + q * ng + (lane >> cls);
-    if (row < tk.b && gl == 0) {
-      const int len = (int)(re[q] - rb[q]);
-      relax_row_pre(p, S, row, len, dd{a, 0.0}, sv[q], zi[q], W ? d1[q] : (double)(len + 1), t);
-    }
-  }
-}
-
-// one warp's work items of a phase, as a TMA-pipelined chunk stream
-template <bool W>
-__device__ __forceinline__ void relax_stream(const KP &p, const Scalars &S, int r0, int nr,
-                                             TAcc &t, WarpSmem *ws, uint32_t &phase_bits) {
-  const int lane = threadIdx.x & 31;
-  const int stride = gridDim.x * (kBlock / 32);
-  int ti = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
-  if (ti >= nr) return;
-  Task T = p.rtasks[r0 + ti];
-  int64_t c0 = T.a0;
-  int st = 0;
-  if (lane == 0) chunk_issue<W>(p, ws, 0, c0, min(T.a1, c0 + (int64_t)kChunk));
-  dd acc{0.0, 0.0};   // warp-unit accumulator (per lane)
-  double pre = 0.0;   // warp-unit row state (lanes 1..5)
-  bool unit_start = true;
-  while (true) {
-    const bool unit = (T.kind & 0xff) == kWarp;
-    const int64_t c1 = unit ? min(T.a1, c0 + (int64_t)kChunk) : T.a1;
-    // next chunk (same unit, or the next work item)
-    Task N = T;
-    int nti = ti;
-    int64_t n0 = c1;
-    if (!unit || c1 >= T.a1) {
-      nti = ti + stride;
-      if (nti < nr) {
-        N = p.rtasks[r0 + nti];
-        n0 = N.a0;
-      }
-    }
-    const bool has_next = nti < nr;
-    if (has_next && lane == 0)
-      chunk_issue<W>(p, ws, st ^ 1, n0,
-                     (N.kind & 0xff) == kWarp ? min(N.a1, n0 + (int64_t)kChunk) : N.a1);
-    const uint32_t par = (phase_bits >> st) & 1u;
-    phase_bits ^= 1u << st;
-    if (!unit) {
-      tile_from_stage<W>(p, S, T, t, ws, st, par);
-    } else {
-      const int row = T.a;
-      if (unit_start) {
-        acc = dd{0.0, 0.0};
-        pre = 0.0;
-        if (lane == 1) pre = (double)__ldg(p.s + row);
-        else if (lane == 2) pre = __ldcg(p.z + row);
-        else if (lane == 3 && W) pre = __ldg(p.d1 + row);
-        else if (lane == 4) pre = (double)__ldg(p.rp + row);
-        else if (lane == 5) pre = (double)__ldg(p.rp + row + 1);
-      }
-      const int off = (int)(c0 & 3);
-      const int na = (int)(c1 - c0);
-      mbar_wait(&ws->bar[st], par);
-      constexpr int U = kChunk / 32;
-      int j[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int e = u * 32 + lane;
-        j[u] = e < na ? ws->col[st][off + e] : -1;
-      }
-      double zj[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) zj[u] = j[u] >= 0 ? ld_z(p.z + j[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int e = u * 32 + lane;
-        if (e < na) {
-          if (W) dd_addprod(acc, (double)ws->w[st][off + e], zj[u]);
-          else dd_add(acc, zj[u]);
-        }
-      }
-      if (c1 >= T.a1) {  // unit done: reduce and finish the row (or its piece)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc_merge(acc, acc_shfl(acc, 0xffffffffu, o));
-        const float sv = (float)__shfl_sync(0xffffffffu, pre, 1);
-        const double zi = __shfl_sync(0xffffffffu, pre, 2);
-        const double rbv = __shfl_sync(0xffffffffu, pre, 4), rev = __shfl_sync(0xffffffffu, pre, 5);
-        const int len = (int)(rev - rbv);
-        const double d1 = W ? __shfl_sync(0xffffffffu, pre, 3) : (double)(len + 1);
-        if (lane == 0) {
-          const int np = T.kind >> 8;
-          bool finish = true;
-          if (np > 1) {
-            __stcg(p.partial + T.slot + T.b, make_double2(acc.hi, acc.lo));
-            finish = (arrive_release(p.arrive + T.slot) + 1) % np == 0;
-            if (finish) {
-              acc = dd{0.0, 0.0};
-              for (int q = 0; q < np; q++) {
-                const double2 x = ld_partial(p.partial + T.slot + q);
-                acc_merge(acc, dd{x.x, x.y});
-              }
-            }
-          }
-          if (finish) relax_row_pre(p, S, row, len, acc, sv, zi, d1, t);
-        }
-      }
-    }
-    __syncwarp();  // stage st and the product slice are free again
-    if (!has_next) break;
-    unit_start = !unit || c1 >= T.a1;
-    st ^= 1;
-    T = N;
-    c0 = n0;
-    ti = nti;
-  }
-}
-
 // ------------------------------------------------------ persistent sweeps
-template <bool W, bool TMA>
+// The sweep list of a phase holds warp units (rows above kWarpTileArcs arcs, or
+// kWarpPiece-arc pieces of hub rows; longest first) and warp tiles (short rows
+// of one length class).  Warps take the items round-robin, the next item's
+// descriptor prefetched; the items are balanced by construction, so no claim
+// atomics sit on the hot loop.  One grid barrier ends each color phase.
+template <bool W>
 __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
-  extern __shared__ double s_prod[];  // per warp: a WarpSmem (TMA stages + products)
+  extern __shared__ double s_prod[];  // per warp: the products of its warp tile
   __shared__ unsigned long long s_dec[3];
   // sharded solve: sweeps queued after the global stopping sweep do nothing
   if (p.stop && __ldcg(p.stop) != 0ull) return;
-  const Scalars S = *p.sc;
-  WarpSmem *ws = reinterpret_cast<WarpSmem *>(s_prod) + (threadIdx.x >> 5);
-  uint32_t phase_bits = 0;
-  if (TMA && (threadIdx.x & 31) == 0) {
-    mbar_init(&ws->bar[0]);
-    mbar_init(&ws->bar[1]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
+  __shared__ Scalars sS;  // shift / thresholds: shared memory, not registers
+  if (threadIdx.x == 0) sS = *p.sc;
+  __syncthreads();
+  const Scalars &S = sS;
   TAcc t{};
   unsigned long long tot_upd = 0, tot_eu = 0;
   int sweeps = 0, reason = 1;
-  int phase = 0;
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
-    for (int k = 0; k < p.ncolors; ++k, ++phase) {
-      if (TMA) {
-        relax_stream<W>(p, S, p.rphase_begin[k], p.rphase_begin[k + 1] - p.rphase_begin[k], t,
-                        ws, phase_bits);
-      } else if (p.dyn) {  // dynamic: warps claim kClaim items at a time
-        const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
-        double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
-        const int lane = threadIdx.x & 31;
-        if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[(phase + 2) % 3] = 0u;
-        for (;;) {
-          int base = 0;
-          if (lane == 0) base = (int)atomicAdd(p.ctr + phase % 3, (unsigned)kClaim);
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (base >= nr) break;
-          const int end = min(nr, base + kClaim);
-          for (int wi = base; wi < end; wi++) {
-            const Task cur = p.rtasks[r0 + wi];
-            if ((cur.kind & 0xff) == kWarp) do_warp<RELAX, W>(p, S, cur, t);
-            else relax_warp_tile<W>(p, S, cur, t, wprod);
-          }
-        }
-      } else {  // static round-robin: one warp per work item, next item prefetched
-        // (tasks are balanced by construction; no claim atomics on the hot loop)
-        const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
-        const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
-        const int stride = gridDim.x * (kBlock / 32);
-        double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
-        // FJ_SYMM: odd sweeps walk the work list backwards (symmetric ordering)
-        const bool rev = p.symm && (sw & 1);
-        int wi = warp_id;
-        Task nxt;
-        if (wi < nr) nxt = p.rtasks[r0 + (rev ? nr - 1 - wi : wi)];
-        while (wi < nr) {
-          const Task cur = nxt;
-          const int wn = wi + stride;
-          if (wn < nr) nxt = p.rtasks[r0 + (rev ? nr - 1 - wn : wn)];
-          if ((cur.kind & 0xff) == kWarp) {
-            if (!(p.dbg & 1)) do_warp<RELAX, W>(p, S, cur, t);
-          } else if (!(p.dbg & 2)) {
-            relax_warp_tile<W>(p, S, cur, t, wprod);
-          }
-          wi = wn;
-        }
+    for (int k = 0; k < p.ncolors; ++k) {
+      const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+      const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
+      const int stride = gridDim.x * (kBlock / 32);
+      double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
+      int wi = warp_id;
+      Task nxt;
+      if (wi < nr) nxt = p.rtasks[r0 + wi];
+      while (wi < nr) {
+        const Task cur = nxt;
+        const int wn = wi + stride;
+        if (wn < nr) nxt = p.rtasks[r0 + wn];
+        if ((cur.kind & 0xff) == kWarp) do_warp<RELAX, W>(p, S, cur, t);
+        else relax_warp_tile<W>(p, S, cur, t, wprod);
+        wi = wn;
       }
       if (k + 1 < p.ncolors) grid_sync(p.bar);
     }
@@ -330,54 +75,6 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
     if (done) { reason = 0; break; }
   }
   sweep_result(p.out, sweeps, tot_upd, tot_eu, reason);
-}
-
-template <bool W>
-__global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_async(KP p, AsyncCtl *c) {
-  extern __shared__ double s_prod[];
-  const Scalars S = *p.sc;
-  const int lane = threadIdx.x & 31;
-  double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
-  const unsigned long long nr = (unsigned long long)(p.rphase_begin[1] - p.rphase_begin[0]);
-  const Task *items = p.rtasks + p.rphase_begin[0];
-  const unsigned long long limit = nr * (unsigned long long)p.max_sweeps;
-  unsigned long long my_epoch = ~0ull;
-  TAcc t{};
-  for (;;) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&c->next, (unsigned long long)kClaim);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    const unsigned int stop = *(volatile unsigned int *)&c->stop;
-    if (stop || base >= limit || nr == 0) break;
-    unsigned long long ep = base / nr, cnt = 0;
-    // bounded staleness: a warp may run at most kRing/2 - 1 sweeps ahead of
-    // the oldest unfinished one (keeps the per-sweep counter slots distinct;
-    // the oldest sweep's holders are never blocked, so this cannot deadlock)
-    if (lane == 0)
-      while (ep >= (unsigned long long)*(volatile unsigned int *)&c->epochs + kRing / 2 - 1 &&
-             !*(volatile unsigned int *)&c->stop)
-        __nanosleep(256);
-    __syncwarp();
-    for (int q = 0; q < kClaim; q++) {
-      const unsigned long long it = base + q;
-      if (it >= limit) break;
-      const unsigned long long e = it / nr;
-      if (e != ep) {  // the batch straddles two epochs: settle the first part
-        async_settle(c, ep, nr, t, cnt);
-        cnt = 0;
-        ep = e;
-      }
-      if (e != my_epoch) {  // a new sweep for this warp: drop stale L1 lines of ẑ
-        __threadfence();
-        my_epoch = e;
-      }
-      const Task tk = items[it - e * nr];
-      if ((tk.kind & 0xff) == kWarp) do_warp<RELAX, W>(p, S, tk, t);
-      else relax_warp_tile<W>(p, S, tk, t, wprod);
-      cnt++;
-    }
-    async_settle(c, ep, nr, t, cnt);
-  }
 }
 
 // measures node pass: z into layout order (fp64) + Σz
@@ -420,7 +117,7 @@ __global__ void k_meas_nodes2(int64_t n, const float *__restrict__ z, const floa
 
 // the one-sweep-per-launch entry of the sharded solve (shard.cu)
 const void *sweep_kernel(bool weighted) {
-  return weighted ? (const void *)k_sweep<true, false> : (const void *)k_sweep<false, false>;
+  return weighted ? (const void *)k_sweep<true> : (const void *)k_sweep<false>;
 }
 size_t sweep_kernel_smem() { return (kBlock / 32) * kWarpTileArcs * sizeof(double); }
 
@@ -439,7 +136,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   // sentinel still decide the outcome).
   if (method == FJ_METHOD_AUTO)
     method = (omega == 1.0 || g->directed) ? FJ_METHOD_ASYNC : FJ_METHOD_COLORED;
-  if (method == FJ_METHOD_COLORED && !g->colors) FJ_TRY(build_coloring(g));
+  if (method == FJ_METHOD_COLORED) FJ_TRY(build_coloring(g, o));
   if (method == FJ_METHOD_PUSH) {
     if (o->z_init) {
       set_error("fj_solve: z_init (warm start) is supported by ASYNC/COLORED, not PUSH");
@@ -517,9 +214,6 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   p.sc = S;
   p.omega = omega;
   p.theta = 1.0;
-  p.dbg = getenv("FJ_DBG_SKIP") ? atoi(getenv("FJ_DBG_SKIP")) : 0;
-  p.dyn = getenv("FJ_DYN") ? atoi(getenv("FJ_DYN")) : 0;
-  p.symm = getenv("FJ_SYMM") ? atoi(getenv("FJ_SYMM")) : 0;
   p.partial = partial;
   p.arrive = arrive;
   p.max_sweeps = o->max_sweeps;
@@ -529,35 +223,13 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   p.out = outv;
   p.cert_max = certbits;
 
-  // TMA-streamed chunks pay off when the arc stream dominates (short rows,
-  // local gathers: lattice, ER); hub-dominated graphs keep the shared memory
-  // as L1 for their gathers and load the stream directly
-  const bool tma = getenv("FJ_TMA") ? atoi(getenv("FJ_TMA")) != 0 : L.stream_tma;
-  const void *fn = W ? (tma ? (const void *)k_sweep<true, true> : (const void *)k_sweep<true, false>)
-                     : (tma ? (const void *)k_sweep<false, true> : (const void *)k_sweep<false, false>);
-  const size_t sweep_smem =
-      tma ? (kBlock / 32) * sizeof(WarpSmem) : (kBlock / 32) * kWarpTileArcs * sizeof(double);
+  const void *fn = W ? (const void *)k_sweep<true> : (const void *)k_sweep<false>;
+  const size_t sweep_smem = sweep_kernel_smem();
   FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem));
-  if (getenv("FJ_CARVEOUT"))  // shared-memory carveout in percent (diagnostics)
-    FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 atoi(getenv("FJ_CARVEOUT"))));
   const int grid = persistent_grid(fn, g->num_sms, sweep_smem);
   float ms_sweep = 0, ms_cert = 0;
   int rounds = 0;
   stats.colors = L.ncolors;
-  // one-phase ASYNC runs barrier-free (k_sweep_async) unless FJ_BARRIER=1
-  // the barrier-free kernel is opt-in (FJ_ASYNC_FREE=1): measured slower on
-  // C4/C5, where overlapping sweeps lose some Gauss–Seidel ordering
-  const bool barrier_free = L.ncolors == 1 && !tma && getenv("FJ_ASYNC_FREE") &&
-                            atoi(getenv("FJ_ASYNC_FREE"));
-  const void *fa = W ? (const void *)k_sweep_async<true> : (const void *)k_sweep_async<false>;
-  const size_t async_smem = (kBlock / 32) * kWarpTileArcs * sizeof(double);
-  AsyncCtl *actl = nullptr;
-  if (barrier_free) {
-    FJ_CUDA(cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)async_smem));
-    FJ_CUDA(ws.alloc(&actl, 1));
-  }
-  const int agrid = barrier_free ? persistent_grid(fa, g->num_sms, async_smem) : 0;
   for (;;) {
     // a3–a5: persistent sweeps with on-device loop control
     FJ_CUDA(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * kCtlWords, st));
@@ -567,14 +239,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     // sweep or the certificate never inherits a half-finished count)
     FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
     FJ_CUDA(cudaEventRecord(es0, st));
-    if (barrier_free) {
-      FJ_CUDA(cudaMemsetAsync(actl, 0, sizeof(AsyncCtl), st));
-      void *args[] = {&p, &actl};
-      fj::count_launch();
-      FJ_CUDA(cudaLaunchKernel(fa, agrid, kBlock, args, async_smem, st));
-      fj::count_launch();
-      k_async_result<<<1, 1, 0, st>>>(actl, outv, (unsigned long long)p.max_sweeps);
-    } else {
+    {
       void *args[] = {&p};
       fj::count_launch();
       FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, sweep_smem, st));

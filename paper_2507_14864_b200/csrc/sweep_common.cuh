@@ -20,7 +20,6 @@ struct NvtxRange {  // tracing: one NVTX range per library phase (nsys/ncu timel
 };
 
 enum Mode { RELAX = 0, CERT = 1, DIS = 2, SPMV = 3 };
-constexpr int kClaim = 16;  // work items per dynamic claim
 constexpr int kCtlWords = 256;  // control block: [0..2] claim counters, [5] cert counter, [8..] barrier
 
 struct Scalars {
@@ -71,9 +70,6 @@ struct KP {
   unsigned long long *cert_max;  // double bits
   double *dis;
   double *rout;                  // CERT: optional residual output (layout order)
-  int dbg;                       // diagnostics (env FJ_DBG_SKIP): 1 skip warp units, 2 skip tiles
-  int dyn;                       // dynamic work claiming in k_sweep (env FJ_DYN)
-  int symm;                      // alternate sweep direction (env FJ_SYMM)
   const unsigned long long *stop;  // sharded solve: nonzero = the loop has ended (k_sweep)
   int64_t empty0, empty1;  // rows with no arcs (the layout's last group): CERT covers them too
 };
@@ -555,61 +551,6 @@ __device__ __forceinline__ void sweep_result(unsigned long long *out, int sweeps
 #ifndef FJ_MINB
 #define FJ_MINB 4
 #endif
-
-// ------------------------------------------- barrier-free asynchronous sweeps
-// ASYNC with one phase: warps claim batches of work items from one monotonic
-// counter; item c belongs to epoch (sweep) c / nr.  Epochs therefore run back
-// to back without a grid barrier, and the claim order balances the load.  The
-// warp that completes an epoch checks its update count: zero updates (no row
-// had |r| > h when evaluated) stops the loop — the paper's Q = ∅ — and the
-// host-side compensated certificate decides (resuming if a row slipped).
-constexpr int kRing = 8;     // per-epoch counter slots
-struct AsyncCtl {
-  unsigned long long next;                 // claim counter (items)
-  unsigned long long upd[kRing], eu[kRing], done[kRing];
-  unsigned long long tot_upd, tot_eu;
-  unsigned int stop, bad, epochs, pad;
-};
-
-// settle one warp's counts for an epoch part: warp-reduce, then lane 0 adds
-// them; the warp that completes the epoch decides whether to stop
-static __device__ __forceinline__ void async_settle(AsyncCtl *c, unsigned long long ep,
-                                             unsigned long long nr, TAcc &t,
-                                             unsigned long long cnt) {
-  unsigned long long u = t.upd, e2 = t.eu, b = t.bad;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    u += __shfl_xor_sync(0xffffffffu, u, off);
-    e2 += __shfl_xor_sync(0xffffffffu, e2, off);
-    b |= __shfl_xor_sync(0xffffffffu, b, off);
-  }
-  t = TAcc{};
-  if ((threadIdx.x & 31) != 0 || cnt == 0) return;
-  const int slot = (int)(ep % kRing);
-  if (u) atomicAdd(&c->upd[slot], u);
-  atomicAdd(&c->tot_upd, u);
-  atomicAdd(&c->tot_eu, e2);
-  if (b) atomicOr(&c->bad, 1u);
-  __threadfence();
-  if (atomicAdd(&c->done[slot], cnt) + cnt == nr) {  // epoch ep complete
-    __threadfence();
-    const unsigned long long uu = atomicAdd(&c->upd[slot], 0ull);
-    atomicMax(&c->epochs, (unsigned int)(ep + 1));
-    if (uu == 0 || atomicAdd(&c->bad, 0u)) atomicExch(&c->stop, 1u);
-    const int z = (int)((ep + kRing / 2) % kRing);  // recycle a slot well ahead
-    c->upd[z] = 0;
-    c->done[z] = 0;
-  }
-}
-
-// out[0..3] = sweeps, relaxations, edge updates, reason (as k_sweep writes)
-static __global__ void k_async_result(const AsyncCtl *c, unsigned long long *out,
-                               unsigned long long max_sweeps) {
-  out[0] = c->epochs;
-  out[1] = c->tot_upd;
-  out[2] = c->tot_eu;
-  out[3] = c->bad ? 2ull : (c->stop ? 0ull : 1ull);
-}
 
 // ------------------------------------------ one pass over all tasks (CERT/DIS)
 template <int MODE, bool W>

@@ -72,18 +72,17 @@ CASES = list(range(1, 301))
 
 
 @pytest.mark.parametrize("seed", CASES)
-def test_fuzz_case(dev, monkeypatch, seed):
+def test_fuzz_case(dev, seed):
     fam, rp, col, w, s, directed, eps, rng = draw(seed)
     n = len(rp) - 1
     sched = ["async", "colored", "push", "batch", "sharded"][(seed // 5) % 5]
     # opt-in paths ride along: the loopback transport (the NCCL path's
     # bookkeeping) for half the sharded cases, the compacted frontier for half
     # the PUSH cases
-    if sched == "sharded" and seed % 2:
-        monkeypatch.setenv("FJ_LOOPBACK", "1")
+    loopback = sched == "sharded" and seed % 2 == 1
+    push_opts = {}
     if sched == "push" and seed % 2:
-        monkeypatch.setenv("FJ_PUSH_COMPACT", "1")
-        monkeypatch.setenv("FJ_PUSH_SPARSE_DIV", str(int(rng.integers(1, 64))))
+        push_opts = dict(push_compact=True, push_sparse_div=int(rng.integers(1, 64)))
     omega = 1.0 if sched in ("batch", "sharded") or rng.random() < 0.4 else \
         float(rng.uniform(1.05, 1.9))
     ref = oracle.solve(rp, col, w, s, eps, 1.0)
@@ -105,7 +104,7 @@ def test_fuzz_case(dev, monkeypatch, seed):
         W = min(W, n)
         orp, ocol, ow = fjgen.to_out_csr(rp, col, w)
         begin = np.array(fj.shard_plan(orp, W))
-        comm = fj.Comm.in_process(W)
+        comm = fj.Comm.in_process(W, loopback=loopback)
         shards = []
         for r in range(W):
             srp, scol, sw = fjgen.shard_rows(orp, ocol, ow, begin, r)
@@ -126,7 +125,8 @@ def test_fuzz_case(dev, monkeypatch, seed):
     g = fj.Graph(n, rp, col, w, directed=directed)
     z = np.empty(n, np.float32)
     zp = np.empty(n, np.float64)
-    st = fj.solve(g, s32, z, eps, omega, method=sched, zprime_out=zp, raise_on_numeric=False)
+    st = fj.solve(g, s32, z, eps, omega, method=sched, zprime_out=zp, raise_on_numeric=False,
+                  **push_opts)
     g.close()
     if st.status == fj.FJ_ERR_NUMERIC:
         # only over-relaxation may fail to converge, and it must say so

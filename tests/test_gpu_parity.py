@@ -35,20 +35,20 @@ def _t(a, dev):
 
 
 def gpu_solve(dev, rp, col, w, s, eps, omega=1.0, directed=True, method="auto", host=False,
-              raise_on_numeric=True):
+              raise_on_numeric=True, **opts):
     n = len(rp) - 1
     if host:
         g = fj.Graph(n, rp, col, w, directed=directed)
         z = np.empty(n, np.float32)
         zp = np.empty(n, np.float64)
         st = fj.solve(g, np.ascontiguousarray(s, np.float32), z, eps, omega, method=method,
-                      zprime_out=zp, raise_on_numeric=raise_on_numeric)
+                      zprime_out=zp, raise_on_numeric=raise_on_numeric, **opts)
         return g, z.astype(np.float64), zp, st
     g = fj.Graph(n, _t(rp, dev), _t(col, dev), _t(w, dev), directed=directed)
     z = torch.empty(n, dtype=torch.float32, device=dev)
     zp = torch.empty(n, dtype=torch.float64, device=dev)
     st = fj.solve(g, _t(np.asarray(s, np.float32), dev), z, eps, omega, method=method,
-                  zprime_out=zp, raise_on_numeric=raise_on_numeric)
+                  zprime_out=zp, raise_on_numeric=raise_on_numeric, **opts)
     torch.cuda.synchronize()
     return g, z.cpu().numpy().astype(np.float64), zp.cpu().numpy(), st
 
@@ -57,8 +57,8 @@ def rel_err(z, ref):
     return np.max(np.abs(z - ref) / np.maximum(np.abs(ref), SIG)) if len(z) else 0.0
 
 
-def check_parity(dev, rp, col, w, s, eps, omega, directed, method="auto", ref_omega=None):
-    g, z, zp, st = gpu_solve(dev, rp, col, w, s, eps, omega, directed, method)
+def check_parity(dev, rp, col, w, s, eps, omega, directed, method="auto", ref_omega=None, **opts):
+    g, z, zp, st = gpu_solve(dev, rp, col, w, s, eps, omega, directed, method, **opts)
     assert st.status == 0 and st.cert_ratio <= 1.0, st
     # independent certificate by the oracle's own routine
     ratio, _ = oracle.certificate(rp, col, w, s, zp, eps)
@@ -200,13 +200,12 @@ def test_long_rows_star(dev, hub_deg):
     check_parity(dev, rp, col, w, s, 1e-6, 1.5, False)
 
 
-def test_determinism_colored(dev, monkeypatch):
+def test_determinism_colored(dev):
     """COLORED sweeps read only other colors' values: bit-reproducible (with the
     tail merge of reading R23 off: the merged tail phase is asynchronous)."""
-    monkeypatch.setenv("FJ_TAIL_FRAC", "0")
     rp, col, w, s, directed = TINY["rmat12w"]()
-    a = gpu_solve(dev, rp, col, w, s, 1e-6, 1.2, directed, method="colored")
-    b = gpu_solve(dev, rp, col, w, s, 1e-6, 1.2, directed, method="colored")
+    a = gpu_solve(dev, rp, col, w, s, 1e-6, 1.2, directed, method="colored", tail_frac=0.0)
+    b = gpu_solve(dev, rp, col, w, s, 1e-6, 1.2, directed, method="colored", tail_frac=0.0)
     assert np.array_equal(a[2], b[2])
     a[0].close(); b[0].close()
 
@@ -214,25 +213,23 @@ def test_determinism_colored(dev, monkeypatch):
 # ------------------------------------------- tail-color merge (reading R23)
 @pytest.mark.parametrize("name", ["chunglu4k", "er2000", "rmat12w"])
 @pytest.mark.parametrize("omega", [1.3, 1.7])
-def test_tail_merge_parity(dev, monkeypatch, name, omega):
+def test_tail_merge_parity(dev, name, omega):
     """Merged tail phase: certified, same z as the oracle, fewer phases."""
     rp, col, w, s, directed = TINY[name]()
     if directed and omega > 1.5:
         pytest.skip("SOR with ω > 1 on a non-symmetric M-matrix may diverge (as in exact SOR)")
     ref_omega = 1.0 if directed else None
-    monkeypatch.setenv("FJ_TAIL_FRAC", "0")
     st0, z0, ref = check_parity(dev, rp, col, w, s, 1e-6, omega, directed, method="colored",
-                                ref_omega=ref_omega)
-    monkeypatch.setenv("FJ_TAIL_FRAC", "0.2")
+                                ref_omega=ref_omega, tail_frac=0.0)
     st1, z1, _ = check_parity(dev, rp, col, w, s, 1e-6, omega, directed, method="colored",
-                              ref_omega=ref_omega)
+                              ref_omega=ref_omega, tail_frac=0.2)
     assert st1.colors <= st0.colors
     if st0.colors > 3:
         assert st1.colors < st0.colors
 
 
 @pytest.mark.parametrize("omega", [1.5, 1.9])
-def test_tail_merge_complete_graph(dev, monkeypatch, omega):
+def test_tail_merge_complete_graph(dev, omega):
     """K_200: every color holds one row, so merging 90% of the rows makes a
     tail whose rows are all adjacent (β_i ≈ 0.9).  The per-row bound
     ω_i = min(ω, 1.98/(1+β_i)) keeps the asynchronous tail a contraction; the
@@ -241,48 +238,34 @@ def test_tail_merge_complete_graph(dev, monkeypatch, omega):
     edges = [(i, j) for i in range(k) for j in range(i + 1, k)]
     rp, col, w = G.in_csr_from_edges(k, edges)
     s = fjgen.uniform(k, 77)
-    monkeypatch.setenv("FJ_TAIL_FRAC", "0.9")
-    g, z, zp, st = gpu_solve(dev, rp, col, w, s, 1e-6, omega, False, method="colored")
+    g, z, zp, st = gpu_solve(dev, rp, col, w, s, 1e-6, omega, False, method="colored",
+                             tail_frac=0.9)
     assert st.status == 0 and st.colors < k
     assert oracle.certificate(rp, col, w, s, zp, 1e-6)[0] <= 1.0
     assert rel_err(z, cf.complete_graph(s.astype(np.float64))) <= 1e-4
     g.close()
 
 
-@pytest.mark.parametrize("knob", ["FJ_TMA", "FJ_ASYNC_FREE", "FJ_DYN", "FJ_SYMM", "FJ_MIX"])
-@pytest.mark.parametrize("name", ["rmat12w", "chunglu4k", "lattice64"])
-def test_diagnostic_schedules(dev, monkeypatch, knob, name):
-    """The opt-in sweep variants of the tuning log (TMA-staged stream,
-    barrier-free epochs, dynamic claims, symmetric order, forced interleave)
-    stay correct: certified and equal to the oracle's z."""
-    monkeypatch.setenv(knob, "1")
-    rp, col, w, s, directed = TINY[name]()
-    check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async")
-
-
 @pytest.mark.parametrize("coloring", ["spec", "jp"])
 @pytest.mark.parametrize("name", ["chunglu4k", "rmat12w"])
-def test_colorings(dev, monkeypatch, coloring, name):
-    """Both colorings (default speculative largest-first, FJ_COLORING=jp) give
-    valid colored solves; the colors are a proper coloring (checked through the
-    sequential-SOR parity of the COLORED schedule without the tail merge)."""
-    monkeypatch.setenv("FJ_COLORING", coloring)
-    monkeypatch.setenv("FJ_TAIL_FRAC", "0")
+def test_colorings(dev, coloring, name):
+    """Both colorings (default speculative largest-first, fj_opts.coloring = 1
+    Jones–Plassmann) give valid colored solves; the colors are a proper coloring
+    (checked through the sequential-SOR parity of the COLORED schedule without
+    the tail merge).  Switching the option on one graph rebuilds the coloring."""
     rp, col, w, s, directed = TINY[name]()
     check_parity(dev, rp, col, w, s, 1e-6, 1.3, directed, method="colored",
-                 ref_omega=1.0 if directed else None)
+                 ref_omega=1.0 if directed else None, coloring=coloring, tail_frac=0.0)
 
 
 @pytest.mark.parametrize("compact", ["0", "1"])
 @pytest.mark.parametrize("omega", [1.0, 1.197, 1.6])
-def test_push_certifies_rows_without_arcs(dev, monkeypatch, compact, omega):
+def test_push_certifies_rows_without_arcs(dev, compact, omega):
     """Rows with d_v = 0 are exact after the pull solvers' init (R20) but PUSH
     relaxes them like any other row, so the certificate (and the residual it
     hands back on a resume) must cover them: the GPU ratio is at least the
     oracle's ratio over those rows, and the result meets the ε bound.  (A
     directed R-MAT graph with isolated nodes and sinks.)"""
-    monkeypatch.setenv("FJ_PUSH_COMPACT", compact)
-    monkeypatch.setenv("FJ_PUSH_SPARSE_DIV", "15")
     rp, col = fjgen.rmat_graph(11, 8, 161)
     n = len(rp) - 1
     s = fjgen.uniform(n, 161)
@@ -295,7 +278,8 @@ def test_push_certifies_rows_without_arcs(dev, monkeypatch, compact, omega):
     for rep in range(3):
         z = np.empty(n, np.float32)
         zp = np.empty(n, np.float64)
-        st = fj.solve(g, s, z, eps, omega, method="push", zprime_out=zp)
+        st = fj.solve(g, s, z, eps, omega, method="push", zprime_out=zp,
+                      push_compact=compact == "1", push_sparse_div=15)
         ratio, R = oracle.certificate(rp, col, None, s, zp, eps)
         _, h, _, _ = oracle.thresholds(s, eps)
         assert ratio <= 1.0 and st.cert_ratio <= 1.0
@@ -351,11 +335,20 @@ def test_chunked_build_mixed_hubs(dev, weighted):
     assert oracle.certificate(rp, col, w, s, outs[0], 1e-6)[0] <= 1.0
 
 
-def test_small_hub_pieces(dev, monkeypatch):
-    """FJ_PIECE: hub rows split into many 64-arc pieces (the combine path)."""
-    monkeypatch.setenv("FJ_PIECE", "64")
-    rp, col, w, s, directed = TINY["rmat12w"]()
-    check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async")
+@pytest.mark.parametrize("weighted", [False, True])
+def test_many_hub_pieces(dev, weighted):
+    """A hub row of 150,000 arcs (74 warp pieces of 2048 arcs, combined by the
+    last-arriving warp in piece order) next to a random directed graph: the
+    piece-combine path of the sweep and of the certificate, against the oracle."""
+    n = 150_001
+    rng = np.random.default_rng(31)
+    arcs = [(0, v) for v in range(1, n)]                       # node 0 listens to everyone
+    extra = rng.integers(1, n, size=(60_000, 2))
+    arcs += [(int(u), int(v)) for u, v in extra if u != v]
+    arcs = sorted(set(arcs))
+    wts = list(rng.uniform(0.1, 1.0, len(arcs))) if weighted else None
+    rp, col, w = G.in_csr_from_arcs(n, arcs, wts)
+    check_parity(dev, rp, col, w, fjgen.uniform(n, 31), 1e-6, 1.0, True, method="async")
 
 
 @pytest.mark.parametrize("name", ["er2000", "rmat12w", "lattice64"])
@@ -487,13 +480,12 @@ def test_tiny_push(dev, name):
 
 @pytest.mark.parametrize("name", ["rmat12w", "chunglu4k", "lattice64"])
 @pytest.mark.parametrize("div", ["1", "64"])
-def test_tiny_push_compacted_frontier(dev, monkeypatch, name, div):
+def test_tiny_push_compacted_frontier(dev, name, div):
     """PUSH with frontier compaction (ballot + per-warp atomic slots) and the
     sparse warp-per-row scatter of the compacted list."""
-    monkeypatch.setenv("FJ_PUSH_COMPACT", "1")
-    monkeypatch.setenv("FJ_PUSH_SPARSE_DIV", div)
     rp, col, w, s, directed = TINY[name]()
-    check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="push")
+    check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="push", push_compact=True,
+                 push_sparse_div=int(div))
 
 
 @pytest.mark.parametrize("name", ["er2000", "lattice64", "chunglu4k"])
@@ -540,6 +532,28 @@ def test_omega_opt_vs_dense(dev, name):
     assert mu == pytest.approx(mu_d, rel=1e-4)
     assert om == pytest.approx(oracle.omega_opt(mu_d), rel=1e-4)
     g.close()
+
+
+@pytest.mark.parametrize("name", ["er2000", "lattice64", "rmat12"])
+def test_omega_sweep_vs_oracle_heuristic(dev, name):
+    """f1: the GPU's fewest-updates pick (fj_omega_sweep, relaxations
+    inside sweeps) lands in the ORACLE's near-optimal band — the ω whose FIFO
+    pop count (the paper's "number of updates") is within 1.25× of the oracle's
+    minimum over the same grid 1.95:−0.05:1.00 (reading R10).  The two count
+    different things (GPU relaxations per sweep schedule vs FIFO pops), so
+    only the band is compared; both tables are in the assertion message."""
+    rp, col, w, s, directed = TINY[name]()
+    n = len(rp) - 1
+    best_o, table = oracle.omega_sweep(rp, col, w, s, 1e-6, prune=False)
+    cost = {round(om, 2): c for om, c, _ in table}
+    cmin = min(cost.values())
+    band = sorted(om for om, c in cost.items() if c <= 1.25 * cmin)
+    g = fj.Graph(n, rp, col, w, directed=directed)
+    best_g, rows = fj.omega_sweep(g, s, 1e-6, lo=1.0, hi=1.95, step=0.05)
+    g.close()
+    msg = f"gpu {best_g} {[(round(r[0], 2), r[1], r[2]) for r in rows]} | oracle {best_o} {table}"
+    assert round(best_g, 2) in band, msg
+    assert best_o in band
 
 
 def test_omega_sweep_heuristic(dev):
@@ -726,7 +740,7 @@ def p_eps(p):
 
 # (config, ω): the oracle's FIFO solve at the same ω and ε finishes in seconds
 # to ~30 s on one host core (profiles/r01f_full_parity.md)
-FULL_VS_ORACLE = [(1, 1.0), (1, 1.5), (2, 1.0), (5, 1.0), (5, 1.25)]
+FULL_VS_ORACLE = [(1, 1.0), (1, 1.5), (2, 1.0), (5, 1.0), (5, 1.25), (5, 1.3)]
 
 
 @pytest.mark.parametrize("cid,omega", FULL_VS_ORACLE, ids=[f"C{c}-w{o}" for c, o in FULL_VS_ORACLE])
@@ -750,7 +764,8 @@ def test_full_size_vs_oracle_z(dev, cid, omega):
         assert abs(m[k] - om[k]) <= 1e-5 * abs(om[k]), (k, m[k], om[k])
 
 
-# (config, ω) whose oracle FIFO solve takes minutes (C3 ω = 1.6: 64 s, C4: 221–1000 s):
+# (config, ω) whose oracle FIFO solve takes minutes (C3 ω = 1.6: 64 s, C4: 221–1000 s;
+# C3's 1.6 is also its tuned ω, fjgen.CONFIG_SOLVE):
 # certified by the oracle's compensated certificate (any size), measures of the same z
 FULL_CERTIFIED = [(3, 1.6), (4, 1.2), (4, 1.4), (4, 1.6)]
 
@@ -783,3 +798,17 @@ def test_full_size_c4_omega18_numeric(dev):
     p = _config(4)
     z, zp, st, m = _full_solve(dev, p, 1.8, raise_on_numeric=False)
     assert st.status == fj.FJ_ERR_NUMERIC and st.reason in (1, 2), st
+
+
+def test_full_size_c2_tuned_omega(dev):
+    """C2 at its tuned ω = 1.55 (the oracle's fewest-updates pick, reading R10):
+    the directed graph runs the ASYNC schedule, where over-relaxation carries
+    no guarantee (P:484 covers the symmetric case; R11) — the solve is either
+    certified by the oracle's own certificate or reported as FJ_ERR_NUMERIC."""
+    p = _config(2)
+    z, zp, st, m = _full_solve(dev, p, fjgen.CONFIG_SOLVE[2]["tuned"], raise_on_numeric=False)
+    if st.status == 0:
+        assert st.cert_ratio <= 1.0
+        assert oracle.certificate(p.row_ptr, p.col, p.w, p.s, zp, 1e-6)[0] <= 1.0
+    else:
+        assert st.status == fj.FJ_ERR_NUMERIC and st.reason in (1, 2), st

@@ -39,12 +39,13 @@ def make_shards(comm, rp, col, w, directed, begin, on_device, dev):
     return shards
 
 
-def sharded_solve(dev, rp, col, w, s, eps, omega, directed, W, on_device=True, begin=None):
+def sharded_solve(dev, rp, col, w, s, eps, omega, directed, W, on_device=True, begin=None,
+                  loopback=False):
     n = len(rp) - 1
     if begin is None:
         orp, _, _ = fjgen.to_out_csr(rp, col, w)
         begin = np.array(fj.shard_plan(orp, W))
-    comm = fj.Comm.in_process(len(begin) - 1)
+    comm = fj.Comm.in_process(len(begin) - 1, loopback=loopback)
     shards = make_shards(comm, rp, col, w, directed, begin, on_device, dev)
     fj.shard_connect(shards)
     s32 = np.asarray(s, np.float32)
@@ -109,13 +110,12 @@ def test_shard_halo_exact(dev, name):
 
 @pytest.mark.parametrize("name", ["rmat12w", "chunglu4k", "lattice64", "dirw-dense"])
 @pytest.mark.parametrize("W", [2, 3, 5])
-def test_shard_loopback_nccl_bookkeeping(dev, monkeypatch, name, W):
-    """FJ_LOOPBACK: the in-process transport runs the NCCL path's send lists,
-    pack kernel and per-peer segments, with device copies in place of
-    ncclSend/ncclRecv — the multi-rank logic one GPU can check."""
-    monkeypatch.setenv("FJ_LOOPBACK", "1")
+def test_shard_loopback_nccl_bookkeeping(dev, name, W):
+    """fj_comm_create_loopback: the in-process transport runs the NCCL path's
+    send lists, pack kernel and per-peer segments, with device copies in place
+    of ncclSend/ncclRecv — the multi-rank logic one GPU can check."""
     rp, col, w, s, directed = TINY[name]()
-    st, z, zp, m = sharded_solve(dev, rp, col, w, s, 1e-6, 1.0, directed, W)
+    st, z, zp, m = sharded_solve(dev, rp, col, w, s, 1e-6, 1.0, directed, W, loopback=True)
     assert st.status == 0 and st.cert_ratio <= 1.0
     assert oracle.certificate(rp, col, w, s, zp, 1e-6)[0] <= 1.0
     assert rel_err(z, oracle.solve(rp, col, w, s, 1e-6, 1.0).z) <= 1e-4

@@ -27,7 +27,7 @@ g = fj.Graph(len(rp) - 1, T(rp), T(col), T(w), directed=directed)
 st_ = T(s); z = torch.empty(len(rp) - 1, dtype=torch.float32, device=dev)
 res = []
 for r in range(reps):
-    st = fj.solve(g, st_, z, 1e-6, om, raise_on_numeric=False)
+    st = fj.solve(g, st_, z, 1e-6, om, raise_on_numeric=False, max_sweeps=4000)
     res.append((st.solve_ms, st.sweeps, st.sweep_ms / max(1, st.sweeps), st.cert_ratio, st.status))
 res.sort()
 t = res[len(res) // 2]
@@ -40,7 +40,11 @@ reps = os.environ.get("AB_REPS", "5")
 for cid in cids:
     for lib in libs:
         env = dict(os.environ, FJ_LIB_PATH=os.path.abspath(lib))
-        out = subprocess.run([sys.executable, "-c", code, str(cid), om, reps], env=env,
-                             capture_output=True, text=True)
+        try:
+            out = subprocess.run([sys.executable, "-c", code, str(cid), om, reps], env=env,
+                                 capture_output=True, text=True, timeout=240)
+        except subprocess.TimeoutExpired:
+            print(f"C{cid} w={om} {lib:45s} TIMEOUT", flush=True)
+            continue
         print(f"C{cid} w={om} {lib:45s}", out.stdout.strip(), out.stderr[-400:] if out.returncode else "",
               flush=True)
