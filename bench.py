@@ -161,61 +161,64 @@ def config_dict(prob, args, extra=None):
 
 
 # ------------------------------------------------------------ reference arm
+#: the oracle's full C4 time-to-ε (ImprovedBLI, FIFO, fp64, one core) from the
+#: round-1 full-size parity run (profiles/r01f_full_parity.md, build r01f)
+ORACLE_FULL_C4 = {"time_to_eps_s": 960.8, "edge_updates_per_s": 5.67e7,
+                  "source": "profiles/r01f_full_parity.md (config 4, omega 1.0, one host core)"}
+#: scale reduction of the CPU sample: config 4's recipe at R-MAT scale 20
+#: (shrink 2) solves to ε in ~45 s on one core at the full-size solve's rate
+#: (5.8e7 vs 5.67e7 edge-updates/s); scale 18 would run 1.5x faster per edge
+#: update (caches), flattering the CPU
+SAMPLE_SHRINK = 2
+
+
+def oracle_full_solve(args, shrink):
+    """One complete ImprovedBLI solve (Alg. 2+1, FIFO, fp64) of the bench
+    config's recipe at a reduced scale: the whole algorithm, start to ε."""
+    import fjgen
+    import oracle
+    p = fjgen.config(args.config, shrink=shrink)
+    r = oracle.solve(p.row_ptr, p.col, p.w, p.s, args.eps, 1.0)
+    return p, r
+
+
 def run_reference(args, prob, world, rank):
     """The oracle (fp64 FIFO ImprovedBLI, single thread) timed on the host
-    cores, each step a bounded sample of the config-4 workload: the first
-    `pushes` pops of Alg. 2+1 on the full graph."""
-    import oracle
+    cores.  Each timed step is a COMPLETE solve to ε of the config-4 recipe at
+    R-MAT scale 20 (representative of the full solve: all of its phases, the
+    same edge-update rate as the full-size run); warm-up steps use scale 16."""
     if rank != 0:
         return None  # rank 0 alone runs the CPU reference
-    total = args.steps + args.warmup
-    budget_s = max(2.0, min(15.0, 150.0 / max(1, total)))
-    pushes = _calibrated_pushes(prob, args, budget_s)
     times, eus = [], []
-    for i in range(total):
-        r = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0, max_pushes=pushes)
+    for i in range(args.warmup + args.steps):
+        p, r = oracle_full_solve(args, max(args.shrink, SAMPLE_SHRINK if i >= args.warmup else 4))
+        assert r.status == 0
         if i >= args.warmup:
             times.append(r.seconds)
             eus.append(r.touched)
     v = sum(eus) / sum(times)
-    sample = (f"first {pushes} pops of ImprovedBLI (Alg. 2+1, FIFO, fp64) on the full "
-              f"{prob.name} graph (n={prob.n}, m={prob.m}); ~{budget_s:.0f} s per step")
+    sample = (f"complete ImprovedBLI solves (Alg. 2+1, FIFO, fp64, to eps={args.eps}) of the "
+              f"config-{args.config} recipe at reduced size ({p.name}, n={p.n}, m={p.m}), "
+              f"{statistics.mean(times):.1f} s each")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (fjgen seeded R-MAT-24, Beta(2,5) opinions)",
+            "data": "synthetic (fjgen seeded R-MAT, Beta(2,5) opinions)",
             "config": config_dict(prob, args, {"omega": 1.0}),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "full_size_time_to_eps": ORACLE_FULL_C4},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     return line
 
 
-def _calibrated_pushes(prob, args, seconds):
-    """Pops of the oracle's FIFO that take about `seconds` on this host: grow a
-    bounded run until it lasts >= seconds/4, then scale (the first pops are the
-    hubs and cost more than later ones)."""
-    import oracle
-    pushes = 100_000
-    while True:
-        cal = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0,
-                           max_pushes=pushes)
-        if cal.status == 0 or cal.seconds >= seconds / 4:
-            break
-        pushes *= 4
-    if cal.status == 0:
-        return pushes  # the whole solve fits the budget
-    return max(1, int(pushes * seconds / max(cal.seconds, 1e-6)))
-
-
 def cpu_baseline(prob, args):
-    import oracle
-    pushes = _calibrated_pushes(prob, args, 15.0)
-    r = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, args.eps, 1.0, max_pushes=pushes)
+    p, r = oracle_full_solve(args, max(args.shrink, SAMPLE_SHRINK))
     return {"value": r.touched / r.seconds, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {r.pushes} pops ({r.touched} edge updates, {r.seconds:.1f} s) of "
-                      f"ImprovedBLI (Alg. 2+1, FIFO, fp64) on the full {prob.name} graph"}
+            "sample": f"one complete ImprovedBLI solve (Alg. 2+1, FIFO, fp64, to eps={args.eps}) "
+                      f"of the config-{args.config} recipe at reduced size ({p.name}, n={p.n}, "
+                      f"m={p.m}): {r.pushes} pops, {r.touched} edge updates, {r.seconds:.1f} s",
+            "full_size_time_to_eps": ORACLE_FULL_C4}
 
 
 # ----------------------------------------------------------------- our arm
