@@ -173,14 +173,20 @@ fj_status fj_solve_ex(fj_graph_t g, const float *s, double eps, double omega,
                       const fj_opts *o, float *z_out, fj_stats *st);
 
 /*
- * Batched solve: k ∈ [1, 4] opinion vectors on one graph
- * in one set of sweeps; ẑ is kept node-major so every gathered cache line and
- * every CSR stream serves all k right-hand sides.  S and Z_out: fp32[n·k],
- * node-major (S[v·k + r]).  Every right-hand side r gets its own Alg. 2 shift
- * c_r and thresholds (reading R5), its own relax decisions, and its own fp64
- * certificate; st (nullable) reports the worst certificate ratio, the sum of
- * relaxations / edge updates over the right-hand sides, and the c of r = 0.
- * Schedule: ASYNC only (o->method AUTO or ASYNC).
+ * Batched solve (the paper runs three opinion
+ * distributions per graph): k ∈ [1, 8] opinion vectors on one graph in
+ * one set of sweeps (padded to K = 2, 4 or 8 internally); ẑ is kept node-major
+ * so every gathered cache line and every CSR stream serves all k right-hand
+ * sides.  S and Z_out: fp32[n·k], node-major (S[v·k + r]).  Every right-hand
+ * side r gets its own Alg. 2 shift c_r and thresholds (reading R5), its own
+ * relax decisions, and its own fp64 certificate; st (nullable) reports the
+ * worst certificate ratio, the sum of relaxations / edge updates over the k
+ * real right-hand sides (padding excluded), and the c of r = 0.
+ * Schedule (o->method): AUTO = ASYNC at ω = 1 or on directed graphs, COLORED
+ * (multicolor SOR, tail merge per o->tail_frac) for ω ≠ 1 on undirected
+ * graphs, as fj_solve; ASYNC or COLORED explicitly; PUSH and z_init →
+ * FJ_ERR_INVALID.  The loop stops after a sweep in which no right-hand side
+ * relaxed any row; FJ_ERR_NUMERIC as fj_solve_ex.
  */
 fj_status fj_solve_batch(fj_graph_t g, const float *S, int k, double eps, double omega,
                          const fj_opts *o, float *Z_out, fj_stats *st);

@@ -1,5 +1,7 @@
-// batch.cu — batched right-hand sides: k ≤ 4 opinion
-// vectors share every CSR stream and every gathered ẑ line.
+// batch.cu — batched right-hand sides: k ≤ 8 opinion
+// vectors share every CSR stream and every gathered ẑ line, under the ASYNC
+// schedule (ω = 1, directed graphs) or the COLORED one (ω ≠ 1 on undirected
+// graphs: multicolor SOR with the merged tail of reading R23, as fj_solve).
 #include "sweep_common.cuh"
 
 namespace fj {
@@ -34,9 +36,15 @@ __device__ __forceinline__ void relax_rowK(const KP &p, const Scalars *SK, int r
     const double ar = fabs(rho);
     out[r] = zi[r];
     if (ar > p.theta * h) {
-      out[r] = zi[r] + p.omega * rho / d1;
-      t.upd++;
-      t.eu += (unsigned long long)len;
+      // tail phase (R23): ω_i = min(ω, 1.98/(1+β_i)), as relax_row_pre
+      double om = p.omega;
+      if (row >= p.tail_row0 && row < p.tail_row1)
+        om = fmin(om, 1.98 / (1.0 + (double)p.tail_beta[row - p.tail_row0]));
+      out[r] = zi[r] + om * rho / d1;
+      if (r < p.kreal) {  // padded right-hand sides relax but do not count
+        t.upd++;
+        t.eu += (unsigned long long)len;
+      }
     }
     if (!(ar <= S.sentinel)) t.bad = 1;
   }
@@ -45,13 +53,30 @@ __device__ __forceinline__ void relax_rowK(const KP &p, const Scalars *SK, int r
   for (int h = 0; h < K / 2; h++) __stcg(q + h, make_double2(out[2 * h], out[2 * h + 1]));
 }
 
-// warp unit (row > kWarpTileArcs arcs, or a piece of one), K right-hand sides
-#ifndef FJ_BWU
-#define FJ_BWU 4
+// warp unit (row > kWarpTileArcs arcs, or a piece of one), K right-hand sides;
+// U·K gathered values in flight per lane (U = 4, 2, 1 arcs for K = 2, 4, 8)
+// Arcs in flight per lane (warp units FJ_BU*, tiles FJ_BT*) and CTAs per SM at
+// K = 4; build-time knobs of the batched kernel, defaults measured on C4/C5
+// (profiles/r02_batch_ab.txt: K = 8 at 2 arcs 6.69 vs 8.07 ms per C4 sweep at
+// 1; K = 4 at 3 CTAs/SM 3.75, at 2 (no spills) 3.71 but +22 % sweeps, at 4 3.67).
+#ifndef FJ_BU4
+#define FJ_BU4 2
+#endif
+#ifndef FJ_BU8
+#define FJ_BU8 2
+#endif
+#ifndef FJ_BT4
+#define FJ_BT4 2
+#endif
+#ifndef FJ_BT8
+#define FJ_BT8 2
+#endif
+#ifndef FJ_BMIN4
+#define FJ_BMIN4 3
 #endif
 template <bool W, int K>
 __device__ __forceinline__ void do_warpK(const KP &p, const Scalars *SK, const Task &tk, TAcc &t) {
-  constexpr int U = FJ_BWU;  // arcs per lane per step (diagnostic build flag FJ_BWU)
+  constexpr int U = K >= 8 ? FJ_BU8 : (K >= 4 ? FJ_BU4 : 4);
   const int lane = threadIdx.x & 31;
   const int row = tk.a, piece = tk.b, np = tk.kind >> 8, slot = tk.slot;
   const int64_t a0 = tk.a0, a1 = tk.a1;
@@ -154,7 +179,9 @@ __device__ __forceinline__ void tileK(const KP &p, const Scalars *SK, const Task
     double a[K];
 #pragma unroll
     for (int r = 0; r < K; r++) a[r] = 0.0;
-#pragma unroll 4
+    // arcs in flight per lane (K gathered values each)
+    constexpr int TU = K >= 8 ? FJ_BT8 : (K >= 4 ? FJ_BT4 : 4);
+#pragma unroll TU
     for (int64_t k = rb + gl; k < re; k += G) {
       const int j = ld_stream(p.col + k);
       const double wk = W ? (double)ld_stream(p.w + k) : 1.0;
@@ -177,36 +204,38 @@ __device__ __forceinline__ void tileK(const KP &p, const Scalars *SK, const Task
 }
 
 // Barrier-synchronised persistent sweeps for K right-hand sides: k_sweep's
-// loop (static round-robin over the sweep list, next item prefetched, one grid
-// barrier per sweep, counters reduced on the device) around the K-wide units
-// and tiles above.  The loop ends after a sweep in which no right-hand side
-// relaxed any row (Q = ∅ for all of them).
-#ifndef FJ_BMINB
-#define FJ_BMINB 4  // CTAs per SM (diagnostic build flag; 3 and 2 measured slower per sweep)
-#endif
+// loop (static round-robin over each phase's list, next item prefetched, one
+// grid barrier per color phase and per sweep, counters reduced on the device)
+// around the K-wide units and tiles above.  The loop ends after a sweep in
+// which no right-hand side relaxed any row (Q = ∅ for all of them).
+// CTAs per SM: 4 at K = 2, 3 at K = 4, 2 at K = 8 (registers for the K-wide
+// accumulators without spills).
 template <bool W, int K>
-__global__ void __launch_bounds__(kBlock, FJ_BMINB) k_sweep_batch_bar(KP p) {
+__global__ void __launch_bounds__(kBlock, K >= 8 ? 2 : (K >= 4 ? FJ_BMIN4 : 4)) k_sweep_batch_bar(KP p) {
   __shared__ Scalars sk[K];
   __shared__ unsigned long long s_dec[3];
   if (threadIdx.x < K) sk[threadIdx.x] = p.sc[threadIdx.x];
   __syncthreads();
-  const int r0 = p.rphase_begin[0], nr = p.rphase_begin[1] - r0;
   const int stride = gridDim.x * (kBlock / 32);
   const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
   TAcc t{};
   unsigned long long tot_upd = 0, tot_eu = 0;
   int sweeps = 0, reason = 1;
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
-    int wi = warp_id;
-    Task nxt;
-    if (wi < nr) nxt = p.rtasks[r0 + wi];
-    while (wi < nr) {
-      const Task cur = nxt;
-      const int wn = wi + stride;
-      if (wn < nr) nxt = p.rtasks[r0 + wn];
-      if ((cur.kind & 0xff) == kWarp) do_warpK<W, K>(p, sk, cur, t);
-      else tileK<W, K>(p, sk, cur, t);
-      wi = wn;
+    for (int k = 0; k < p.ncolors; ++k) {
+      const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
+      int wi = warp_id;
+      Task nxt;
+      if (wi < nr) nxt = p.rtasks[r0 + wi];
+      while (wi < nr) {
+        const Task cur = nxt;
+        const int wn = wi + stride;
+        if (wn < nr) nxt = p.rtasks[r0 + wn];
+        if ((cur.kind & 0xff) == kWarp) do_warpK<W, K>(p, sk, cur, t);
+        else tileK<W, K>(p, sk, cur, t);
+        wi = wn;
+      }
+      if (k + 1 < p.ncolors) grid_sync(p.bar);
     }
     unsigned long long dec[3];
     sweep_totals(p.cnt, p.bar, sw, t, s_dec, dec);
@@ -218,6 +247,12 @@ __global__ void __launch_bounds__(kBlock, FJ_BMINB) k_sweep_batch_bar(KP p) {
     if (done) { reason = 0; break; }
   }
   sweep_result(p.out, sweeps, tot_upd, tot_eu, reason);
+}
+
+template <bool W>
+static const void *batch_kernel(int K) {
+  return K == 2 ? (const void *)k_sweep_batch_bar<W, 2>
+                : (K == 4 ? (const void *)k_sweep_batch_bar<W, 4> : (const void *)k_sweep_batch_bar<W, 8>);
 }
 
 // s (node order, k columns) → layout order, K padded columns (pad = last)
@@ -259,18 +294,23 @@ __global__ void k_finalize_batch(int64_t n, int k, int K, const int32_t *__restr
   for (int r = 0; r < k; r++) Z[u * k + r] = (float)(zK[i * K + r] - SK[r].c);
 }
 
-// k ≤ 4 right-hand sides per solve, ASYNC schedule, one
-// certificate per right-hand side
+// k ≤ 8 right-hand sides per solve (padded to K = 2, 4, 8), ASYNC
+// or COLORED schedule, one certificate per right-hand side
 fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, double omega,
                                   const fj_opts *o, float *Z_out, fj_stats *st_out) {
   NvtxRange nv("fj_solve_batch");
   cudaStream_t st = g->stream;
   const int64_t n = g->n;
-  const int K = k <= 2 ? 2 : 4;
-  const Layout &L = g->async_layout;
+  const int K = k <= 2 ? 2 : (k <= 4 ? 4 : 8);
+  // AUTO as fj_solve: multicolor SOR for ω ≠ 1 on undirected graphs
+  int method = o->method;
+  if (method == FJ_METHOD_AUTO)
+    method = (omega == 1.0 || g->directed) ? FJ_METHOD_ASYNC : FJ_METHOD_COLORED;
+  if (method == FJ_METHOD_COLORED) FJ_TRY(build_coloring(g, o));
+  const Layout &L = method == FJ_METHOD_COLORED ? g->color_layout : g->async_layout;
   const bool W = g->weighted != 0;
   fj_stats stats{};
-  stats.colors = 1;
+  stats.colors = L.ncolors;
   Workspace ws(st);
   cudaEvent_t e0, e1, es0, es1;
   for (cudaEvent_t *e : {&e0, &e1, &es0, &es1}) FJ_CUDA(ws.event(e));
@@ -335,10 +375,10 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
   p.partial = partial;
   p.arrive = arrive;
   p.max_sweeps = o->max_sweeps;
+  p.kreal = k;
   // barrier-synchronised persistent sweeps (an epoch-claim barrier-free
   // variant measured slower: C4 k = 4 1065 vs 1010 ms, C5 124 vs 99 ms)
-  const void *fb = K == 2 ? (W ? (const void *)k_sweep_batch_bar<true, 2> : (const void *)k_sweep_batch_bar<false, 2>)
-                          : (W ? (const void *)k_sweep_batch_bar<true, 4> : (const void *)k_sweep_batch_bar<false, 4>);
+  const void *fb = W ? batch_kernel<true>(K) : batch_kernel<false>(K);
   const int bgrid = persistent_grid(fb, g->num_sms);
   const void *cf = W ? (const void *)k_pass<CERT, true> : (const void *)k_pass<CERT, false>;
   const int cgrid = persistent_grid(cf, g->num_sms);
@@ -352,6 +392,7 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
     FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 8, st));
     FJ_CUDA(cudaMemsetAsync(ctlb, 0, sizeof(unsigned) * kCtlWords, st));
     FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(SweepCounters) * 3, st));
+    FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * np, st));
     FJ_CUDA(cudaEventRecord(es0, st));
     void *args[] = {&p};
     fj::count_launch();
@@ -398,7 +439,7 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
     p.max_sweeps = std::min(o->max_sweeps, 2000);
   }
   stats.cert_rounds = rounds;
-  stats.phases = stats.sweeps;
+  stats.phases = stats.sweeps * L.ncolors;
   stats.rows_read = stats.sweeps * L.active_rows;
   stats.arcs_read = stats.sweeps * L.m;
   stats.relaxations += L.empty_rows * k;
@@ -435,16 +476,20 @@ fj_status fj_solve_batch(fj_graph_t g, const float *S, int k, double eps, double
     if (d.max_sweeps <= 0) d.max_sweeps = 1000000;
     if (d.cert_rounds < 0) d.cert_rounds = 3;
   }
-  if (!g || !S || !Z_out || k < 1 || k > 4) {
-    fj::set_error("fj_solve_batch: need non-null arguments and 1 <= k <= 4");
+  if (!g || !S || !Z_out || k < 1 || k > 8) {
+    fj::set_error("fj_solve_batch: need non-null arguments and 1 <= k <= 8");
     return FJ_ERR_INVALID;
   }
   if (!(eps > 0.0 && eps < 1.0) || !(omega > 0.0 && omega < 2.0)) {
     fj::set_error("fj_solve_batch: eps in (0,1) and omega in (0,2) required");
     return FJ_ERR_INVALID;
   }
-  if (d.method != FJ_METHOD_AUTO && d.method != FJ_METHOD_ASYNC) {
-    fj::set_error("fj_solve_batch: only the ASYNC schedule is batched");
+  if (d.method != FJ_METHOD_AUTO && d.method != FJ_METHOD_ASYNC && d.method != FJ_METHOD_COLORED) {
+    fj::set_error("fj_solve_batch: the ASYNC and COLORED schedules are batched, not PUSH");
+    return FJ_ERR_INVALID;
+  }
+  if (d.z_init) {
+    fj::set_error("fj_solve_batch: z_init (warm start) is not supported for batches");
     return FJ_ERR_INVALID;
   }
   return fj::batch_solve_impl(g, S, k, eps, omega, &d, Z_out, st);
