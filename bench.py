@@ -166,9 +166,11 @@ def config_dict(prob, args, extra=None):
 ORACLE_FULL_C4 = {"time_to_eps_s": 960.8, "edge_updates_per_s": 5.67e7,
                   "source": "profiles/r01f_full_parity.md (config 4, omega 1.0, one host core)"}
 #: scale reduction of the CPU sample: config 4's recipe at R-MAT scale 20
-#: (shrink 2) solves to ε in ~45 s on one core at the full-size solve's rate
-#: (5.8e7 vs 5.67e7 edge-updates/s); scale 18 would run 1.5x faster per edge
-#: update (caches), flattering the CPU
+#: (shrink 2), a complete solve to ε in 23–46 s on one core depending on the
+#: host.  A smaller graph caches better, so its edge-update rate is an upper
+#: bound of the full-size rate (GPU box, round 2: 1.15e8 at scale 20 against
+#: 5.67e7 for the full C4 solve of round 1): the sample flatters the CPU, and
+#: the full-size time-to-ε is quoted beside it
 SAMPLE_SHRINK = 2
 
 
@@ -379,7 +381,7 @@ def run_ours(args, prob, world, rank, local):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
-                         "kernel": "k_sweep (persistent window sweep)",
+                         "kernel": "k_sweep (persistent tile/unit sweep)",
                          "algorithmic_bytes_per_launch": ab,
                          "bytes_model": "SURVEY 8(d): 12 B per edge-update (col, w, gathered z_j) "
                                         "+ 36 B per relaxation (row_ptr, s, z_i r/w, 1+d)",
