@@ -57,12 +57,22 @@ def main():
         torch.cuda.synchronize()
         tcreate = time.time() - t0
         info = g.info()
-        ref = None
-        if a.oracle:
+        refs = {}
+
+        def oracle_ref(om):
+            """The oracle's z at the same ε: at the same ω on undirected graphs,
+            at ω = 1 on directed ones (reading R11)."""
             import oracle
-            ref = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, eps, 1.0)
+            ro = 1.0 if prob.directed else om
+            if ro not in refs:
+                refs[ro] = oracle.solve(prob.row_ptr, prob.col, prob.w, prob.s, eps, ro)
+            return ro, refs[ro]
+
         for method in a.methods.split(","):
             for om in omegas:
+                ref = None
+                if a.oracle:
+                    ref_omega, ref = oracle_ref(om)
                 best = None
                 for r in range(a.repeat):
                     st = fj.solve(g, s, z, eps, om, method=method, zprime_out=zp,
@@ -100,7 +110,8 @@ def main():
                                    P_rel_vs_oracle=abs(m["P"] - omr["P"]) / abs(omr["P"]),
                                    D_rel_vs_oracle=abs(m["D"] - omr["D"]) / abs(omr["D"]),
                                    oracle_s=ref.seconds, oracle_touched=ref.touched,
-                                   oracle_pushes=ref.pushes)
+                                   oracle_pushes=ref.pushes, oracle_omega=ref_omega,
+                                   oracle_status=ref.status)
                 line = json.dumps(rec)
                 print(line, flush=True)
                 if out:
