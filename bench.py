@@ -162,15 +162,16 @@ def config_dict(prob, args, extra=None):
 
 # ------------------------------------------------------------ reference arm
 #: the oracle's full C4 time-to-ε (ImprovedBLI, FIFO, fp64, one core) from the
-#: round-1 full-size parity run (profiles/r01f_full_parity.md, build r01f)
-ORACLE_FULL_C4 = {"time_to_eps_s": 960.8, "edge_updates_per_s": 5.67e7,
-                  "source": "profiles/r01f_full_parity.md (config 4, omega 1.0, one host core)"}
+#: round-2 full-size parity run (profiles/r02_full_parity.md)
+ORACLE_FULL_C4 = {"time_to_eps_s": 843.8, "edge_updates_per_s": 6.45e7,
+                  "source": "profiles/r02_full_parity.md (config 4, omega 1.0, one host core "
+                            "of the GPU box, round 2)"}
 #: scale reduction of the CPU sample: config 4's recipe at R-MAT scale 20
 #: (shrink 2), a complete solve to ε in 23–46 s on one core depending on the
 #: host.  A smaller graph caches better, so its edge-update rate is an upper
 #: bound of the full-size rate (GPU box, round 2: 1.15e8 at scale 20 against
-#: 5.67e7 for the full C4 solve of round 1): the sample flatters the CPU, and
-#: the full-size time-to-ε is quoted beside it
+#: 6.45e7 for the full C4 solve): the sample flatters the CPU, and the
+#: full-size time-to-ε is quoted beside it
 SAMPLE_SHRINK = 2
 
 

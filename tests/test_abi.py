@@ -61,3 +61,30 @@ def test_binding_has_no_host_compute():
     src = open(os.path.join(ROOT, "paper_2507_14864_b200", "__init__.py")).read()
     assert "oracle" not in src.replace("oracle/", "")
     assert "import numpy" not in src
+
+
+def test_library_reads_no_environment():
+    """Schedule options are fj_opts fields and diagnostics are compile-time
+    builds: no source of libfj calls getenv (the binary still references it
+    through the NVTX headers, which look up their injection library)."""
+    import glob
+    for f in glob.glob(os.path.join(ROOT, "paper_2507_14864_b200", "csrc", "*.cu*")):
+        src = re.sub(r"//.*", "", open(f).read())
+        assert "getenv" not in src, f
+
+
+def test_binding_checks_lengths():
+    """The binding refuses buffers shorter than the library will read or
+    write (a short host output would be overrun by the device→host copy)."""
+    import paper_2507_14864_b200 as fj
+
+    class G:
+        n = 10
+    with pytest.raises(ValueError):
+        fj.solve(G(), np.zeros(5, np.float32), np.zeros(10, np.float32), 1e-6)
+    with pytest.raises(ValueError):
+        fj.solve(G(), np.zeros(10, np.float32), np.zeros(9, np.float32), 1e-6)
+    with pytest.raises(TypeError):
+        fj.solve(G(), np.zeros(10, np.float64), np.zeros(10, np.float32), 1e-6)
+    with pytest.raises(ValueError):
+        fj.solve_batch(G(), np.zeros(10 * 3, np.float32), np.zeros(10 * 2, np.float32), 3, 1e-6)

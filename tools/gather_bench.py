@@ -60,3 +60,31 @@ for carve in (0, 25, 50, 75, 100):
     print(f"  no hot 4x256 carve={carve:3d}%: " + " ".join(f"{t:.3f}" for t in ts) + " ms", flush=True)
     ts = [run(4, 0, rcol, 0, 1024, carve, 0) for _ in range(3)]
     print(f"  no hot 1x1024 carve={carve:3d}%: " + " ".join(f"{t:.3f}" for t in ts) + " ms", flush=True)
+
+# ---- arc order inside 256-arc tiles: rows of ≤ 256 arcs, layout-like order
+# (length class descending, id), each consecutive 256-arc chunk sorted by column
+if os.environ.get("GB_TILESORT"):
+    deg = torch.from_numpy(np.diff(p.row_ptr)).to(dev)          # pull row lengths: out-degree
+    odeg = torch.bincount(col.long(), minlength=p.n)             # out-row length of u
+    short = (odeg > 0) & (odeg <= 256)
+    cls = torch.clamp(torch.ceil(torch.log2(odeg.clamp(min=1).double())).long(), 0, 8)
+    key = (8 - cls) * p.n + torch.arange(p.n, device=dev)
+    order = torch.argsort(torch.where(short, key, torch.full_like(key, 1 << 62)))
+    order = order[: int(short.sum())]
+    # arcs of the short rows in that row order
+    ostart = torch.zeros(p.n + 1, dtype=torch.long, device=dev)
+    ostart[1:] = torch.cumsum(odeg, 0)
+    lens = odeg[order]
+    starts = ostart[order]
+    seg = torch.repeat_interleave(torch.arange(len(order), device=dev), lens)
+    off = torch.arange(int(lens.sum()), device=dev) - torch.repeat_interleave(torch.cumsum(lens, 0) - lens, lens)
+    arcs = starts[seg] + off
+    tcol = rcol[arcs].contiguous()                               # popularity ids, tile order
+    ms = (len(tcol) // 256) * 256
+    tcol = tcol[:ms].contiguous()
+    chunk = torch.arange(ms, device=dev) // 256
+    sc = tcol[torch.argsort(chunk * p.n + tcol.long())].contiguous()
+    mm = ms
+    def run2(c, reps=10):
+        return L.gb_run(1, 0, mm, c.data_ptr(), 0, x.data_ptr(), 0, 256, -1, reps, 0)
+    print(f"  short-row arcs {ms}: tile order {run2(tcol):.3f} ms, tile-sorted {run2(sc):.3f} ms", flush=True)
