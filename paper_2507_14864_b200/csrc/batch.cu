@@ -349,20 +349,12 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
   FJ_CUDA(ws.alloc(&cnt, 3));
   if (!zdev) FJ_CUDA(ws.alloc(&Zd, n * k));
   // a2 per right-hand side: shift and thresholds (Alg. 2, reading R5)
-  {
-    size_t t1 = 0, t2 = 0;
-    FJ_CUDA(cub::DeviceReduce::Min(nullptr, t1, col, mm, n, st));
-    FJ_CUDA(cub::DeviceReduce::Max(nullptr, t2, col, mm + 1, n, st));
-    unsigned char *t = nullptr;
-    FJ_CUDA(ws.alloc(&t, std::max(t1, t2)));
-    for (int r = 0; r < K; r++) {
-      fj::count_launch();
-      k_column<<<gridn(n), kBlock, 0, st>>>(n, k, r < k ? r : k - 1, S, col);
-      FJ_CUDA(cub::DeviceReduce::Min(t, t1, col, mm, n, st));
-      FJ_CUDA(cub::DeviceReduce::Max(t, t2, col, mm + 1, n, st));
-      fj::count_launch();
-      k_scalars<<<1, 1, 0, st>>>(mm, mm + 1, eps, o->sigma, o->c, SK + r);
-    }
+  for (int r = 0; r < K; r++) {
+    fj::count_launch();
+    k_column<<<gridn(n), kBlock, 0, st>>>(n, k, r < k ? r : k - 1, S, col);
+    FJ_TRY(minmax_f32(col, n, mm, ws, g->num_sms));
+    fj::count_launch();
+    k_scalars<<<1, 1, 0, st>>>(mm, mm + 1, eps, o->sigma, o->c, SK + r);
   }
   fj::count_launch();
   k_init_batch<<<gridn(n), kBlock, 0, st>>>(n, k, K, L.perm, L.rp, S, SK, sK, zK);

@@ -20,7 +20,6 @@
 #include <stdio.h>
 #include <string.h>
 
-#include <cub/cub.cuh>
 
 #include "fj_internal.cuh"
 
@@ -304,17 +303,9 @@ static fj_status spec_coloring(fj_graph *g, Workspace &ws, const int64_t *orp, c
   FJ_CUDA(ws.alloc(&ord, (size_t)n));
   fj::count_launch();
   k_deg_bucket<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, st>>>(n, g->in_rp, orp, k0, wb);
-  {
-    cub::DoubleBuffer<uint32_t> dk(k0, k1);
-    cub::DoubleBuffer<int32_t> dv(wb, ord);
-    size_t tmp = 0;
-    FJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, n, 0, 6, st));
-    unsigned char *t = nullptr;
-    FJ_CUDA(ws.alloc(&t, tmp));
-    FJ_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, n, 0, 6, st));
-    if (dk.Current() != k0) std::swap(k0, k1);
-    if (dv.Current() != ord) std::swap(ord, wb);
-  }
+  // stable sort by bucket (prims.cu); the sorted ids end in `ord`, `wb` is free again
+  FJ_TRY((radix_sort_pairs<uint32_t, int32_t>(k0, k1, wb, ord, n, 6, ws)));
+  std::swap(ord, wb);
   std::vector<uint32_t> hk((size_t)n);
   FJ_CUDA(cudaMemcpyAsync(hk.data(), k0, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, st));
   FJ_CUDA(cudaStreamSynchronize(st));

@@ -190,6 +190,17 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
                                 int ncolors, Layout *L, bool need_d1 = false);
 // color.cu
 fj_status build_coloring(fj_graph *g, const fj_opts *o);  // (re)builds if o asks for other options
+// prims.cu: hand-written primitives of the graph build and the shift
+fj_status minmax_f32(const float *x, int64_t n, float *out2 /* device [min, max] */, Workspace &ws,
+                     int num_sms);
+fj_status max_nonneg_i64(const int64_t *x, int64_t n, int64_t *out /* device */, Workspace &ws,
+                         int num_sms);
+fj_status exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, Workspace &ws);
+// stable LSD radix sort on the low nbits of the keys; on return keys/vals point
+// at the sorted data (the buffers may have been swapped with the *_alt ones)
+template <class K, class V>
+fj_status radix_sort_pairs(K *&keys, K *&keys_alt, V *&vals, V *&vals_alt, int64_t m, int nbits,
+                           Workspace &ws);
 // memory helpers (api.cu)
 bool is_device_ptr(const void *p);
 // every kernel launch issued by this library is counted (fj_kernel_launches)

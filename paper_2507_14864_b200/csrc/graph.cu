@@ -21,7 +21,6 @@
 #include <time.h>
 
 #include <algorithm>
-#include <cub/cub.cuh>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -304,18 +303,7 @@ static unsigned grid_warps(int64_t rows) {  // warp-per-row kernels: grid-stride
 template <class K, class V>
 static fj_status sort_pairs(K *&keys, K *&keys_alt, V *&val, V *&val_alt, int64_t m, int nbits,
                             Workspace &ws) {
-  if (m == 0) return FJ_OK;
-  cudaStream_t st = ws.st;
-  cub::DoubleBuffer<K> dk(keys, keys_alt);
-  cub::DoubleBuffer<V> dv(val, val_alt);
-  size_t tmp = 0;
-  FJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, m, 0, nbits, st));
-  unsigned char *t = nullptr;
-  FJ_CUDA(ws.alloc(&t, tmp));
-  FJ_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, m, 0, nbits, st));
-  if (dk.Current() != keys) std::swap(keys, keys_alt);
-  if (dv.Current() != val) std::swap(val, val_alt);
-  return FJ_OK;
+  return radix_sort_pairs<K, V>(keys, keys_alt, val, val_alt, m, nbits, ws);  // prims.cu (stable LSD)
 }
 
 template <int KM>

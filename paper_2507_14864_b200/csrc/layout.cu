@@ -13,7 +13,6 @@
 #include <time.h>
 
 #include <algorithm>
-#include <cub/cub.cuh>
 
 #include "fj_internal.cuh"
 
@@ -37,9 +36,12 @@ static unsigned gridn(int64_t work) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 1 << 30));
 }
 
+// group of every row (color, length class descending; empty rows last) as the
+// sort key, the row id as the payload: a stable sort by group keeps ids ascending
 __global__ void k_layout_keys(int64_t n, const int64_t *__restrict__ ort,
                               const int32_t *__restrict__ color, int ncolors,
-                              uint64_t *__restrict__ keys, unsigned long long *__restrict__ gcount) {
+                              uint32_t *__restrict__ keys, uint32_t *__restrict__ ids,
+                              unsigned long long *__restrict__ gcount) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   uint64_t grp = ~0ull;
   if (u < n) {
@@ -50,7 +52,8 @@ __global__ void k_layout_keys(int64_t n, const int64_t *__restrict__ ort,
       int c = color ? color[u] : 0;
       grp = (uint64_t)c * kClasses + (uint64_t)(kClasses - 1 - row_class(L));
     }
-    keys[u] = (grp << 31) | (uint64_t)u;
+    keys[u] = (uint32_t)grp;
+    ids[u] = (uint32_t)u;
   }
   // warp-aggregated histogram: one atomic per distinct group in the warp
   const unsigned act = __ballot_sync(0xffffffffu, u < n);
@@ -60,12 +63,12 @@ __global__ void k_layout_keys(int64_t n, const int64_t *__restrict__ ort,
   }
 }
 
-__global__ void k_perm(int64_t n, const uint64_t *__restrict__ keys, const int64_t *__restrict__ ort,
+__global__ void k_perm(int64_t n, const uint32_t *__restrict__ ids, const int64_t *__restrict__ ort,
                        int32_t *__restrict__ perm, int32_t *__restrict__ iperm,
                        int64_t *__restrict__ len) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  int32_t u = (int32_t)(keys[i] & 0x7fffffffull);
+  int32_t u = (int32_t)ids[i];
   perm[i] = u;
   iperm[u] = (int32_t)i;
   len[i] = ort[u + 1] - ort[u];
@@ -259,29 +262,23 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   L->ncolors = ncolors;
   const int ngroups = ncolors * kClasses + 1;
 
-  uint64_t *k0 = nullptr, *k1 = nullptr;
+  uint32_t *k0 = nullptr, *k1 = nullptr, *id0 = nullptr, *id1 = nullptr;
   unsigned long long *gcount = nullptr;
   int64_t *len = nullptr;
   FJ_CUDA(ws.alloc(&k0, n));
   FJ_CUDA(ws.alloc(&k1, n));
+  FJ_CUDA(ws.alloc(&id0, n));
+  FJ_CUDA(ws.alloc(&id1, n));
   FJ_CUDA(ws.alloc(&gcount, ngroups));
   FJ_CUDA(cudaMemsetAsync(gcount, 0, sizeof(unsigned long long) * ngroups, st));
   FJ_CUDA(ws.alloc(&len, (n + 1)));
   FJ_CUDA(cudaMemsetAsync(len + n, 0, sizeof(int64_t), st));
   fj::count_launch();
-  k_layout_keys<<<gridn(n), kBlock, 0, st>>>(n, ort, color, ncolors, k0, gcount);
+  k_layout_keys<<<gridn(n), kBlock, 0, st>>>(n, ort, color, ncolors, k0, id0, gcount);
 
   int gbits = 1;
   while ((1 << gbits) <= ngroups) gbits++;
-  {
-    cub::DoubleBuffer<uint64_t> dk(k0, k1);
-    size_t tmp = 0;
-    FJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, dk, n, 0, 31 + gbits, st));
-    unsigned char *t = nullptr;
-    FJ_CUDA(ws.alloc(&t, tmp));
-    FJ_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, dk, n, 0, 31 + gbits, st));
-    if (dk.Current() != k0) std::swap(k0, k1);
-  }
+  FJ_TRY((radix_sort_pairs<uint32_t, uint32_t>(k0, k1, id0, id1, n, gbits, ws)));  // prims.cu
   FJ_CUDA(cudaMallocAsync(&L->perm, sizeof(int32_t) * n, st));
   FJ_CUDA(cudaMallocAsync(&L->iperm, sizeof(int32_t) * n, st));
   FJ_CUDA(cudaMallocAsync(&L->rp, sizeof(int64_t) * (n + 2), st));
@@ -293,14 +290,8 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   }
   if (g->weighted || need_d1) FJ_CUDA(cudaMallocAsync(&L->d1, sizeof(double) * n, st));
   fj::count_launch();
-  k_perm<<<gridn(n), kBlock, 0, st>>>(n, k0, ort, L->perm, L->iperm, len);
-  {
-    size_t tmp = 0;
-    FJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, len, L->rp, n + 1, st));
-    unsigned char *t = nullptr;
-    FJ_CUDA(ws.alloc(&t, tmp));
-    FJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, len, L->rp, n + 1, st));
-  }
+  k_perm<<<gridn(n), kBlock, 0, st>>>(n, id0, ort, L->perm, L->iperm, len);
+  FJ_TRY(exclusive_scan_i64(len, L->rp, n + 1, ws));
   fj::count_launch();
   mark("keys+sort+perm+scan");
   {
@@ -319,13 +310,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   int64_t *dmax = nullptr;
   int64_t hmax = 0;
   FJ_CUDA(ws.alloc(&dmax, 1));
-  {
-    size_t tmp = 0;
-    FJ_CUDA(cub::DeviceReduce::Max(nullptr, tmp, len, dmax, n, st));
-    unsigned char *t = nullptr;
-    FJ_CUDA(ws.alloc(&t, tmp));
-    FJ_CUDA(cub::DeviceReduce::Max(t, tmp, len, dmax, n, st));
-  }
+  FJ_TRY(max_nonneg_i64(len, n, dmax, ws, g->num_sms));
   FJ_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   std::vector<unsigned long long> hcount(ngroups);
   FJ_CUDA(cudaMemcpyAsync(hcount.data(), gcount, sizeof(unsigned long long) * ngroups,
@@ -361,13 +346,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
 #endif
   L->piece = piece;
   k_piece_counts<<<gridn(n + 1), kBlock, 0, st>>>(n, L->rp, piece, npc);
-  {
-    size_t tmp = 0;
-    FJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, npc, scan, n + 1, st));
-    unsigned char *t = nullptr;
-    FJ_CUDA(ws.alloc(&t, tmp));
-    FJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, npc, scan, n + 1, st));
-  }
+  FJ_TRY(exclusive_scan_i64(npc, scan, n + 1, ws));
   std::vector<int64_t> hpos(ngroups + 1), hrp(ngroups + 1), hscan(ngroups + 1);
   for (int q = 0; q <= ngroups; q++) hpos[q] = gstart[q];
   FJ_CUDA(ws.alloc(&dpos, (ngroups + 1)));

@@ -258,15 +258,7 @@ fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double ome
   FJ_CUDA(ws.alloc(&outv, 8));
   if (!zdev) FJ_CUDA(ws.alloc(&zo, n));
   if (o->zprime_out && !zpdev) FJ_CUDA(ws.alloc(&zp, n));
-  {
-    size_t t1 = 0, t2 = 0;
-    FJ_CUDA(cub::DeviceReduce::Min(nullptr, t1, s.dev, smin, n, st));
-    FJ_CUDA(cub::DeviceReduce::Max(nullptr, t2, s.dev, smin + 1, n, st));
-    unsigned char *t = nullptr;
-    FJ_CUDA(ws.alloc(&t, std::max(t1, t2)));
-    FJ_CUDA(cub::DeviceReduce::Min(t, t1, s.dev, smin, n, st));
-    FJ_CUDA(cub::DeviceReduce::Max(t, t2, s.dev, smin + 1, n, st));
-  }
+  FJ_TRY(minmax_f32(s.dev, n, smin, ws, g->num_sms));
   fj::count_launch();
   k_scalars<<<1, 1, 0, st>>>(smin, smin + 1, eps, o->sigma, o->c, S);
   fj::count_launch();

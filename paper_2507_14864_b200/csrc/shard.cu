@@ -703,14 +703,7 @@ static fj_status shard_solve_impl(fj_shard **sh, int count, const float *const *
     if (!is_device_ptr(z_out[i])) FJ_CUDA(ws.alloc(&w.zo, nl));
     if (zp_out && zp_out[i] && !is_device_ptr(zp_out[i]))
       FJ_CUDA(ws.alloc(&w.zp, nl));
-    size_t tmp = 0, tmp2 = 0;
-    FJ_CUDA(cub::DeviceReduce::Min(nullptr, tmp, w.s.dev, w.smm, nl, st));
-    FJ_CUDA(cub::DeviceReduce::Max(nullptr, tmp2, w.s.dev, w.smm + 1, nl, st));
-    tmp = std::max(tmp, tmp2);
-    unsigned char *t = nullptr;
-    FJ_CUDA(ws.alloc(&t, tmp));
-    FJ_CUDA(cub::DeviceReduce::Min(t, tmp, w.s.dev, w.smm, nl, st));
-    FJ_CUDA(cub::DeviceReduce::Max(t, tmp, w.s.dev, w.smm + 1, nl, st));
+    FJ_TRY(minmax_f32(w.s.dev, nl, w.smm, ws, cm->num_sms));
   }
   // a2: global shift from the global min / max of s (Alg. 2)
   {

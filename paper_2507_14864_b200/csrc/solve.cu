@@ -181,17 +181,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   if (o->zprime_out && !zpdev) FJ_CUDA(ws.alloc(&zp, n));
 
   // a2: shift and init (Alg. 2)
-  {
-    size_t tmp = 0;
-    FJ_CUDA(cub::DeviceReduce::Min(nullptr, tmp, s.dev, smin, n, st));
-    size_t tmp2 = 0;
-    FJ_CUDA(cub::DeviceReduce::Max(nullptr, tmp2, s.dev, smax, n, st));
-    tmp = std::max(tmp, tmp2);
-    unsigned char *t = nullptr;
-    FJ_CUDA(ws.alloc(&t, tmp));
-    FJ_CUDA(cub::DeviceReduce::Min(t, tmp, s.dev, smin, n, st));
-    FJ_CUDA(cub::DeviceReduce::Max(t, tmp, s.dev, smax, n, st));
-  }
+  FJ_TRY(minmax_f32(s.dev, n, smin, ws, g->num_sms));  // smin[0] = min s, smin[1] = smax = max s
   fj::count_launch();
   k_scalars<<<1, 1, 0, st>>>(smin, smax, eps, o->sigma, o->c, S);
   const double *zinit = nullptr;
@@ -226,6 +216,21 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   const void *fn = W ? (const void *)k_sweep<true> : (const void *)k_sweep<false>;
   const size_t sweep_smem = sweep_kernel_smem();
   FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem));
+  // Shared-memory carveout: the tile staging needs ≈ 68 KB per SM, for which
+  // the driver's default picks the 132 KB configuration (124 KB of L1).  On
+  // hub-dominated layouts (warp units hold over half the arcs: C2, C4) the
+  // 100 KB configuration's larger L1 (156 KB) keeps more hub ẑ lines: C4
+  // 1.418 → 1.335 ms per sweep, C2 0.1055 → 0.1015; on short-row layouts the
+  // staler L1 lines cost more sweeps than the larger L1 saves (C3 +6 % sweeps),
+  // so they keep the default (profiles/r02_carveout_ab.txt).
+#ifdef FJ_CARVE
+  const int carve = FJ_CARVE;  // diagnostic build: forced preference (percent)
+#else
+  const int carve = 2 * L.warp_unit_arcs > L.m ? 31 : -1;
+#endif
+  // (a per-function setting: set on every solve, −1 = the driver's default)
+  FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault));
   const int grid = persistent_grid(fn, g->num_sms, sweep_smem);
   float ms_sweep = 0, ms_cert = 0;
   int rounds = 0;

@@ -6,7 +6,6 @@
 
 #include <algorithm>
 #include <cuda/atomic>
-#include <cub/cub.cuh>
 #include <nvtx3/nvToolsExt.h>
 #include <type_traits>
 
