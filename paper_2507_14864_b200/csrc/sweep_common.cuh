@@ -57,6 +57,7 @@ struct KP {
   const int *wphase_begin;
   int ncolors;
   int kreal;                // batched solves: right-hand sides that count (the rest is padding)
+  int tail_pct;             // k_sweep: percent of each phase's items claimed dynamically at its end
   int tail_phase;           // merged tail colors (reading R23); −1 if none
   int64_t tail_row0, tail_row1;  // rows of the tail phase (empty range if none)
   const float *tail_beta;   // per tail row: β_i (see color.cu)
