@@ -192,6 +192,23 @@ fj_status fj_solve_batch(fj_graph_t g, const float *S, int k, double eps, double
                          const fj_opts *o, float *Z_out, fj_stats *st);
 
 /*
+ * ω batch (rows f1/f2): ONE opinion vector s (fp32[n]) solved at k ∈ [1, 8]
+ * relaxation factors omegas[r] ∈ (0, 2) (host array) in one set of sweeps —
+ * the paper's ω heuristic evaluates many ω on the same problem.
+ * Z_out: fp32[n·k] node-major, column r = z at omegas[r].  A column whose
+ * residual trips the divergence sentinel is frozen (no longer
+ * relaxed) instead of stopping the batch: status_out[r] (nullable, host int[k])
+ * = FJ_OK if column r met its certificate, FJ_ERR_NUMERIC if it diverged or
+ * failed it; relax_out[r] (nullable, host int64[k]) = its relaxations (the
+ * paper's "number of updates").  Schedule as fj_solve_batch (AUTO: ASYNC if all
+ * ω are 1 or the graph is directed, COLORED otherwise).  Returns FJ_OK if at
+ * least one column converged, FJ_ERR_NUMERIC if none did.
+ */
+fj_status fj_solve_batch_omega(fj_graph_t g, const float *s, int k, const double *omegas,
+                               double eps, const fj_opts *o, float *Z_out, fj_stats *st,
+                               int64_t *relax_out, int *status_out);
+
+/*
  * ω selection.
  * fj_omega_opt: μ = ρ((I+D)^{-1}A) by power iteration from the
  * all-ones vector (at most max_iters SpMV sweeps, stop when the estimate moves
@@ -207,7 +224,11 @@ fj_status fj_omega_opt(fj_graph_t g, int max_iters, double tol, double *mu, doub
  * ("minimum number of updates"); diverging points cost +∞, ties go to the
  * smaller ω.  table (nullable, host, 3·(*npts) doubles on entry =
  * capacity): rows (ω, relaxations, status).  *npts returns the point count.
- * method: fj_method for every solve.
+ * method: fj_method of the schedule (AUTO, ASYNC or COLORED; PUSH →
+ * FJ_ERR_INVALID).  The grid runs as ω batches of up to 8 points
+ * (fj_solve_batch_omega): every ω of one call shares one schedule (AUTO: ASYNC
+ * on directed graphs, COLORED on undirected ones), so the relaxation counts
+ * compare like with like.
  */
 fj_status fj_omega_sweep(fj_graph_t g, const float *s, double eps, double lo, double hi,
                          double step, int method, double *best_omega, double *table, int *npts);

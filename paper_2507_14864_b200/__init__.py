@@ -25,7 +25,7 @@ METHODS = {"auto": 0, "async": 1, "colored": 2, "push": 3}
 EXPORTS = ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve", "fj_solve_ex",
            "fj_measures", "fj_measures_ex", "fj_opts_default", "fj_last_error",
            "fj_abi_version", "fj_kernel_launches", "fj_omega_opt", "fj_omega_sweep",
-           "fj_solve_batch", "fj_shard_plan", "fj_comm_unique_id", "fj_comm_create",
+           "fj_solve_batch", "fj_solve_batch_omega", "fj_shard_plan", "fj_comm_unique_id", "fj_comm_create",
            "fj_comm_create_local", "fj_comm_create_loopback", "fj_comm_destroy", "fj_shard_create",
            "fj_shard_connect",
            "fj_shard_solve", "fj_shard_measures", "fj_shard_destroy", "fj_shard_info", "fj_gather_probe")
@@ -93,6 +93,8 @@ def lib():
         L.fj_omega_opt.argtypes = [P, i, d, ctypes.POINTER(d), ctypes.POINTER(d)]
         L.fj_omega_sweep.argtypes = [P, P, d, d, d, d, i, ctypes.POINTER(d), P,
                                      ctypes.POINTER(i)]
+        L.fj_solve_batch_omega.argtypes = [P, P, i, P, d, ctypes.POINTER(_Opts), P,
+                                           ctypes.POINTER(_Stats), P, P]
         PP = ctypes.POINTER(P)
         L.fj_shard_plan.argtypes = [i64, P, i, P]
         L.fj_comm_unique_id.argtypes = [P]
@@ -110,7 +112,8 @@ def lib():
         L.fj_shard_info.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         for f in ("fj_graph_create", "fj_graph_destroy", "fj_graph_get_info", "fj_solve",
                   "fj_solve_ex", "fj_measures", "fj_measures_ex", "fj_omega_opt",
-                  "fj_omega_sweep", "fj_solve_batch", "fj_shard_plan", "fj_comm_unique_id",
+                  "fj_omega_sweep", "fj_solve_batch", "fj_solve_batch_omega", "fj_shard_plan",
+                  "fj_comm_unique_id",
                   "fj_comm_create", "fj_comm_create_local", "fj_comm_create_loopback",
                   "fj_comm_destroy",
                   "fj_shard_create", "fj_shard_connect", "fj_shard_solve",
@@ -279,6 +282,29 @@ def solve_batch(g: Graph, S, Z_out, k: int, eps: float, omega: float = 1.0,
         return stats
     _check(rc)
     return stats
+
+
+def solve_batch_omega(g: Graph, s, Z_out, omegas, eps: float, sigma: float = 1e-5,
+                      max_sweeps: int = 0, method: str = "auto", tail_frac: float = -1.0):
+    """fj_solve_batch_omega: one opinion vector at k ≤ 8 values of ω in one
+    solve.  Returns (stats, relaxations per ω, status per ω)."""
+    k = len(omegas)
+    _dtype_ok(s, "s", "float32", g.n)
+    _dtype_ok(Z_out, "Z_out", "float32", g.n * k)
+    o = _Opts()
+    lib().fj_opts_default(ctypes.byref(o))
+    o.sigma, o.max_sweeps = sigma, max_sweeps
+    o.method, o.tail_frac = METHODS[method], float(tail_frac)
+    om = (ctypes.c_double * k)(*[float(x) for x in omegas])
+    rel = (ctypes.c_int64 * k)()
+    sts = (ctypes.c_int * k)()
+    st = _Stats()
+    rc = lib().fj_solve_batch_omega(g._h, _ptr(s), k, om, float(eps), ctypes.byref(o),
+                                    _ptr(Z_out), ctypes.byref(st), rel, sts)
+    if rc != FJ_ERR_NUMERIC:
+        _check(rc)
+    stats = SolveStats(**{kk: getattr(st, kk) for kk, _ in _Stats._fields_})
+    return stats, list(rel), list(sts)
 
 
 def solve_simple(g: Graph, s, z_out, eps: float, omega: float = 1.0):

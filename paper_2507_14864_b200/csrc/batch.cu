@@ -22,31 +22,46 @@ __device__ __forceinline__ void gatherK(const double *__restrict__ z, int j, dou
   }
 }
 
+// per-CTA shared state of a batched sweep: every column's shift/thresholds,
+// its relaxation factor, and — for the ω batch (k values of ω for one opinion
+// vector, fj_solve_batch_omega) — its divergence flag and relaxation count
+struct BCtx {
+  Scalars sk[8];
+  double om[8];
+  int bad[8];          // column diverged (ω batch): frozen, no longer relaxed
+  unsigned cupd[8];    // relaxations of this CTA in the current sweep (ω batch)
+  int omb;             // ω batch mode
+};
+
 template <int K>
-__device__ __forceinline__ void relax_rowK(const KP &p, const Scalars *SK, int row, int len,
+__device__ __forceinline__ void relax_rowK(const KP &p, BCtx *bc, int row, int len,
                                            dd (&tot)[K], const float (&sv)[K],
                                            const double (&zi)[K], double d1, TAcc &t) {
   double out[K];
 #pragma unroll
   for (int r = 0; r < K; r++) {
-    const Scalars &S = SK[r];
+    const Scalars &S = bc->sk[r];
     const double sp = (double)sv[r] + S.c;
     const double h = threshold(S, sp);
     const double rho = residual_dd(tot[r], sp, d1, zi[r]);
     const double ar = fabs(rho);
     out[r] = zi[r];
-    if (ar > p.theta * h) {
+    if (ar > p.theta * h && !bc->bad[r]) {
       // tail phase (R23): ω_i = min(ω, 1.98/(1+β_i)), as relax_row_pre
-      double om = p.omega;
+      double om = bc->om[r];
       if (row >= p.tail_row0 && row < p.tail_row1)
         om = fmin(om, 1.98 / (1.0 + (double)p.tail_beta[row - p.tail_row0]));
       out[r] = zi[r] + om * rho / d1;
       if (r < p.kreal) {  // padded right-hand sides relax but do not count
         t.upd++;
         t.eu += (unsigned long long)len;
+        if (bc->omb) atomicAdd(&bc->cupd[r], 1u);
       }
     }
-    if (!(ar <= S.sentinel)) t.bad = 1;
+    if (!(ar <= S.sentinel)) {  // divergence sentinel
+      if (bc->omb) atomicOr(p.colbad + r, 1);  // ω batch: this column only
+      else t.bad = 1;
+    }
   }
   double2 *q = reinterpret_cast<double2 *>(p.z + (int64_t)row * K);
 #pragma unroll
@@ -75,7 +90,7 @@ __device__ __forceinline__ void relax_rowK(const KP &p, const Scalars *SK, int r
 #define FJ_BMIN4 3
 #endif
 template <bool W, int K>
-__device__ __forceinline__ void do_warpK(const KP &p, const Scalars *SK, const Task &tk, TAcc &t) {
+__device__ __forceinline__ void do_warpK(const KP &p, BCtx *bc, const Task &tk, TAcc &t) {
   constexpr int U = K >= 8 ? FJ_BU8 : (K >= 4 ? FJ_BU4 : 4);
   const int lane = threadIdx.x & 31;
   const int row = tk.a, piece = tk.b, np = tk.kind >> 8, slot = tk.slot;
@@ -140,13 +155,13 @@ __device__ __forceinline__ void do_warpK(const KP &p, const Scalars *SK, const T
         acc_merge(a[r], dd{x.x, x.y});
       }
   }
-  relax_rowK<K>(p, SK, row, len, a, sv, zi, d1, t);
+  relax_rowK<K>(p, bc, row, len, a, sv, zi, d1, t);
 }
 
 // warp tile (short rows), K right-hand sides: G lanes per row accumulate
 // directly in registers (no shared memory), two row steps
 template <bool W, int K>
-__device__ __forceinline__ void tileK(const KP &p, const Scalars *SK, const Task &tk, TAcc &t) {
+__device__ __forceinline__ void tileK(const KP &p, BCtx *bc, const Task &tk, TAcc &t) {
   const int lane = threadIdx.x & 31;
   const int cls = tk.kind & 0xff;
   const int G = 1 << cls;
@@ -198,7 +213,7 @@ __device__ __forceinline__ void tileK(const KP &p, const Scalars *SK, const Task
       dd tot[K];
 #pragma unroll
       for (int r = 0; r < K; r++) tot[r] = dd{a[r], 0.0};
-      relax_rowK<K>(p, SK, row, len, tot, sv, zi, W ? d1 : (double)(len + 1), t);
+      relax_rowK<K>(p, bc, row, len, tot, sv, zi, W ? d1 : (double)(len + 1), t);
     }
   }
 }
@@ -212,9 +227,16 @@ __device__ __forceinline__ void tileK(const KP &p, const Scalars *SK, const Task
 // accumulators without spills).
 template <bool W, int K>
 __global__ void __launch_bounds__(kBlock, K >= 8 ? 2 : (K >= 4 ? FJ_BMIN4 : 4)) k_sweep_batch_bar(KP p) {
-  __shared__ Scalars sk[K];
+  __shared__ BCtx bc;
   __shared__ unsigned long long s_dec[3];
-  if (threadIdx.x < K) sk[threadIdx.x] = p.sc[threadIdx.x];
+  __shared__ int s_nbad;
+  if (threadIdx.x < K) {
+    bc.sk[threadIdx.x] = p.sc[threadIdx.x];
+    bc.om[threadIdx.x] = p.omegas ? p.omegas[threadIdx.x] : p.omega;
+    bc.bad[threadIdx.x] = 0;
+    bc.cupd[threadIdx.x] = 0u;
+  }
+  if (threadIdx.x == 0) bc.omb = p.colbad != nullptr;
   __syncthreads();
   const int stride = gridDim.x * (kBlock / 32);
   const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
@@ -231,18 +253,34 @@ __global__ void __launch_bounds__(kBlock, K >= 8 ? 2 : (K >= 4 ? FJ_BMIN4 : 4)) 
         const Task cur = nxt;
         const int wn = wi + stride;
         if (wn < nr) nxt = p.rtasks[r0 + wn];
-        if ((cur.kind & 0xff) == kWarp) do_warpK<W, K>(p, sk, cur, t);
-        else tileK<W, K>(p, sk, cur, t);
+        if ((cur.kind & 0xff) == kWarp) do_warpK<W, K>(p, &bc, cur, t);
+        else tileK<W, K>(p, &bc, cur, t);
         wi = wn;
       }
       if (k + 1 < p.ncolors) grid_sync(p.bar);
+    }
+    if (bc.omb) {  // ω batch: this CTA's per-column relaxations of the sweep
+      __syncthreads();
+      if (threadIdx.x < K && bc.cupd[threadIdx.x]) {
+        atomicAdd(p.colupd + threadIdx.x, (unsigned long long)bc.cupd[threadIdx.x]);
+        bc.cupd[threadIdx.x] = 0u;
+      }
     }
     unsigned long long dec[3];
     sweep_totals(p.cnt, p.bar, sw, t, s_dec, dec);
     tot_upd += dec[0];
     tot_eu += dec[1];
     sweeps = sw + 1;
-    const bool bad = dec[2] != 0, done = dec[0] == 0;
+    if (bc.omb) {  // columns that diverged anywhere are frozen from now on
+      if (threadIdx.x == 0) s_nbad = 0;
+      __syncthreads();
+      if (threadIdx.x < K) {
+        bc.bad[threadIdx.x] = __ldcg(p.colbad + threadIdx.x);
+        if (bc.bad[threadIdx.x] && threadIdx.x < p.kreal) atomicAdd(&s_nbad, 1);
+      }
+      __syncthreads();
+    }
+    const bool bad = dec[2] != 0 || (bc.omb && s_nbad == p.kreal), done = dec[0] == 0;
     if (bad) { reason = 2; break; }
     if (done) { reason = 0; break; }
   }
@@ -296,16 +334,31 @@ __global__ void k_finalize_batch(int64_t n, int k, int K, const int32_t *__restr
 
 // k ≤ 8 right-hand sides per solve (padded to K = 2, 4, 8), ASYNC
 // or COLORED schedule, one certificate per right-hand side
+// replicate one opinion vector into k node-major columns (the ω batch)
+__global__ void k_replicate(int64_t n, int k, const float *__restrict__ s, float *__restrict__ S) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u < n)
+    for (int r = 0; r < k; r++) S[u * k + r] = s[u];
+}
+
+// omegas == nullptr: k opinion vectors at one ω (fj_solve_batch).  Otherwise
+// the ω batch (fj_solve_batch_omega): S_in is ONE vector, column r runs at
+// omegas[r] (host), a column whose residual trips the sentinel is frozen and
+// reported in status_out[r]; relax_out[r] = its relaxations.
 fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, double omega,
-                                  const fj_opts *o, float *Z_out, fj_stats *st_out) {
+                           const fj_opts *o, float *Z_out, fj_stats *st_out,
+                           const double *omegas, int64_t *relax_out, int *status_out) {
   NvtxRange nv("fj_solve_batch");
   cudaStream_t st = g->stream;
   const int64_t n = g->n;
   const int K = k <= 2 ? 2 : (k <= 4 ? 4 : 8);
   // AUTO as fj_solve: multicolor SOR for ω ≠ 1 on undirected graphs
+  bool all_one = omega == 1.0;
+  if (omegas)
+    for (int r = 0; r < k; r++) all_one = all_one && omegas[r] == 1.0;
   int method = o->method;
   if (method == FJ_METHOD_AUTO)
-    method = (omega == 1.0 || g->directed) ? FJ_METHOD_ASYNC : FJ_METHOD_COLORED;
+    method = (all_one || g->directed) ? FJ_METHOD_ASYNC : FJ_METHOD_COLORED;
   if (method == FJ_METHOD_COLORED) FJ_TRY(build_coloring(g, o));
   const Layout &L = method == FJ_METHOD_COLORED ? g->color_layout : g->async_layout;
   const bool W = g->weighted != 0;
@@ -317,10 +370,30 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
   FJ_CUDA(cudaEventRecord(e0, st));
   const float *S = S_in;
   float *S_owned = nullptr;
+  const int64_t s_len = omegas ? n : n * k;
   if (!is_device_ptr(S_in)) {
-    FJ_CUDA(ws.alloc(&S_owned, n * k));
-    FJ_CUDA(cudaMemcpyAsync(S_owned, S_in, sizeof(float) * n * k, cudaMemcpyHostToDevice, st));
+    FJ_CUDA(ws.alloc(&S_owned, s_len));
+    FJ_CUDA(cudaMemcpyAsync(S_owned, S_in, sizeof(float) * s_len, cudaMemcpyHostToDevice, st));
     S = S_owned;
+  }
+  double *d_om = nullptr;
+  int *colbad = nullptr;
+  unsigned long long *colupd = nullptr;
+  if (omegas) {  // one vector → k columns; per-column ω, flags and counts
+    float *Srep = nullptr;
+    FJ_CUDA(ws.alloc(&Srep, n * k));
+    fj::count_launch();
+    k_replicate<<<gridn(n), kBlock, 0, st>>>(n, k, S, Srep);
+    S = Srep;
+    double hom[8];
+    for (int r = 0; r < K; r++) hom[r] = omegas[r < k ? r : k - 1];
+    FJ_CUDA(ws.alloc(&d_om, 8));
+    FJ_CUDA(cudaMemcpyAsync(d_om, hom, sizeof(double) * 8, cudaMemcpyHostToDevice, st));
+    FJ_CUDA(ws.alloc(&colbad, 8));
+    FJ_CUDA(cudaMemsetAsync(colbad, 0, sizeof(int) * 8, st));
+    FJ_CUDA(ws.alloc(&colupd, 8));
+    FJ_CUDA(cudaMemsetAsync(colupd, 0, sizeof(unsigned long long) * 8, st));
+    FJ_CUDA(cudaStreamSynchronize(st));  // hom is stack-owned
   }
   const bool zdev = is_device_ptr(Z_out);
   float *sK = nullptr, *col = nullptr, *mm = nullptr, *s1 = nullptr, *Zd = nullptr;
@@ -368,6 +441,9 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
   p.arrive = arrive;
   p.max_sweeps = o->max_sweeps;
   p.kreal = k;
+  p.omegas = d_om;
+  p.colbad = colbad;
+  p.colupd = colupd;
   // barrier-synchronised persistent sweeps (an epoch-claim barrier-free
   // variant measured slower: C4 k = 4 1065 vs 1010 ms, C5 124 vs 99 ms)
   const void *fb = W ? batch_kernel<true>(K) : batch_kernel<false>(K);
@@ -392,9 +468,19 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
     FJ_CUDA(cudaEventRecord(es1, st));
     unsigned long long h[8];
     FJ_CUDA(cudaMemcpyAsync(h, outv, sizeof(h), cudaMemcpyDeviceToHost, st));
-    // compensated certificate of every right-hand side
+    // compensated certificate of every right-hand side (ω batch: of every
+    // column that did not diverge)
     double worst = 0.0;
+    int hbad[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (colbad) {
+      FJ_CUDA(cudaMemcpyAsync(hbad, colbad, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
+      FJ_CUDA(cudaStreamSynchronize(st));
+    }
     for (int r = 0; r < k; r++) {
+      if (hbad[r]) {
+        if (status_out) status_out[r] = FJ_ERR_NUMERIC;
+        continue;
+      }
       fj::count_launch();
       k_columnL<<<gridn(n), kBlock, 0, st>>>(n, K, r, sK, zK, s1, z1);
       KP q = make_kp(g, L);
@@ -415,6 +501,7 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
       FJ_CUDA(cudaStreamSynchronize(st));
       const double ratio = __builtin_bit_cast(double, bits);
       if (!(ratio <= worst)) worst = ratio;
+      if (status_out) status_out[r] = ratio <= 1.0 ? FJ_OK : FJ_ERR_NUMERIC;
     }
     FJ_CUDA(cudaStreamSynchronize(st));
     float a = 0;
@@ -435,6 +522,12 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
   stats.rows_read = stats.sweeps * L.active_rows;
   stats.arcs_read = stats.sweeps * L.m;
   stats.relaxations += L.empty_rows * k;
+  if (relax_out) {  // ω batch: relaxations per column (rows solved at init included)
+    unsigned long long hu[8];
+    FJ_CUDA(cudaMemcpyAsync(hu, colupd, sizeof(hu), cudaMemcpyDeviceToHost, st));
+    FJ_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < k; r++) relax_out[r] = (int64_t)hu[r] + L.empty_rows;
+  }
   fj::count_launch();
   k_finalize_batch<<<gridn(n), kBlock, 0, st>>>(n, k, K, L.iperm, zK, SK, zdev ? Z_out : Zd);
   if (!zdev) FJ_CUDA(cudaMemcpyAsync(Z_out, Zd, sizeof(float) * n * k, cudaMemcpyDeviceToHost, st));
@@ -484,7 +577,52 @@ fj_status fj_solve_batch(fj_graph_t g, const float *S, int k, double eps, double
     fj::set_error("fj_solve_batch: z_init (warm start) is not supported for batches");
     return FJ_ERR_INVALID;
   }
-  return fj::batch_solve_impl(g, S, k, eps, omega, &d, Z_out, st);
+  return fj::batch_solve_impl(g, S, k, eps, omega, &d, Z_out, st, nullptr, nullptr, nullptr);
+}
+
+fj_status fj_solve_batch_omega(fj_graph_t g, const float *s, int k, const double *omegas,
+                               double eps, const fj_opts *o, float *Z_out, fj_stats *st,
+                               int64_t *relax_out, int *status_out) {
+  fj_opts d;
+  fj_opts_default(&d);
+  if (o) {
+    d = *o;
+    if (!(d.sigma > 0)) d.sigma = 1e-5;
+    if (d.max_sweeps <= 0) d.max_sweeps = 1000000;
+    if (d.cert_rounds < 0) d.cert_rounds = 3;
+  }
+  if (!g || !s || !Z_out || !omegas || k < 1 || k > 8) {
+    fj::set_error("fj_solve_batch_omega: need non-null arguments and 1 <= k <= 8");
+    return FJ_ERR_INVALID;
+  }
+  for (int r = 0; r < k; r++)
+    if (!(omegas[r] > 0.0 && omegas[r] < 2.0)) {
+      fj::set_error("fj_solve_batch_omega: omega[%d] = %g outside (0, 2)", r, omegas[r]);
+      return FJ_ERR_INVALID;
+    }
+  if (!(eps > 0.0 && eps < 1.0)) {
+    fj::set_error("fj_solve_batch_omega: eps in (0,1) required");
+    return FJ_ERR_INVALID;
+  }
+  if (d.method != FJ_METHOD_AUTO && d.method != FJ_METHOD_ASYNC && d.method != FJ_METHOD_COLORED) {
+    fj::set_error("fj_solve_batch_omega: the ASYNC and COLORED schedules are batched, not PUSH");
+    return FJ_ERR_INVALID;
+  }
+  if (d.z_init) {
+    fj::set_error("fj_solve_batch_omega: z_init (warm start) is not supported for batches");
+    return FJ_ERR_INVALID;
+  }
+  int stat[8];
+  fj_status rc = fj::batch_solve_impl(g, s, k, eps, omegas[0], &d, Z_out, st, omegas, relax_out,
+                                      stat);
+  if (status_out)
+    for (int r = 0; r < k; r++) status_out[r] = stat[r];
+  if (rc == FJ_ERR_NUMERIC) {  // per-column outcomes are in status_out
+    bool any_ok = false;
+    for (int r = 0; r < k; r++) any_ok = any_ok || stat[r] == FJ_OK;
+    if (any_ok) rc = FJ_OK;
+  }
+  return rc;
 }
 
 

@@ -21,6 +21,8 @@
 // A separate compensated fp64 pass (certificate) re-checks max |r_v|/h_v.
 #include <stdlib.h>
 
+#include <vector>
+
 
 #include "sweep_common.cuh"
 
@@ -582,35 +584,50 @@ fj_status fj_omega_sweep(fj_graph_t g, const float *s, double eps, double lo, do
     fj::set_error("fj_omega_sweep: bad argument");
     return FJ_ERR_INVALID;
   }
+  if (method == FJ_METHOD_PUSH) {
+    fj::set_error("fj_omega_sweep: the sweep runs batched (ASYNC / COLORED), not PUSH");
+    return FJ_ERR_INVALID;
+  }
   const int cap = *npts;
-  int k = 0;
-  double best = 1.0;
-  int64_t best_cost = -1;
-  float *z = nullptr;
-  FJ_CUDA(cudaMallocAsync(&z, sizeof(float) * g->n, g->stream));
-  fj_opts o;
-  fj_opts_default(&o);
-  o.method = method;
   // the paper's heuristic: start near 2, lower ω by a fixed step to 1,
-  // keep the ω with the fewest updates; diverging ω cost +inf
+  // keep the ω with the fewest updates; diverging ω cost +inf.  The
+  // grid runs as ω batches of up to 8 columns (fj_solve_batch_omega): one
+  // schedule for every ω of the grid, one set of CSR streams per batch.
+  std::vector<double> grid;
   for (int i = 0;; i++) {
     const double om = hi - i * step;
     if (om < lo - 1e-12) break;
+    grid.push_back(om);
+  }
+  float *z = nullptr;
+  FJ_CUDA(cudaMallocAsync(&z, sizeof(float) * g->n * 8, g->stream));
+  fj_opts o;
+  fj_opts_default(&o);
+  o.method = method;
+  double best = 1.0;
+  int64_t best_cost = -1;
+  int k = 0;
+  for (size_t c0 = 0; c0 < grid.size(); c0 += 8) {
+    const int kc = (int)std::min<size_t>(8, grid.size() - c0);
+    int64_t rel[8];
+    int stat[8];
     fj_stats st;
-    fj_status rc = fj_solve_ex(g, s, eps, om, &o, z, &st);
+    fj_status rc = fj_solve_batch_omega(g, s, kc, grid.data() + c0, eps, &o, z, &st, rel, stat);
     if (rc != FJ_OK && rc != FJ_ERR_NUMERIC) {
       cudaFreeAsync(z, g->stream);
       return rc;
     }
-    if (table && k < cap) {
-      table[3 * k] = om;
-      table[3 * k + 1] = (double)st.relaxations;
-      table[3 * k + 2] = (double)rc;
-    }
-    k++;
-    if (rc == FJ_OK && (best_cost < 0 || st.relaxations <= best_cost)) {
-      best_cost = st.relaxations;  // ties go to the smaller ω
-      best = om;
+    for (int r = 0; r < kc; r++, k++) {
+      const double om = grid[c0 + r];
+      if (table && k < cap) {
+        table[3 * k] = om;
+        table[3 * k + 1] = (double)rel[r];
+        table[3 * k + 2] = (double)stat[r];
+      }
+      if (stat[r] == FJ_OK && (best_cost < 0 || rel[r] <= best_cost)) {
+        best_cost = rel[r];  // ties go to the smaller ω: later in the walk
+        best = om;
+      }
     }
   }
   cudaFreeAsync(z, g->stream);

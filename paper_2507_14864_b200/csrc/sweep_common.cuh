@@ -58,6 +58,9 @@ struct KP {
   int ncolors;
   int kreal;                // batched solves: right-hand sides that count (the rest is padding)
   int tail_pct;             // k_sweep: percent of each phase's items claimed dynamically at its end
+  const double *omegas;     // ω batch (fj_solve_batch_omega): ω per column [K]; else null
+  int *colbad;              // ω batch: per-column divergence flags [K]; null otherwise
+  unsigned long long *colupd;  // ω batch: per-column relaxations [K]
   int tail_phase;           // merged tail colors (reading R23); −1 if none
   int64_t tail_row0, tail_row1;  // rows of the tail phase (empty range if none)
   const float *tail_beta;   // per tail row: β_i (see color.cu)
@@ -728,6 +731,7 @@ size_t sweep_kernel_smem();
 fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double omega,
                           const fj_opts *o, float *z_out, fj_stats *st_out);
 fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, double omega,
-                           const fj_opts *o, float *Z_out, fj_stats *st_out);
+                           const fj_opts *o, float *Z_out, fj_stats *st_out,
+                           const double *omegas, int64_t *relax_out, int *status_out);
 
 }  // namespace fj
