@@ -1,7 +1,7 @@
 // tma_gather.cu — diagnostics, not part of libfj: can TMA tile::gather4 move
 // random fp64 gathers off the L1TEX LSU path?  The pull sweep is bound by L1TEX
 // wavefronts (one per 128-byte line a warp-wide gather touches, ≈ 1 per SM
-// clock).  A gather4 fetches four 16-byte rows of a 2-D tensor map
+// clock).  A gather4 fetches four 32-byte rows of a 2-D tensor map
 // straight from L2 into shared memory (async proxy, no LSU wavefronts, no L1
 // line allocated per miss).  This probe streams col and sums x[col] over m arcs
 //   mode 0: LDG gathers (the sweep's path), 4 arcs per lane per step, 2 steps in flight
@@ -71,16 +71,17 @@ __device__ double ldg_part(const int *col, const double *x, int64_t c0, int64_t 
 
 // TMA path over chunks [c0, c1), kS chunks in flight per warp
 __device__ double tma_part(const int *col, const CUtensorMap *tm, int64_t c0, int64_t c1,
-                           int64_t wi, int64_t nwarps, double2 *buf, uint64_t *bars) {
+                           int64_t wi, int64_t nwarps, double *buf, uint64_t *bars) {
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
   int4 hold[kS];
   auto issue = [&](int s, int64_t c) {
     const int4 cc = ld_col4(col + c * kChunk + 4 * lane);
     hold[s] = cc;
-    if (lane == 0) mbar_expect(bars + s, kChunk * 16);
+    if (lane == 0) mbar_expect(bars + s, kChunk * 32);
     __syncwarp();
-    g4(buf + s * kChunk + 4 * lane, tm, make_int4(cc.x >> 1, cc.y >> 1, cc.z >> 1, cc.w >> 1),
+    // 128-byte aligned destination: four 32-byte rows (one L2 sector each)
+    g4(buf + (s * kChunk + 4 * lane) * 4, tm, make_int4(cc.x >> 2, cc.y >> 2, cc.z >> 2, cc.w >> 2),
        bars + s);
   };
   int64_t it = 0;
@@ -95,11 +96,18 @@ __device__ double tma_part(const int *col, const CUtensorMap *tm, int64_t c0, in
       const int64_t c = cb + s * nwarps;
       if (c >= c1) break;
       mbar_wait(bars + s, (uint32_t)(it & 1));
+      // read back with few bank conflicts: in read step u lane l takes row
+      // i = l % 4 of issuer lane 8u + l / 4 (its column offset comes by shuffle)
       const int4 cc = hold[s];
-      const double2 *q = buf + s * kChunk + 4 * lane;
-      const double2 a = q[0], b = q[1], d = q[2], e = q[3];
-      acc += (cc.x & 1 ? a.y : a.x) + (cc.y & 1 ? b.y : b.x) + (cc.z & 1 ? d.y : d.x) +
-             (cc.w & 1 ? e.y : e.x);
+      const double *q = buf + (size_t)s * kChunk * 4;
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int src = 8 * u + (lane >> 2), i = lane & 3;
+        const int cx = __shfl_sync(0xffffffffu, cc.x, src), cy = __shfl_sync(0xffffffffu, cc.y, src);
+        const int cz = __shfl_sync(0xffffffffu, cc.z, src), cw = __shfl_sync(0xffffffffu, cc.w, src);
+        const int cj = i == 0 ? cx : (i == 1 ? cy : (i == 2 ? cz : cw));
+        acc += q[src * 16 + i * 4 + (cj & 3)];
+      }
       __syncwarp();
       const int64_t cn = c + (int64_t)kS * nwarps;
       if (cn < c1) issue(s, cn);
@@ -121,8 +129,8 @@ __global__ void __launch_bounds__(256, 4) k_probe(int mode, int64_t nchunks, con
     const int tw = mode == 1 ? nw : tma_warps;
     const int64_t tc = mode == 1 ? nchunks : tma_chunks;
     if (wib < tw) {
-      double2 *buf = reinterpret_cast<double2 *>(sm) + (size_t)wib * kS * kChunk;
-      uint64_t *bars = reinterpret_cast<uint64_t *>(sm + (size_t)tw * kS * kChunk * 16) + wib * kS;
+      double *buf = reinterpret_cast<double *>(sm) + (size_t)wib * kS * kChunk * 4;
+      uint64_t *bars = reinterpret_cast<uint64_t *>(sm + (size_t)tw * kS * kChunk * 32) + wib * kS;
       if (lane == 0)
         for (int s = 0; s < kS; s++) mbar_init(bars + s);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -176,9 +184,9 @@ extern "C" float tg_run(int mode, int64_t m, const int *col, const double *x, in
     enc = (EncodeFn)fp;
   }
   CUtensorMap tm;
-  const cuuint64_t dims[2] = {2, (cuuint64_t)((n + 1) / 2)};
-  const cuuint64_t strides[1] = {16};
-  const cuuint32_t box[2] = {2, 1};
+  const cuuint64_t dims[2] = {4, (cuuint64_t)((n + 3) / 4)};
+  const cuuint64_t strides[1] = {32};
+  const cuuint32_t box[2] = {4, 1};
   const cuuint32_t es[2] = {1, 1};
   const CUtensorMapL2promotion pr =
       l2promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
@@ -191,7 +199,7 @@ extern "C" float tg_run(int mode, int64_t m, const int *col, const double *x, in
   const int64_t nchunks = m / kChunk;
   const int nw = threads / 32;
   const int tw = mode == 1 ? nw : (mode == 2 ? tma_warps : 0);
-  const size_t smem = (size_t)tw * kS * (kChunk * 16 + 8);
+  const size_t smem = (size_t)tw * kS * (kChunk * 32 + 8);
   cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);

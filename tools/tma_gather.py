@@ -38,17 +38,17 @@ if "--c4" in sys.argv:
     del c, rows, idx
 
 for name, n, m, col in sets:
-    x = torch.rand(n + 2, dtype=torch.float64, device=dev)
+    x = torch.rand(n + 4, dtype=torch.float64, device=dev)
     def run(mode, cps=4, thr=256, tw=0, frac=0.0, promo=0, reps=7):
         return L.tg_run(mode, m, col.data_ptr(), x.data_ptr(), n, cps, thr, tw, frac, promo, reps)
     print(f"{name}: m={m} n={n}", flush=True)
     t0 = run(0)
     print(f"  LDG 4x256                        {t0:.3f} ms  ({m / t0 / 1e6:.1f} G gathers/s)", flush=True)
-    for cps, thr in ((2, 256), (3, 256), (1, 512), (4, 128)):
+    for cps, thr in ((1, 256), (1, 128), (2, 128), (3, 128)):
         for promo in (0, 2):
             t = run(1, cps, thr, promo=promo)
             print(f"  TMA {cps}x{thr} promo={promo}               {t:.3f} ms  ({m / t / 1e6:.1f} G/s)", flush=True)
-    for tw in (1, 2, 3):
+    for tw in (1, 2):
         for frac in (0.2, 0.3, 0.4, 0.5):
             t = run(2, 4, 256, tw, frac)
             print(f"  hybrid 4x256 tma_warps={tw} frac={frac:.1f}  {t:.3f} ms  ({m / t / 1e6:.1f} G/s)",
