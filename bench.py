@@ -248,11 +248,24 @@ def streamed_bytes(st, weighted: bool, empty_rows: int):
 
 
 def lib_fingerprint():
-    """sha256 (16 hex) of the loaded libfj.so: ties an ncu capture to its build."""
+    """sha256 (16 hex) of the SASS of the loaded libfj.so (cuobjdump, source paths
+    dropped): ties an ncu capture to its machine code.  The .so bytes themselves
+    differ between checkouts (-lineinfo records the build path)."""
     import hashlib
     import paper_2507_14864_b200 as fj
-    with open(fj.LIB_PATH, "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()[:16]
+    return sass_fingerprint(fj.LIB_PATH)
+
+
+def sass_fingerprint(path):
+    import hashlib
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True,
+                             timeout=120).stdout
+    except Exception:
+        return None
+    keep = [ln for ln in out.splitlines() if ln and "identifier" not in ln and
+            not ln.startswith("Fatbin")]
+    return hashlib.sha256("\n".join(keep).encode()).hexdigest()[:16] if keep else None
 
 
 def run_ours(args, prob, world, rank, local):
@@ -317,7 +330,8 @@ def run_ours(args, prob, world, rank, local):
             # ncu's dram bytes per sweep of its captured launch × this launch's
             # sweeps — only if the capture was taken on this very build
             tj = json.load(open(prof))
-            if tj.get("lib_sha16") == lib_fingerprint() and args.config == tj.get("config", 4):
+            fp = lib_fingerprint()
+            if fp and tj.get("sass_sha16") == fp and args.config == tj.get("config", 4):
                 traffic = tj["dram_bytes_per_sweep"] * st0.sweeps
                 traffic_src = tj.get("source")
         except Exception:
@@ -388,7 +402,7 @@ def run_ours(args, prob, world, rank, local):
                                         "+ 36 B per relaxation (row_ptr, s, z_i r/w, 1+d)",
                          "streamed_bytes_per_launch": sb,
                          "streamed_gbs": sb / (st0.sweep_ms / 1e3) / 1e9,
-                         "traffic_source": traffic_src, "lib_sha16": lib_fingerprint()},
+                         "traffic_source": traffic_src, "sass_sha16": lib_fingerprint()},
             "gather_ceiling": ceiling,
             "batched": batched,
             "omega_sweep": omega_table,

@@ -1,5 +1,5 @@
 """Refresh profiles/ncu_sweep_traffic.json from an ncu capture of k_sweep on
-the CURRENT build (bench.py uses it only when lib_sha16 matches the loaded
+the CURRENT build (bench.py uses it only when sass_sha16 matches the loaded
 libfj.so).  Run on the GPU box:
 
     ncu --set full --clock-control none --import-source on -k regex:k_sweep -c 1 \\
@@ -20,10 +20,12 @@ def get(name):
     return float(vals[i].replace(",", "")) * scale
 rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
 lib = os.path.join(ROOT, "paper_2507_14864_b200", "libfj.so")
-sha = hashlib.sha256(open(lib, "rb").read()).hexdigest()[:16]
+sys.path.insert(0, ROOT)
+from bench import sass_fingerprint  # noqa: E402
+sha = sass_fingerprint(lib)
 out = {"kernel": vals[hdr.index("Kernel Name")], "config": 4, "source": os.path.basename(rep),
        "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
        "sweeps_in_launch": sweeps, "dram_bytes_per_sweep": (rd + wr) / sweeps,
-       "duration_ms": get("gpu__time_duration.sum"), "lib_sha16": sha}
+       "duration_ms": get("gpu__time_duration.sum"), "sass_sha16": sha}
 json.dump(out, open(os.path.join(ROOT, "profiles", "ncu_sweep_traffic.json"), "w"), indent=1)
 print(json.dumps(out))
