@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define FJ_ABI_VERSION 2
+#define FJ_ABI_VERSION 3
 
 typedef struct fj_graph *fj_graph_t;
 
@@ -95,6 +95,13 @@ typedef struct {
                         < n / push_sparse_div rows; <= 0 → 8                            */
   /* The coloring and tail merge are built at the first COLORED solve of a graph and
      rebuilt if a later solve asks for a different coloring or tail_frac. */
+  int shadow;        /* ASYNC/COLORED: 1 = the sweeps gather from a 32-bit fixed-point
+                        shadow of ẑ' (4 B per gather) until a sweep relaxes
+                        nothing or only the shadow's rounding noise, then fp64 sweeps from
+                        the same ẑ' finish the ε rule (Lemma 3) and the fp64
+                        certificate decides as always; 0 = fp64 sweeps only; < 0
+                        (default) → 1 on hub-dominated graphs (rows above 256 arcs hold
+                        over half the arcs), else 0                                     */
 } fj_opts;
 
 typedef struct {
@@ -113,6 +120,8 @@ typedef struct {
   double solve_ms;       /* device time of the whole solve (CUDA events, graph stream) */
   double sweep_ms;       /* device time inside the sweep kernel launches               */
   double cert_ms;        /* device time inside the certificate kernel                  */
+  int64_t shadow_sweeps; /* of `sweeps`: those that gathered from the shadow           */
+  double shadow_ms;      /* of `sweep_ms`: device time of the shadow sweep launch      */
 } fj_stats;
 
 typedef struct {

@@ -43,7 +43,7 @@ class _Opts(ctypes.Structure):
                 ("certify", ctypes.c_int), ("zprime_out", ctypes.c_void_p),
                 ("z_init", ctypes.c_void_p), ("tail_frac", ctypes.c_double),
                 ("coloring", ctypes.c_int), ("push_compact", ctypes.c_int),
-                ("push_sparse_div", ctypes.c_int)]
+                ("push_sparse_div", ctypes.c_int), ("shadow", ctypes.c_int)]
 
 
 class _Stats(ctypes.Structure):
@@ -54,7 +54,8 @@ class _Stats(ctypes.Structure):
                 ("c", ctypes.c_double), ("eps_prime", ctypes.c_double),
                 ("colors", ctypes.c_int), ("status", ctypes.c_int), ("reason", ctypes.c_int),
                 ("solve_ms", ctypes.c_double), ("sweep_ms", ctypes.c_double),
-                ("cert_ms", ctypes.c_double)]
+                ("cert_ms", ctypes.c_double), ("shadow_sweeps", ctypes.c_int64),
+                ("shadow_ms", ctypes.c_double)]
 
 
 class _Info(ctypes.Structure):
@@ -186,6 +187,8 @@ class SolveStats:
     solve_ms: float
     sweep_ms: float
     cert_ms: float
+    shadow_sweeps: int = 0
+    shadow_ms: float = 0.0
 
 
 class Graph:
@@ -233,8 +236,10 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
           sigma: float = 1e-5, c: float = 0.0, max_sweeps: int = 0, cert_rounds: int = -1,
           certify: bool = True, zprime_out=None, raise_on_numeric: bool = True,
           z_init=None, tail_frac: float = -1.0, coloring: str = "spec",
-          push_compact: bool = False, push_sparse_div: int = 8) -> SolveStats:
+          push_compact: bool = False, push_sparse_div: int = 8,
+          shadow: int = -1) -> SolveStats:
     """fj_solve_ex: writes z into ``z_out`` (float32[n]); returns the stats.
+    ``shadow``: fj_opts.shadow (1 = shadow sweeps, 0 = fp64 only, −1 = library default).
     ``z_init`` (float64[n], optional): warm start / resume from an earlier z.
     Schedule options (fj_opts): ``tail_frac`` (COLORED tail merge, R23; 0 =
     exact multicolor SOR), ``coloring`` ("spec" or "jp"), ``push_compact`` /
@@ -248,6 +253,7 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
     o.max_sweeps, o.cert_rounds, o.certify = max_sweeps, cert_rounds, int(certify)
     o.tail_frac, o.coloring = float(tail_frac), {"spec": 0, "jp": 1}[coloring]
     o.push_compact, o.push_sparse_div = int(bool(push_compact)), int(push_sparse_div)
+    o.shadow = int(shadow)
     zp = _ptr(zprime_out)
     o.zprime_out = zp.value if zp is not None else None
     _dtype_ok(z_init, "z_init", "float64", g.n)

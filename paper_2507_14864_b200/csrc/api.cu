@@ -81,6 +81,7 @@ void fj_opts_default(fj_opts *o) {
   o->coloring = 0;
   o->push_compact = 0;
   o->push_sparse_div = 8;
+  o->shadow = -1;
 }
 
 fj_status fj_graph_get_info(fj_graph_t g, fj_graph_info *info) {

@@ -48,7 +48,17 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
   unsigned long long tot_upd = 0, tot_eu = 0;
   int sweeps = 0, reason = 1;
   int phase = 0;
-  for (int sw = 0; sw < p.max_sweeps; ++sw) {
+  int max_sweeps = p.max_sweeps;
+  int sweeps0 = 0;
+  if (p.prev) {
+    // fp64 tail of a shadow solve: the totals continue those of the shadow launch
+    // (whatever ended it: the tail restarts from ẑ, Lemma 3)
+    sweeps0 = (int)__ldcg(p.prev);
+    tot_upd = __ldcg(p.prev + 1);
+    tot_eu = __ldcg(p.prev + 2);
+    max_sweeps = max(1, max_sweeps - sweeps0);
+  }
+  for (int sw = 0; sw < max_sweeps; ++sw) {
     for (int k = 0; k < p.ncolors; ++k, ++phase) {
       const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
       const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
@@ -91,7 +101,79 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
     if (bad) { reason = 2; break; }
     if (done) { reason = 0; break; }
   }
+  sweep_result(p.out, sweeps0 + sweeps, tot_upd, tot_eu, reason);
+}
+
+// Shadow sweeps (fj_opts.shadow): k_sweep with the ẑ gathers served by the 32-bit
+// fixed-point shadow of ẑ' (sweep_common.cuh: sh_dec) — 4 B per gather as SURVEY §8(d)
+// counts them, and the whole shadow (n·4 B) stays in L2 where fp64 ẑ' (n·8 B) does not on
+// C4.  A relaxed row stores its fp64 ẑ' and its shadow.  The shadow loop ends like
+// k_sweep's (a sweep without relaxations, the sentinel, the watchdog), when a value
+// leaves the shadow's range, or when a sweep moved no ẑ' by ≥ 4 shadow quanta (it is then
+// relaxing the shadow's rounding noise); the fp64 sweeps of k_sweep then run from the
+// same ẑ' until nothing relaxes (Lemma 3: ẑ alone determines r), and the
+// compensated certificate decides as always.
+template <bool W>
+__global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_sh(KP p) {
+  extern __shared__ double s_prod[];
+  __shared__ unsigned long long s_dec[3];
+  __shared__ Scalars sS;
+  if (threadIdx.x == 0) sS = *p.sc;
+  __syncthreads();
+  const Scalars &S = sS;
+  TAcc t{};
+  unsigned long long tot_upd = 0, tot_eu = 0;
+  int sweeps = 0, reason = 1;
+  int phase = 0;
+  for (int sw = 0; sw < p.max_sweeps; ++sw) {
+    for (int k = 0; k < p.ncolors; ++k, ++phase) {
+      const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+      const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
+      const int stride = gridDim.x * (kBlock / 32);
+      double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
+      const int ns = nr - (int)((long long)nr * p.tail_pct / 100);
+      unsigned *claim = p.ctr + (phase % 3);
+      if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[(phase + 2) % 3] = 0u;
+      int wi = warp_id;
+      Task nxt;
+      if (wi < ns) nxt = p.rtasks[r0 + wi];
+      while (wi < ns) {
+        const Task cur = nxt;
+        const int wn = wi + stride;
+        if (wn < ns) nxt = p.rtasks[r0 + wn];
+        if ((cur.kind & 0xff) == kWarp) do_warp<RELAX, W, 1>(p, S, cur, t);
+        else relax_warp_tile<W, 1>(p, S, cur, t, wprod);
+        wi = wn;
+      }
+      for (; ns < nr;) {
+        int c = 0;
+        if ((threadIdx.x & 31) == 0) c = ns + (int)atomicAdd(claim, 1u);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c >= nr) break;
+        const Task cur = p.rtasks[r0 + c];
+        if ((cur.kind & 0xff) == kWarp) do_warp<RELAX, W, 1>(p, S, cur, t);
+        else relax_warp_tile<W, 1>(p, S, cur, t, wprod);
+      }
+      if (k + 1 < p.ncolors) grid_sync(p.bar);
+    }
+    unsigned long long dec[3];
+    sweep_totals(p.cnt, p.bar, sw, t, s_dec, dec);
+    tot_upd += dec[0];
+    tot_eu += dec[1];
+    sweeps = sw + 1;
+    // dec[2]: bit 0 = sentinel or shadow range, bit 1 = some move of ≥ 4 quanta
+    const bool bad = (dec[2] & 1) != 0, done = dec[0] == 0 || (dec[2] & 2) == 0;
+    if (bad) { reason = 2; break; }
+    if (done) { reason = 0; break; }
+  }
   sweep_result(p.out, sweeps, tot_upd, tot_eu, reason);
+}
+
+// shadow init: zs = encode(ẑ') for every row
+__global__ void k_shadow_init(int64_t n, const double *__restrict__ z, const Scalars *__restrict__ S,
+                              unsigned *__restrict__ zs) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) zs[i] = __double2uint_rn(z[i] * S->sh_enc);
 }
 
 // measures node pass: z into layout order (fp64) + Σz
@@ -163,6 +245,11 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   }
   const Layout &L = (method == FJ_METHOD_COLORED) ? g->color_layout : g->async_layout;
   const bool W = g->weighted != 0;
+  // shadow sweeps (fj_opts.shadow; default: on hub-dominated layouts, where the warp units
+  // hold over half the arcs — C2 / C4 gain 5–8 % per sweep, the short-row layouts C3 / C5
+  // lose as much to the extra shadow store and decode, profiles/r02_shadow_*.txt)
+  const bool use_shadow =
+      L.m > 0 && (o->shadow > 0 || (o->shadow < 0 && 2 * L.warp_unit_arcs > L.m));
 
   Workspace ws(st);
   cudaEvent_t e0, e1, es0, es1, ec0, ec1;
@@ -183,6 +270,8 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   unsigned *ctl = nullptr;  // ctr[3] + bar[2]
   SweepCounters *cnt = nullptr;
   unsigned long long *outv = nullptr, *certbits = nullptr;
+  unsigned *zs = nullptr;
+  if (use_shadow) FJ_CUDA(ws.alloc(&zs, n));
   FJ_CUDA(ws.alloc(&s_l, n));
   FJ_CUDA(ws.alloc(&z, n));
   FJ_CUDA(ws.alloc(&smin, 2));
@@ -192,7 +281,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   FJ_CUDA(ws.alloc(&arrive, std::max(1, L.npartials)));
   FJ_CUDA(ws.alloc(&ctl, kCtlWords));
   FJ_CUDA(ws.alloc(&cnt, 3));
-  FJ_CUDA(ws.alloc(&outv, 8));
+  FJ_CUDA(ws.alloc(&outv, 12));  // [0..3] sweep result, [4] certificate, [8..11] shadow result
   certbits = outv + 4;
   if (!zdev) FJ_CUDA(ws.alloc(&zo, n));
   if (o->zprime_out && !zpdev) FJ_CUDA(ws.alloc(&zp, n));
@@ -200,7 +289,8 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   // a2: shift and init (Alg. 2)
   FJ_TRY(minmax_f32(s.dev, n, smin, ws, g->num_sms));  // smin[0] = min s, smin[1] = smax = max s
   fj::count_launch();
-  k_scalars<<<1, 1, 0, st>>>(smin, smax, eps, o->sigma, o->c, S);
+  k_scalars<<<1, 1, 0, st>>>(smin, smax, eps, o->sigma, o->c, S,
+                             (omega > 1.0 || o->z_init) ? 1 : 0);
   const double *zinit = nullptr;
   double *zinit_owned = nullptr;
   if (o->z_init) {
@@ -214,8 +304,13 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   }
   fj::count_launch();
   k_init<<<gridn(n), kBlock, 0, st>>>(n, L.perm, L.rp, s.dev, S, s_l, z, zinit);
+  if (use_shadow) {
+    fj::count_launch();
+    k_shadow_init<<<gridn(n), kBlock, 0, st>>>(n, z, S, zs);
+  }
 
   KP p = make_kp(g, L);
+  p.zs = zs;
   p.s = s_l;
   p.z = z;
   p.sc = S;
@@ -253,18 +348,44 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault));
   const int grid = persistent_grid(fn, g->num_sms, sweep_smem);
-  float ms_sweep = 0, ms_cert = 0;
+  // shadow launch: the fp64 kernel's shape (same staging, carveout and grid)
+  const void *shfn = W ? (const void *)k_sweep_sh<true> : (const void *)k_sweep_sh<false>;
+  int sh_grid = 0;
+  if (use_shadow) {
+    FJ_CUDA(cudaFuncSetAttribute(shfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem));
+    FJ_CUDA(cudaFuncSetAttribute(shfn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault));
+    sh_grid = persistent_grid(shfn, g->num_sms, sweep_smem);
+  }
+  cudaEvent_t esh;
+  FJ_CUDA(ws.event(&esh));
+  float ms_sweep = 0, ms_cert = 0, ms_shadow = 0;
   int rounds = 0;
   stats.colors = L.ncolors;
   for (;;) {
     // a3–a5: persistent sweeps with on-device loop control
     FJ_CUDA(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * kCtlWords, st));
     FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(SweepCounters) * 3, st));
-    FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 8, st));
+    FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 12, st));
     // hub-piece arrival counters start at 0 for every launch (a resumed
     // sweep or the certificate never inherits a half-finished count)
     FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
     FJ_CUDA(cudaEventRecord(es0, st));
+    const bool sh_round = use_shadow && rounds == 0;  // resumes run in fp64 only
+    p.prev = nullptr;
+    if (sh_round) {
+      KP q = p;
+      q.out = outv + 8;
+      void *args[] = {&q};
+      fj::count_launch();
+      FJ_CUDA(cudaLaunchCooperativeKernel(shfn, sh_grid, kBlock, args, sweep_smem, st));
+      FJ_CUDA(cudaEventRecord(esh, st));
+      // the fp64 sweeps start from counters at rest (ring slots, claim words, arrivals)
+      FJ_CUDA(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * kCtlWords, st));
+      FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(SweepCounters) * 3, st));
+      FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
+      p.prev = outv + 8;
+    }
     {
       void *args[] = {&p};
       fj::count_launch();
@@ -283,12 +404,17 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
       FJ_CUDA(cudaLaunchKernel(cf, persistent_grid(cf, g->num_sms), kBlock, cargs, 0, st));
       FJ_CUDA(cudaEventRecord(ec1, st));
     }
-    unsigned long long h[8];
+    unsigned long long h[12];
     FJ_CUDA(cudaMemcpyAsync(h, outv, sizeof(h), cudaMemcpyDeviceToHost, st));
     FJ_CUDA(cudaStreamSynchronize(st));
     float a = 0;
     FJ_CUDA(cudaEventElapsedTime(&a, es0, es1));
     ms_sweep += a;
+    if (sh_round) {
+      FJ_CUDA(cudaEventElapsedTime(&a, es0, esh));
+      ms_shadow += a;
+      stats.shadow_sweeps += (int64_t)h[8];
+    }
     if (o->certify) {
       FJ_CUDA(cudaEventElapsedTime(&a, ec0, ec1));
       ms_cert += a;
@@ -328,6 +454,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   FJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   stats.solve_ms = ms;
   stats.sweep_ms = ms_sweep;
+  stats.shadow_ms = ms_shadow;
   stats.cert_ms = ms_cert;
   stats.c = hs.c;
   stats.eps_prime = hs.eps_p;

@@ -30,6 +30,9 @@ struct Scalars {
   double sentinel; // divergence sentinel 1e6·max|s'|
   int floored;
   int bad_input;
+  // shadow ẑ (k_sweep_sh): fixed point on [0, 2^e), 2^e ≥ max s' (twice that when ω > 1 or
+  // warm-started): decode fma(2^52 + u, sh_scale, sh_off) = u·2^(e−32); encode ẑ'·sh_enc
+  double sh_scale, sh_off, sh_enc;
 };
 
 struct SweepCounters {
@@ -76,6 +79,9 @@ struct KP {
   double *rout;                  // CERT: optional residual output (layout order)
   const unsigned long long *stop;  // sharded solve: nonzero = the loop has ended (k_sweep)
   int64_t empty0, empty1;  // rows with no arcs (the layout's last group): CERT covers them too
+  // shadow sweeps (k_sweep_sh, solve.cu): 32-bit fixed-point copy of ẑ' for the gathers
+  unsigned *zs;            // [n] layout order: u = round(ẑ'·S.sh_enc), ẑ' ≈ u·S.sh_scale
+  const unsigned long long *prev;  // out[] of the launch before this one (fp64 tail after shadow)
 };
 
 // CSR streams are read once per sweep: read-only path, no L1 allocation, so
@@ -100,6 +106,14 @@ __device__ __forceinline__ float ld_stream(const float *q) {
 // and every color phase read current values.
 // (weak loads: the compiler may batch them; __ldca compiles to a strong load)
 __device__ __forceinline__ double ld_z(const double *q) { return *q; }
+
+// Shadow ẑ (k_sweep_sh): the gathers read a 32-bit fixed-point copy of ẑ'
+// (4 B per gather, the whole copy resident in L2; SURVEY §8(d) "fp32 shadow",
+// fixed point because ẑ' is bounded: its error is uniform, ≤ 2^-33·range).
+// decode: u·scale, exact, as one FMA on the double 2^52 + u (no I2F).
+__device__ __forceinline__ double sh_dec(unsigned u, double scale, double off) {
+  return fma(__hiloint2double(0x43300000, (int)u), scale, off);
+}
 
 // Hub-row pieces (see do_warp): a piece's partial sum is stored, then its
 // arrival is counted with release semantics (MEMBAR.ALL.GPU orders the store
@@ -189,6 +203,7 @@ __device__ __forceinline__ double residual_dd(dd sum, double sp, double d1, doub
 }
 
 // relax one row from its residual; row state loaded by the caller (prefetched)
+template <int SH = 0>
 __device__ __forceinline__ void relax_row_pre(const KP &p, const Scalars &S, int row, int len,
                                               dd total, float sv, double zi, double d1, TAcc &t) {
   const double sp = (double)sv + S.c;
@@ -200,11 +215,25 @@ __device__ __forceinline__ void relax_row_pre(const KP &p, const Scalars &S, int
     double om = p.omega;
     if (row >= p.tail_row0 && row < p.tail_row1)
       om = fmin(om, 1.98 / (1.0 + (double)p.tail_beta[row - p.tail_row0]));
-    __stcg(p.z + row, zi + om * rho / d1);
+    const double zn = zi + om * rho / d1;
+    __stcg(p.z + row, zn);
+    if constexpr (SH != 0) {
+      // outside the shadow's range [0, 2^e): the shadow loop ends and the fp64 sweeps
+      // carry on from ẑ (Lemma 3: any ẑ is a valid state)
+      const double ze = zn * S.sh_enc;
+      if (!(ze >= 0.0 && ze <= 4294967295.0)) t.bad |= 1;
+      // bit 1: this sweep still moved some ẑ' by ≥ 4 shadow quanta.  The shadow's own
+      // rounding can move a row by < ω quanta at most (Σ_j a_ij·½ quantum·ω/(1+d_i)), so
+      // a sweep without such a move is relaxing rounding noise (at ω ≠ 1 that noise need
+      // not die out): the shadow loop ends and the fp64 sweeps take over
+      if (fabs(zn - zi) * S.sh_enc >= 4.0) t.bad |= 2;
+      const unsigned u = __double2uint_rn(ze);
+      __stcg(p.zs + row, u);
+    }
     t.upd++;
     t.eu += (unsigned long long)len;
   }
-  if (!(ar <= S.sentinel)) t.bad = 1;
+  if (!(ar <= S.sentinel)) t.bad |= 1;
 }
 
 template <bool W>
@@ -287,10 +316,14 @@ __device__ __forceinline__ A block_reduce(A a, A *sm) {
 // with shuffles (no block barrier).
 // Pieces of one row are combined by the last-arriving warp in piece order
 // (deterministic).
-template <int MODE, bool W>
+// SH (RELAX only): 0 = fp64 ẑ gathers; 1 = shadow gathers (sh_dec of p.zs).
+// Shadow sums are plain fp64: the shadow's own rounding (2^-33·range per value) is far
+// above what double-double would recover; the fp64 tail sweeps and the certificate follow.
+template <int MODE, bool W, int SH = 0>
 __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Task &tk, TAcc &t) {
+  static_assert(SH == 0 || MODE == RELAX, "shadow gathers are a RELAX path");
   // rows above 256 arcs accumulate in double-double for RELAX and CERT
-  using A = typename std::conditional<MODE == DIS || MODE == SPMV, double, dd>::type;
+  using A = typename std::conditional<MODE == DIS || MODE == SPMV || SH != 0, double, dd>::type;
 #ifndef FJ_WU
 #define FJ_WU 4
 #endif
@@ -326,12 +359,22 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
     }
     // stage 2: all gathers
     double zj[U];
+    if constexpr (SH == 0) {
 #pragma unroll
-    for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
+      for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
+    } else {
+      unsigned zu[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) zu[u] = p.zs[j[u]];
+#pragma unroll
+      for (int u = 0; u < U; u++) zj[u] = sh_dec(zu[u], S.sh_scale, S.sh_off);
+    }
     // stage 3: accumulate
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      if constexpr (MODE == SPMV) {
+      if constexpr (SH != 0) {
+        a = fma((double)wv[u], zj[u], a);
+      } else if constexpr (MODE == SPMV) {
         a = fma((double)wv[u], zj[u], a);
       } else if constexpr (MODE != DIS) {
 #ifdef FJ_PLAIN_WARP
@@ -365,8 +408,11 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
     atomicAdd(p.rout + row, a);  // pieces of one row add up (y zeroed first)
     return;
   } else {
+    dd ad;
+    if constexpr (SH != 0) ad = dd{a, 0.0};
+    else ad = a;
     if (np > 1) {
-      __stcg(p.partial + slot + piece, make_double2(a.hi, a.lo));
+      __stcg(p.partial + slot + piece, make_double2(ad.hi, ad.lo));
       // cumulative arrival count: the np-th, 2np-th, ... arrival finishes the
       // row (no reset, so overlapping sweeps of the barrier-free kernel can
       // never lose an arrival; mixing partials of two sweeps is still a
@@ -376,20 +422,20 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
       // the hub ẑ gathers — once per hub piece.
       const int old = arrive_release(p.arrive + slot);
       if ((old + 1) % np != 0) return;
-      acc_zero(a);
+      acc_zero(ad);
       for (int q = 0; q < np; q++) {  // fixed order ⇒ deterministic row sum
         const double2 x = ld_partial(p.partial + slot + q);
-        acc_merge(a, dd{x.x, x.y});
+        acc_merge(ad, dd{x.x, x.y});
       }
     }
     if constexpr (MODE == RELAX) {
       // a non-final piece returned above; a multi-piece row is finished by
       // the last-arriving warp, whose prefetched ẑ_row is still current (only
       // this row's finisher writes it, once per phase)
-      relax_row_pre(p, S, row, len, a, sv, zi, d1, t);
+      relax_row_pre<SH>(p, S, row, len, ad, sv, zi, d1, t);
     } else {
       const int lenc = (int)(__ldg(p.rp + row + 1) - __ldg(p.rp + row));
-      cert_row<W>(p, S, row, lenc, a, t);
+      cert_row<W>(p, S, row, lenc, ad, t);
     }
   }
 }
@@ -401,7 +447,7 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
 //            col + w loads, then the ẑ gathers, products a_ij ẑ_j → smem;
 //   phase 2: each group sums its row's products from smem, lane 0 relaxes.
 // One __syncthreads per task (smem double-buffered across tasks).
-template <bool W>
+template <bool W, int SH = 0>
 __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, const Task &tk,
                                                 TAcc &t, double *wprod) {
   constexpr int U = kWarpTileArcs / 32;
@@ -427,8 +473,16 @@ __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, c
     wv[u] = W ? ld_stream(p.w + a0 + (ok ? e : 0)) : 1.0f;
   }
   double zj[U];
+  if constexpr (SH == 0) {
 #pragma unroll
-  for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
+    for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
+  } else {
+    unsigned zu[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) zu[u] = p.zs[j[u]];
+#pragma unroll
+    for (int u = 0; u < U; u++) zj[u] = sh_dec(zu[u], S.sh_scale, S.sh_off);
+  }
 #pragma unroll
   for (int u = 0; u < U; u++) {
     const int e = u * 32 + lane;
@@ -459,8 +513,8 @@ __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, c
     const int row = tk.a + q * ng + (lane >> cls);
     if (row < tk.b && gl == 0) {
       const int len = (int)(re[q] - rb[q]);
-      relax_row_pre(p, S, row, len, dd{a, 0.0}, sv[q], zi[q], W ? d1[q] : (double)(len + 1),
-                          t);
+      relax_row_pre<SH>(p, S, row, len, dd{a, 0.0}, sv[q], zi[q],
+                        W ? d1[q] : (double)(len + 1), t);
     }
   }
   __syncwarp();  // the slice is reused by this warp's next task
@@ -595,7 +649,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_pass(KP p) {
 
 // ----------------------------------------------------------- node kernels
 static __global__ void k_scalars(const float *__restrict__ smin, const float *__restrict__ smax,
-                          double eps, double sigma, double c_override, Scalars *S) {
+                          double eps, double sigma, double c_override, Scalars *S,
+                          int sh_wide = 0) {
   const double lo = (double)*smin, hi = (double)*smax;
   Scalars s{};
   s.bad_input = !(isfinite(lo) && isfinite(hi));
@@ -606,6 +661,14 @@ static __global__ void k_scalars(const float *__restrict__ smin, const float *__
   s.hs = s.floored ? sigma / (s.c + sigma) : s.eps_p;
   s.heps = 0.5 * eps;
   s.sentinel = 1e6 * fmax(fabs(hi + s.c), fabs(lo + s.c));
+  {
+    int e = 0;
+    const double top = (hi + s.c) * (sh_wide ? 2.0 : 1.0);
+    if (isfinite(top) && top > 0) frexp(top, &e);  // top < 2^e
+    s.sh_scale = ldexp(1.0, e - 32);
+    s.sh_enc = ldexp(1.0, 32 - e);
+    s.sh_off = -ldexp(1.0, e + 20);
+  }
   *S = s;
 }
 

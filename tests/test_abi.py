@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(L, name), name
     assert set(fj.EXPORTS) == set(_declared())
-    assert L.fj_abi_version() == 2
+    assert L.fj_abi_version() == 3
 
 
 def test_library_is_sm100a():

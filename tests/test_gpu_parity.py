@@ -868,3 +868,76 @@ def test_batch_omega_columns(dev, name):
     if not directed:
         assert all(x == 0 for x in stat)
         assert rel[2] < rel[0]   # over-relaxation needs fewer updates
+
+
+# ------------------------------------------------- shadow sweeps (fj_opts.shadow)
+# The sweeps gather from the 32-bit fixed-point shadow of ẑ' until nothing relaxes (or only
+# the shadow's rounding noise does), then fp64 sweeps finish: same bar as every solve — the
+# oracle's z, the oracle's certificate of the GPU's ẑ', P and D.
+@pytest.mark.parametrize("name", sorted(TINY))
+def test_shadow_async(dev, name):
+    rp, col, w, s, directed = TINY[name]()
+    st, z, ref = check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async", shadow=1)
+    assert 0 < st.shadow_sweeps < st.sweeps
+    # the shadow changes the path, not the answer: fp64-only solve of the same input
+    _, z0, _, st0 = gpu_solve(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async", shadow=0)
+    assert st0.shadow_sweeps == 0
+    assert rel_err(z, z0) <= 4e-6
+
+
+@pytest.mark.parametrize("name", ["er2000", "chunglu4k", "lattice64"])
+@pytest.mark.parametrize("omega", [1.25, 1.6])
+def test_shadow_colored_sor(dev, name, omega):
+    # floored thresholds (chunglu4k, lattice64: h ≈ 1e-11) lie far below the shadow's
+    # resolution: the shadow loop must hand over to fp64 (at ω ≠ 1 its rounding noise need
+    # not die out) instead of running into the watchdog
+    rp, col, w, s, directed = TINY[name]()
+    st, _, _ = check_parity(dev, rp, col, w, s, 1e-6, omega, directed, shadow=1, max_sweeps=20000)
+    assert 0 < st.shadow_sweeps < st.sweeps
+
+
+@pytest.mark.parametrize("name", ["rmat12", "rmat12w"])
+def test_shadow_async_sor_directed(dev, name):
+    rp, col, w, s, directed = TINY[name]()
+    st, _, _ = check_parity(dev, rp, col, w, s, 1e-6, 1.3, directed, method="async", ref_omega=1.0,
+                            shadow=1)
+    assert st.shadow_sweeps > 0
+
+
+@pytest.mark.parametrize("hub_deg", [300, 2049, 20000])
+def test_shadow_long_rows_star(dev, hub_deg):
+    # hub pieces (partials + arrival counters) under the shadow kernel, then under the fp64 tail
+    n = hub_deg + 1
+    edges = [(0, i) for i in range(1, n)]
+    rp, col, w = G.in_csr_from_edges(n, edges)
+    s = fjgen.uniform(n, 31)
+    st, _, _ = check_parity(dev, rp, col, w, s, 1e-6, 1.0, False, method="async", shadow=1)
+    assert st.shadow_sweeps > 0
+
+
+def test_shadow_warm_start_and_range(dev):
+    # a warm start far above max s' leaves the shadow's range [0, 2·2^e): the shadow loop
+    # ends at once and the fp64 sweeps solve from that ẑ (any ẑ is a valid state, Lemma 3)
+    rp, col, w, s, directed = TINY["er2000"]()
+    ref = oracle.solve(rp, col, w, s, 1e-6, 1.0)
+    for z0 in (np.full(len(s), 50.0), ref.z.copy()):
+        g, z, zp, st = gpu_solve(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async", shadow=1,
+                                 z_init=_t(z0, dev))
+        assert st.status == 0 and st.cert_ratio <= 1.0
+        assert rel_err(z, ref.z) <= 1e-4
+        ratio, _ = oracle.certificate(rp, col, w, s, zp, 1e-6)
+        assert ratio <= 1.0
+        g.close()
+
+
+def test_shadow_divergence_reported(dev):
+    # a diverging ω under the shadow kernel still ends in FJ_ERR_NUMERIC (range exit or
+    # sentinel, then the fp64 sweeps' own sentinel)
+    rp, col, w, s, directed = TINY["rmat12"]()
+    g, z, zp, st = gpu_solve(dev, rp, col, w, s, 1e-6, 1.95, directed, method="async",
+                             raise_on_numeric=False, shadow=1, max_sweeps=5000)
+    if st.status == 0:
+        assert oracle.certificate(rp, col, w, s, zp, 1e-6)[0] <= 1.0
+    else:
+        assert st.status == fj.FJ_ERR_NUMERIC and st.reason in (1, 2)
+    g.close()
