@@ -15,7 +15,8 @@ SW=$(python - "$TAG" <<'PY'
 import json, sys
 for line in open(f"gpurun_out/prof_{sys.argv[1]}.log"):
     if line.startswith("{"):
-        print(json.loads(line)["step_breakdown"]["sweeps"])
+        b = json.loads(line)["step_breakdown"]
+        print(b.get("shadow_sweeps") or b["sweeps"])  # sweeps of the captured (first) launch
 PY
 )
 python tools/ncu_traffic.py gpurun_out/prof_$TAG.ncu-rep "$SW" > gpurun_out/traffic_$TAG.json 2>&1
