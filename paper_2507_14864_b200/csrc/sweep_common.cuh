@@ -203,19 +203,31 @@ __device__ __forceinline__ double residual_dd(dd sum, double sp, double d1, doub
 }
 
 // relax one row from its residual; row state loaded by the caller (prefetched)
+// 1/x to ≈ 4e-15 relative (single-precision reciprocal + one Newton step): the size of a
+// relaxation step need not be exactly rounded (Lemma 3: any amount is a valid state)
+__device__ __forceinline__ double rcp_newton(double x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)x));
+  const double y = (double)r;
+  return y * fma(-x, y, 2.0);
+}
+
 template <int SH = 0>
 __device__ __forceinline__ void relax_row_pre(const KP &p, const Scalars &S, int row, int len,
                                               dd total, float sv, double zi, double d1, TAcc &t) {
   const double sp = (double)sv + S.c;
   const double h = threshold(S, sp);
-  const double rho = residual_dd(total, sp, d1, zi);
+  // shadow sweeps: plain fp64 combination (the shadow's rounding is far above its error)
+  const double rho = SH != 0 ? fma(-d1, zi, sp + total.hi) : residual_dd(total, sp, d1, zi);
   const double ar = fabs(rho);
   if (ar > p.theta * h) {
     // tail phase (R23): ω_i = min(ω, 1.98/(1+β_i)) keeps |1−ω_i| + ω_i β_i < 1
     double om = p.omega;
-    if (row >= p.tail_row0 && row < p.tail_row1)
+    if (p.tail_phase >= 0 && row >= p.tail_row0 && row < p.tail_row1)
       om = fmin(om, 1.98 / (1.0 + (double)p.tail_beta[row - p.tail_row0]));
-    const double zn = zi + om * rho / d1;
+    // (the fp64 kernel keeps the division: the reciprocal form costs it registers — spills)
+    const double dz = SH != 0 ? om * rho * rcp_newton(d1) : om * rho / d1;
+    const double zn = zi + dz;
     __stcg(p.z + row, zn);
     if constexpr (SH != 0) {
       // outside the shadow's range [0, 2^e): the shadow loop ends and the fp64 sweeps
@@ -226,7 +238,7 @@ __device__ __forceinline__ void relax_row_pre(const KP &p, const Scalars &S, int
       // rounding can move a row by < ω quanta at most (Σ_j a_ij·½ quantum·ω/(1+d_i)), so
       // a sweep without such a move is relaxing rounding noise (at ω ≠ 1 that noise need
       // not die out): the shadow loop ends and the fp64 sweeps take over
-      if (fabs(zn - zi) * S.sh_enc >= 4.0) t.bad |= 2;
+      if (fabs(dz) * S.sh_enc >= 4.0) t.bad |= 2;
       const unsigned u = __double2uint_rn(ze);
       __stcg(p.zs + row, u);
     }
@@ -491,6 +503,7 @@ __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, c
   __syncwarp();
 #pragma unroll
   for (int q = 0; q < 2; q++) {
+    if (SH != 0 && q == 1 && tk.a + ng >= tk.b) break;  // no rows left for the second step (uniform)
     {
       const int row = tk.a + q * ng + (lane >> cls);
       rb[q] = re[q] = 0;
