@@ -88,3 +88,31 @@ def test_binding_checks_lengths():
         fj.solve(G(), np.zeros(10, np.float64), np.zeros(10, np.float32), 1e-6)
     with pytest.raises(ValueError):
         fj.solve_batch(G(), np.zeros(10 * 3, np.float32), np.zeros(10 * 2, np.float32), 3, 1e-6)
+
+
+def test_binding_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors of fj_opts / fj_stats have the header's field names, order, offsets and
+    sizes (a C program compiled against include/fj.h prints them)."""
+    import subprocess
+    import paper_2507_14864_b200 as fj
+    fields = {"fj_opts": [n for n, _ in fj._Opts._fields_],
+              "fj_stats": [n for n, _ in fj._Stats._fields_]}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "fj.h"', 'int main(void) {']
+    for st, names in fields.items():
+        lines.append(f'  printf("{st} %zu\\n", sizeof({st}));')
+        for n in names:
+            lines.append(f'  printf("{st}.{n} %zu\\n", offsetof({st}, {n}));')
+    lines += ['  return 0;', '}']
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                 check=True).stdout.splitlines())
+    for st, cls in (("fj_opts", fj._Opts), ("fj_stats", fj._Stats)):
+        assert int(out[st]) == ctypes.sizeof(cls), st
+        for n, _ in cls._fields_:
+            assert int(out[f"{st}.{n}"]) == getattr(cls, n).offset, (st, n)
+    o = fj._Opts()
+    fj.lib().fj_opts_default(ctypes.byref(o))
+    assert o.shadow == -1
