@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define FJ_ABI_VERSION 3
+#define FJ_ABI_VERSION 4
 
 typedef struct fj_graph *fj_graph_t;
 
@@ -102,6 +102,12 @@ typedef struct {
                         certificate decides as always; 0 = fp64 sweeps only; < 0
                         (default) → 1 on hub-dominated graphs (rows above 256 arcs hold
                         over half the arcs), else 0                                     */
+  int slices;        /* ASYNC/COLORED: how a sweep walks rows of ≤ 256 arcs.  Nonzero
+                        (default −1): row slices — 32 rows per warp, one lane per row,
+                        arcs stored slice by slice (sliced ELL), sums in registers;
+                        0: warp tiles — a warp per ≤ 256 contiguous CSR arcs, products
+                        staged in shared memory.  Same relaxations either way (the order
+                        of a row's sum differs in rounding only)                        */
 } fj_opts;
 
 typedef struct {

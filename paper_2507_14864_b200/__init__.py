@@ -43,7 +43,8 @@ class _Opts(ctypes.Structure):
                 ("certify", ctypes.c_int), ("zprime_out", ctypes.c_void_p),
                 ("z_init", ctypes.c_void_p), ("tail_frac", ctypes.c_double),
                 ("coloring", ctypes.c_int), ("push_compact", ctypes.c_int),
-                ("push_sparse_div", ctypes.c_int), ("shadow", ctypes.c_int)]
+                ("push_sparse_div", ctypes.c_int), ("shadow", ctypes.c_int),
+                ("slices", ctypes.c_int)]
 
 
 class _Stats(ctypes.Structure):
@@ -237,9 +238,10 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
           certify: bool = True, zprime_out=None, raise_on_numeric: bool = True,
           z_init=None, tail_frac: float = -1.0, coloring: str = "spec",
           push_compact: bool = False, push_sparse_div: int = 8,
-          shadow: int = -1) -> SolveStats:
+          shadow: int = -1, slices: int = -1) -> SolveStats:
     """fj_solve_ex: writes z into ``z_out`` (float32[n]); returns the stats.
     ``shadow``: fj_opts.shadow (1 = shadow sweeps, 0 = fp64 only, −1 = library default).
+    ``slices``: fj_opts.slices (nonzero = short rows as row slices, 0 = as warp tiles).
     ``z_init`` (float64[n], optional): warm start / resume from an earlier z.
     Schedule options (fj_opts): ``tail_frac`` (COLORED tail merge, R23; 0 =
     exact multicolor SOR), ``coloring`` ("spec" or "jp"), ``push_compact`` /
@@ -254,6 +256,7 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
     o.tail_frac, o.coloring = float(tail_frac), {"spec": 0, "jp": 1}[coloring]
     o.push_compact, o.push_sparse_div = int(bool(push_compact)), int(push_sparse_div)
     o.shadow = int(shadow)
+    o.slices = int(slices)
     zp = _ptr(zprime_out)
     o.zprime_out = zp.value if zp is not None else None
     _dtype_ok(z_init, "z_init", "float64", g.n)

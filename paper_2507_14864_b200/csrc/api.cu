@@ -33,7 +33,8 @@ bool is_device_ptr(const void *p) {
 void Layout::release(cudaStream_t st) {
   for (void *q : {(void *)perm, (void *)iperm, (void *)rp, (void *)col, (void *)w, (void *)d1,
                   (void *)tasks, (void *)wtasks, (void *)d_phase_begin, (void *)d_wphase_begin,
-                  (void *)d_crow, (void *)rtasks, (void *)d_rphase_begin, (void *)tail_beta})
+                  (void *)d_crow, (void *)rtasks, (void *)d_rphase_begin, (void *)tail_beta,
+                  (void *)scol, (void *)sw, (void *)stasks, (void *)d_sphase_begin})
     if (q) cudaFreeAsync(q, st);
   perm = iperm = nullptr;
   rp = nullptr;
@@ -51,6 +52,13 @@ void Layout::release(cudaStream_t st) {
   d_rphase_begin = nullptr;
   nrtasks = 0;
   rphase_begin.clear();
+  scol = nullptr;
+  sw = nullptr;
+  stasks = nullptr;
+  d_sphase_begin = nullptr;
+  nslots = 0;
+  nstasks = 0;
+  sphase_begin.clear();
   ntasks = nwtasks = 0;
   ncolors = 0;
   phase_begin.clear();
@@ -82,6 +90,7 @@ void fj_opts_default(fj_opts *o) {
   o->push_compact = 0;
   o->push_sparse_div = 8;
   o->shadow = -1;
+  o->slices = -1;
 }
 
 fj_status fj_graph_get_info(fj_graph_t g, fj_graph_info *info) {

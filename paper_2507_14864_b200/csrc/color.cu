@@ -396,7 +396,7 @@ fj_status build_coloring(fj_graph *g, const fj_opts *o) {
     g->ncolors = nc;
     g->colors = cs;
     FJ_TRY(merge_tail_colors(g, frac));
-    fj_status s = build_layout_from_out(g, ort, ocol, ow, g->colors, g->ncolors, &g->color_layout);
+    fj_status s = build_layout_from_out(g, ort, ocol, ow, g->colors, g->ncolors, &g->color_layout, false, true);
     if (s == FJ_OK) s = tail_bounds(g, &g->color_layout);
     FJ_CUDA(cudaStreamSynchronize(st));
     return s;
@@ -440,7 +440,7 @@ fj_status build_coloring(fj_graph *g, const fj_opts *o) {
   g->ncolors = hmax + 1;
   g->colors = c0;
   FJ_TRY(merge_tail_colors(g, frac));
-  fj_status s = build_layout_from_out(g, ort, ocol, ow, g->colors, g->ncolors, &g->color_layout);
+  fj_status s = build_layout_from_out(g, ort, ocol, ow, g->colors, g->ncolors, &g->color_layout, false, true);
   if (s == FJ_OK) s = tail_bounds(g, &g->color_layout);
   FJ_CUDA(cudaStreamSynchronize(st));
   return s;

@@ -68,7 +68,8 @@ __device__ __forceinline__ int chunk_row_of(int nr, int64_t my_rp, int64_t k) {
 //                                    combined by the last-arriving warp
 enum TaskKind : int32_t {
   kG1 = 0, kG2 = 1, kG4 = 2, kG8 = 3, kG16 = 4, kG32 = 5,  // CTA tile, G = 1 << kind
-  kWarp = 6                                                   // warp unit
+  kWarp = 6,                                                  // warp unit
+  kSlice = 7                                                  // row slice (sweep list only)
 };
 
 // One unit of sweep work.  Tile (kind 0..5): rows [a, b) with
@@ -76,6 +77,9 @@ enum TaskKind : int32_t {
 // Warp unit (kind & 0xff == kWarp): row a, piece b of npieces = kind >> 8;
 // slot = first partial slot of the row (also its arrival counter index).
 // [a0, a1) is the unit's arc range in the layout CSR.
+// Row slice (kind kSlice, Layout::stasks only): rows [a, b), b − a ≤ 32, one lane per row;
+// slot = the slice's width Wd (its longest row); [a0, a1) = its 32·Wd slots in
+// Layout::scol / sw, arc t of row a + l at a0 + 32 t + l (padding: column n, weight 0).
 struct alignas(16) Task {
   int32_t a, b, kind, slot;
   int64_t a0, a1;
@@ -103,6 +107,16 @@ struct Layout {
   int nrtasks = 0;
   std::vector<int> rphase_begin;
   int *d_rphase_begin = nullptr;
+  // Row slices (the single-RHS sweeps' short rows): the arcs of rows ≤ kWarpTileArcs in
+  // slice order (sliced ELL: 32 rows per slice, one lane per row, coalesced column-major
+  // slots), and the sweep list that walks them: warp units, then slices
+  int32_t *scol = nullptr;        // [nslots]
+  float *sw = nullptr;            // [nslots] or null
+  int64_t nslots = 0;
+  Task *stasks = nullptr;
+  int nstasks = 0;
+  std::vector<int> sphase_begin;
+  int *d_sphase_begin = nullptr;
   std::vector<int> phase_begin;   // host, ncolors + 1 entries (tile tasks)
   std::vector<int> wphase_begin;  // host, ncolors + 1 entries (warp units)
   int *d_phase_begin = nullptr;   // device copies
@@ -187,7 +201,8 @@ fj_status transpose_in_csr(fj_graph *g, Workspace &ws, int64_t **ort, int32_t **
 // layout.cu: sweep layout from the pull CSR (original ids)
 fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *ocol,
                                 const float *ow, const int32_t *color /* nullable */,
-                                int ncolors, Layout *L, bool need_d1 = false);
+                                int ncolors, Layout *L, bool need_d1 = false,
+                                bool slices = false);
 // color.cu
 fj_status build_coloring(fj_graph *g, const fj_opts *o);  // (re)builds if o asks for other options
 // prims.cu: hand-written primitives of the graph build and the shift

@@ -570,7 +570,7 @@ static fj_status create_impl(int64_t n, int64_t nnz, const int64_t *rp_in, const
   }
 
   // 7. sweep layout (1 color)
-  fj_status s = build_layout_from_out(g, ort, ocol, ow, nullptr, 1, &g->async_layout);
+  fj_status s = build_layout_from_out(g, ort, ocol, ow, nullptr, 1, &g->async_layout, false, true);
   if (s != FJ_OK) return s;
   FJ_CUDA(cudaStreamSynchronize(st));
   FJ_CUDA(cudaGetLastError());

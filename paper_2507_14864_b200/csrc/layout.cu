@@ -36,8 +36,14 @@ static unsigned gridn(int64_t work) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 1 << 30));
 }
 
-// group of every row (color, length class descending; empty rows last) as the
-// sort key, the row id as the payload: a stable sort by group keeps ids ascending
+// group of every row (color, length class descending; empty rows last) and, below it,
+// the row's length descending inside a short-row class (so that the 32 rows of a row
+// slice have the same length but at ≤ 256 boundaries per group) as the sort key, the row
+// id as the payload: a stable sort keeps ids ascending among equal keys
+constexpr int kSubBits = 8;
+__host__ __device__ static inline int class_lmax(int cls) {
+  return cls == 5 ? (kWarpTileArcs > 64 ? kWarpTileArcs : 128) : (4 << cls);
+}
 __global__ void k_layout_keys(int64_t n, const int64_t *__restrict__ ort,
                               const int32_t *__restrict__ color, int ncolors,
                               uint32_t *__restrict__ keys, uint32_t *__restrict__ ids,
@@ -52,7 +58,12 @@ __global__ void k_layout_keys(int64_t n, const int64_t *__restrict__ ort,
       int c = color ? color[u] : 0;
       grp = (uint64_t)c * kClasses + (uint64_t)(kClasses - 1 - row_class(L));
     }
-    keys[u] = (uint32_t)grp;
+    uint32_t sub = 0;
+    if (L > 0) {
+      const int cls = row_class(L);
+      if (cls <= 5) sub = (uint32_t)min((int64_t)255, (int64_t)class_lmax(cls) - L);
+    }
+    keys[u] = ((uint32_t)grp << kSubBits) | sub;
     ids[u] = (uint32_t)u;
   }
   // warp-aggregated histogram: one atomic per distinct group in the warp
@@ -233,9 +244,60 @@ __global__ void k_gather_tasks(int64_t n, const int32_t *__restrict__ idx, const
   if (i < n) dst[i] = src[idx[i]];
 }
 
+// ---- row slices (sliced ELL for the single-RHS sweeps' short rows) ----
+// slots of every item of the slice sweep list: 32 · (longest row) for a slice, 0 for a unit
+__global__ void k_slice_slots(int ntasks, const Task *__restrict__ tasks,
+                              const int64_t *__restrict__ rp, int64_t *__restrict__ slots) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > ntasks) return;
+  int64_t v = 0;
+  if (i < ntasks) {
+    const Task t = tasks[i];
+    if ((t.kind & 0xff) == kSlice) {
+      int64_t mx = 0;
+      for (int r = t.a; r < t.b; r++) mx = max(mx, rp[r + 1] - rp[r]);
+      v = 32 * mx;
+    }
+  }
+  slots[i] = v;
+}
+// a warp per slice: slot 32 t + l = arc t of row a + l, or the padding (column n — the
+// zero entry after ẑ' — and weight 0); the task gets its slot range and width
+__global__ void k_slice_fill(int ntasks, Task *__restrict__ tasks, const int64_t *__restrict__ off,
+                             const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                             const float *__restrict__ w, int32_t npad,
+                             int32_t *__restrict__ scol, float *__restrict__ sw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < ntasks; i += nwarps) {
+    Task t = tasks[i];
+    if ((t.kind & 0xff) != kSlice) continue;
+    const int64_t o0 = off[i], o1 = off[i + 1];
+    const int wd = (int)((o1 - o0) >> 5);
+    const int row = t.a + lane;
+    int64_t rb = 0;
+    int len = 0;
+    if (row < t.b) {
+      rb = rp[row];
+      len = (int)(rp[row + 1] - rb);
+    }
+    for (int q = 0; q < wd; q++) {
+      const bool ok = q < len;
+      scol[o0 + 32 * q + lane] = ok ? col[rb + q] : npad;
+      if (sw) sw[o0 + 32 * q + lane] = ok ? w[rb + q] : 0.0f;
+    }
+    if (lane == 0) {
+      t.a0 = o0;
+      t.a1 = o1;
+      t.slot = wd;
+      tasks[i] = t;
+    }
+  }
+}
+
 fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *ocol,
                                 const float *ow, const int32_t *color, int ncolors, Layout *L,
-                                bool need_d1) {
+                                bool need_d1, bool slices) {
   cudaStream_t st = g->stream;
   const int64_t n = g->n, m = g->m;
 #ifdef FJ_DIAG
@@ -278,7 +340,11 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
 
   int gbits = 1;
   while ((1 << gbits) <= ngroups) gbits++;
-  FJ_TRY((radix_sort_pairs<uint32_t, uint32_t>(k0, k1, id0, id1, n, gbits, ws)));  // prims.cu
+  if (gbits + kSubBits > 32) {
+    set_error("layout: %d colors exceed the sort key", ncolors);
+    return FJ_ERR_INVALID;
+  }
+  FJ_TRY((radix_sort_pairs<uint32_t, uint32_t>(k0, k1, id0, id1, n, gbits + kSubBits, ws)));  // prims.cu
   FJ_CUDA(cudaMallocAsync(&L->perm, sizeof(int32_t) * n, st));
   FJ_CUDA(cudaMallocAsync(&L->iperm, sizeof(int32_t) * n, st));
   FJ_CUDA(cudaMallocAsync(&L->rp, sizeof(int64_t) * (n + 2), st));
@@ -364,17 +430,20 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
   L->phase_begin.assign(ncolors + 1, 0);
   L->wphase_begin.assign(ncolors + 1, 0);
   L->rphase_begin.assign(ncolors + 1, 0);
-  std::vector<TileGroup> ctag, rtag;  // CTA tiles, warp tiles
+  L->sphase_begin.assign(ncolors + 1, 0);
+  std::vector<TileGroup> ctag, rtag, stag;  // CTA tiles, warp tiles, row slices
   std::vector<std::pair<int64_t, int64_t>> unit_copy;  // per color: (src wtask begin, count)
-  int64_t nt = 0, nrt = 0;
+  int64_t nt = 0, nrt = 0, nst = 0;
   for (int c = 0; c < ncolors; c++) {
     L->phase_begin[c] = (int)nt;
     L->rphase_begin[c] = (int)nrt;
+    L->sphase_begin[c] = (int)nst;
     const int q6 = c * kClasses + 0, q5 = c * kClasses + 2;  // cd 0,1 = classes 7,6
     const int64_t u0 = hscan[q6], u1 = hscan[q5];
     L->wphase_begin[c] = (int)u0;
     unit_copy.push_back({u0, u1 - u0});
     nrt += u1 - u0;
+    nst += u1 - u0;
     L->warp_unit_arcs += hrp[q5] - hrp[q6];
     for (int cd = 2; cd < kClasses; cd++) {
       const int q = c * kClasses + cd, cls = kClasses - 1 - cd;
@@ -384,14 +453,20 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
       const int64_t cnt = (r1 - r0 + per - 1) / per, wcnt = (r1 - r0 + wper - 1) / wper;
       ctag.push_back(TileGroup{nt, cnt, (int32_t)r0, (int32_t)r1, (int32_t)per, cls});
       rtag.push_back(TileGroup{nrt, wcnt, (int32_t)r0, (int32_t)r1, (int32_t)wper, cls});
+      const int64_t scnt = (r1 - r0 + 31) / 32;
+      stag.push_back(TileGroup{nst, scnt, (int32_t)r0, (int32_t)r1, 32, kSlice});
       nt += cnt;
       nrt += wcnt;
+      nst += scnt;
     }
   }
   const int64_t nwt = hscan[ngroups - 1];  // all warp units precede the empty rows
   L->phase_begin[ncolors] = (int)nt;
   L->wphase_begin[ncolors] = (int)nwt;
   L->rphase_begin[ncolors] = (int)nrt;
+  L->sphase_begin[ncolors] = (int)nst;
+  if (!slices) nst = 0;
+  L->nstasks = (int)nst;
   L->ntasks = (int)nt;
   L->nwtasks = (int)nwt;
   L->nrtasks = (int)nrt;
@@ -405,8 +480,17 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     k_fill_units<<<gridn(n), kBlock, 0, st>>>(n, scan, L->wtasks);
   }
   TileGroup *dg = nullptr;
-  const size_t ngd = ctag.size() + rtag.size();
+  const size_t ngd = ctag.size() + rtag.size() + stag.size();
   FJ_CUDA(ws.alloc(&dg, std::max<size_t>(1, ngd)));
+  if (nst > 0) {
+    FJ_CUDA(cudaMallocAsync(&L->stasks, sizeof(Task) * nst, st));
+    if (!stag.empty()) {
+      TileGroup *dsg = dg + ctag.size() + rtag.size();
+      FJ_CUDA(cudaMemcpyAsync(dsg, stag.data(), sizeof(TileGroup) * stag.size(), cudaMemcpyHostToDevice, st));
+      fj::count_launch();
+      k_fill_tiles<<<gridn(nst), kBlock, 0, st>>>((int)stag.size(), dsg, nst, L->stasks);
+    }
+  }
   if (!ctag.empty())
     FJ_CUDA(cudaMemcpyAsync(dg, ctag.data(), sizeof(TileGroup) * ctag.size(), cudaMemcpyHostToDevice, st));
   if (!rtag.empty())
@@ -421,24 +505,28 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     k_fill_tiles<<<gridn(nrt), kBlock, 0, st>>>((int)rtag.size(), dg + ctag.size(), nrt, L->rtasks);
   }
   for (int c = 0; c < ncolors; c++)  // warp units of color c head its sweep list
-    if (unit_copy[c].second > 0)
+    if (unit_copy[c].second > 0) {
       FJ_CUDA(cudaMemcpyAsync(L->rtasks + L->rphase_begin[c], L->wtasks + unit_copy[c].first,
                               sizeof(Task) * unit_copy[c].second, cudaMemcpyDeviceToDevice, st));
-  for (Task *lst : {L->tasks, L->wtasks, L->rtasks}) {
-    const int64_t cnt = lst == L->tasks ? nt : lst == L->wtasks ? nwt : nrt;
-    if (cnt > 0) {
+      if (nst > 0)
+        FJ_CUDA(cudaMemcpyAsync(L->stasks + L->sphase_begin[c], L->wtasks + unit_copy[c].first,
+                                sizeof(Task) * unit_copy[c].second, cudaMemcpyDeviceToDevice, st));
+    }
+  for (Task *lst : {L->tasks, L->wtasks, L->rtasks, L->stasks}) {
+    const int64_t cnt = lst == L->tasks ? nt : lst == L->wtasks ? nwt : lst == L->rtasks ? nrt : nst;
+    if (lst && cnt > 0) {
       fj::count_launch();
       k_task_arcs<<<gridn(cnt), kBlock, 0, st>>>((int)cnt, L->rp, piece, lst);
     }
   }
-  // Interleave warp units and warp tiles in the one-phase sweep list (Bresenham
+  // Interleave warp units and short-row items in the one-phase sweep lists (Bresenham
   // on the counts) so every SM works on a mix of both at any time.  Measured:
   // C3 (Chung–Lu, few hub rows) 0.477 → 0.450 ms per sweep; C4 (R-MAT-24, 65 %
   // of the arcs in hub rows) 1.386 → 1.40, so only graphs whose warp units hold
   // under half the arcs get it.
   const bool mix = 2 * L->warp_unit_arcs < m;
-  if (ncolors == 1 && mix && nrt > 0) {
-    const int64_t U = L->wphase_begin[1] - L->wphase_begin[0], N = nrt, T = N - U;
+  auto interleave = [&](Task *list, int64_t N) -> fj_status {
+    const int64_t U = L->wphase_begin[1] - L->wphase_begin[0], T = N - U;
     std::vector<int32_t> hp(N);
     int64_t iu = 0, itl = 0;
     for (int64_t i = 0; i < N; i++) {
@@ -451,9 +539,33 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     FJ_CUDA(ws.alloc(&tmpt, (size_t)N));
     FJ_CUDA(cudaMemcpyAsync(dp, hp.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
     fj::count_launch();
-    k_gather_tasks<<<gridn(N), kBlock, 0, st>>>(N, dp, L->rtasks, tmpt);
-    FJ_CUDA(cudaMemcpyAsync(L->rtasks, tmpt, sizeof(Task) * N, cudaMemcpyDeviceToDevice, st));
+    k_gather_tasks<<<gridn(N), kBlock, 0, st>>>(N, dp, list, tmpt);
+    FJ_CUDA(cudaMemcpyAsync(list, tmpt, sizeof(Task) * N, cudaMemcpyDeviceToDevice, st));
     FJ_CUDA(cudaStreamSynchronize(st));  // hp is stack-owned
+    return FJ_OK;
+  };
+  if (ncolors == 1 && mix && nrt > 0) FJ_TRY(interleave(L->rtasks, nrt));
+  if (ncolors == 1 && mix && nst > 0) FJ_TRY(interleave(L->stasks, nst));
+  // row slices: slots per item, scan, fill (the list order is final by now)
+  if (nst > 0) {
+    int64_t *slots = nullptr, *soff = nullptr;
+    FJ_CUDA(ws.alloc(&slots, (size_t)nst + 1));
+    FJ_CUDA(ws.alloc(&soff, (size_t)nst + 1));
+    fj::count_launch();
+    k_slice_slots<<<gridn(nst + 1), kBlock, 0, st>>>((int)nst, L->stasks, L->rp, slots);
+    FJ_TRY(exclusive_scan_i64(slots, soff, nst + 1, ws));
+    int64_t total = 0;
+    FJ_CUDA(cudaMemcpyAsync(&total, soff + nst, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FJ_CUDA(cudaStreamSynchronize(st));
+    L->nslots = total;
+    FJ_CUDA(cudaMallocAsync(&L->scol, sizeof(int32_t) * std::max<int64_t>(1, total), st));
+    if (ow) FJ_CUDA(cudaMallocAsync(&L->sw, sizeof(float) * std::max<int64_t>(1, total), st));
+    fj::count_launch();
+    k_slice_fill<<<g->num_sms * 8, kBlock, 0, st>>>((int)nst, L->stasks, soff, L->rp, L->col, L->w,
+                                                    (int32_t)n, L->scol, L->sw);
+    FJ_CUDA(cudaMallocAsync(&L->d_sphase_begin, sizeof(int) * (ncolors + 1), st));
+    FJ_CUDA(cudaMemcpyAsync(L->d_sphase_begin, L->sphase_begin.data(), sizeof(int) * (ncolors + 1),
+                            cudaMemcpyHostToDevice, st));
   }
   FJ_CUDA(cudaStreamSynchronize(st));  // host vectors above are stack-owned
   mark("task lists");

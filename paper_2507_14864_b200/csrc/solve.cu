@@ -34,9 +34,19 @@ namespace fj {
 // of one length class).  Warps take the items round-robin, the next item's
 // descriptor prefetched; the items are balanced by construction, so no claim
 // atomics sit on the hot loop.  One grid barrier ends each color phase.
-template <bool W>
+// SL: the short rows run as row slices (Layout::stasks, one lane per row, no shared
+// memory) instead of warp tiles (Layout::rtasks, products staged in shared memory).
+template <bool W, int SH, bool SL>
+__device__ __forceinline__ void sweep_item(const KP &p, const Scalars &S, const Task &cur, TAcc &t,
+                                           double *wprod) {
+  if ((cur.kind & 0xff) == kWarp) do_warp<RELAX, W, SH>(p, S, cur, t);
+  else if constexpr (SL) relax_slice<W, SH>(p, S, cur, t);
+  else relax_warp_tile<W, SH>(p, S, cur, t, wprod);
+}
+
+template <bool W, bool SL>
 __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
-  extern __shared__ double s_prod[];  // per warp: the products of its warp tile
+  extern __shared__ double s_prod[];  // per warp: the products of its warp tile (!SL)
   __shared__ unsigned long long s_dec[3];
   // sharded solve: sweeps queued after the global stopping sweep do nothing
   if (p.stop && __ldcg(p.stop) != 0ull) return;
@@ -61,9 +71,11 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
   for (int sw = 0; sw < max_sweeps; ++sw) {
     for (int k = 0; k < p.ncolors; ++k, ++phase) {
       const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
-      const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
+      const Task *__restrict__ list = SL ? p.stasks : p.rtasks;
+      const int *pb = SL ? p.sphase_begin : p.rphase_begin;
+      const int r0 = pb[k], nr = pb[k + 1] - r0;
       const int stride = gridDim.x * (kBlock / 32);
-      double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
+      double *wprod = SL ? nullptr : s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
       // the first items round-robin (the Gauss–Seidel order of the list), the
       // last tail_pct percent claimed one by one, so no warp idles at the end
       const int ns = nr - (int)((long long)nr * p.tail_pct / 100);
@@ -71,13 +83,12 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
       if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[(phase + 2) % 3] = 0u;
       int wi = warp_id;
       Task nxt;
-      if (wi < ns) nxt = p.rtasks[r0 + wi];
+      if (wi < ns) nxt = list[r0 + wi];
       while (wi < ns) {
         const Task cur = nxt;
         const int wn = wi + stride;
-        if (wn < ns) nxt = p.rtasks[r0 + wn];
-        if ((cur.kind & 0xff) == kWarp) do_warp<RELAX, W>(p, S, cur, t);
-        else relax_warp_tile<W>(p, S, cur, t, wprod);
+        if (wn < ns) nxt = list[r0 + wn];
+        sweep_item<W, 0, SL>(p, S, cur, t, wprod);
         wi = wn;
       }
       for (; ns < nr;) {
@@ -85,9 +96,8 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
         if ((threadIdx.x & 31) == 0) c = ns + (int)atomicAdd(claim, 1u);
         c = __shfl_sync(0xffffffffu, c, 0);
         if (c >= nr) break;
-        const Task cur = p.rtasks[r0 + c];
-        if ((cur.kind & 0xff) == kWarp) do_warp<RELAX, W>(p, S, cur, t);
-        else relax_warp_tile<W>(p, S, cur, t, wprod);
+        const Task cur = list[r0 + c];
+        sweep_item<W, 0, SL>(p, S, cur, t, wprod);
       }
       if (k + 1 < p.ncolors) grid_sync(p.bar);
     }
@@ -113,7 +123,7 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
 // relaxing the shadow's rounding noise); the fp64 sweeps of k_sweep then run from the
 // same ẑ' until nothing relaxes (Lemma 3: ẑ alone determines r), and the
 // compensated certificate decides as always.
-template <bool W>
+template <bool W, bool SL>
 __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_sh(KP p) {
   extern __shared__ double s_prod[];
   __shared__ unsigned long long s_dec[3];
@@ -128,21 +138,22 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_sh(KP p) {
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
     for (int k = 0; k < p.ncolors; ++k, ++phase) {
       const int warp_id = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
-      const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
+      const Task *__restrict__ list = SL ? p.stasks : p.rtasks;
+      const int *pb = SL ? p.sphase_begin : p.rphase_begin;
+      const int r0 = pb[k], nr = pb[k + 1] - r0;
       const int stride = gridDim.x * (kBlock / 32);
-      double *wprod = s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
+      double *wprod = SL ? nullptr : s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
       const int ns = nr - (int)((long long)nr * p.tail_pct / 100);
       unsigned *claim = p.ctr + (phase % 3);
       if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[(phase + 2) % 3] = 0u;
       int wi = warp_id;
       Task nxt;
-      if (wi < ns) nxt = p.rtasks[r0 + wi];
+      if (wi < ns) nxt = list[r0 + wi];
       while (wi < ns) {
         const Task cur = nxt;
         const int wn = wi + stride;
-        if (wn < ns) nxt = p.rtasks[r0 + wn];
-        if ((cur.kind & 0xff) == kWarp) do_warp<RELAX, W, 1>(p, S, cur, t);
-        else relax_warp_tile<W, 1>(p, S, cur, t, wprod);
+        if (wn < ns) nxt = list[r0 + wn];
+        sweep_item<W, 1, SL>(p, S, cur, t, wprod);
         wi = wn;
       }
       for (; ns < nr;) {
@@ -150,9 +161,8 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_sh(KP p) {
         if ((threadIdx.x & 31) == 0) c = ns + (int)atomicAdd(claim, 1u);
         c = __shfl_sync(0xffffffffu, c, 0);
         if (c >= nr) break;
-        const Task cur = p.rtasks[r0 + c];
-        if ((cur.kind & 0xff) == kWarp) do_warp<RELAX, W, 1>(p, S, cur, t);
-        else relax_warp_tile<W, 1>(p, S, cur, t, wprod);
+        const Task cur = list[r0 + c];
+        sweep_item<W, 1, SL>(p, S, cur, t, wprod);
       }
       if (k + 1 < p.ncolors) grid_sync(p.bar);
     }
@@ -216,7 +226,7 @@ __global__ void k_meas_nodes2(int64_t n, const float *__restrict__ z, const floa
 
 // the one-sweep-per-launch entry of the sharded solve (shard.cu)
 const void *sweep_kernel(bool weighted) {
-  return weighted ? (const void *)k_sweep<true> : (const void *)k_sweep<false>;
+  return weighted ? (const void *)k_sweep<true, false> : (const void *)k_sweep<false, false>;
 }
 size_t sweep_kernel_smem() { return (kBlock / 32) * kWarpTileArcs * sizeof(double); }
 
@@ -271,9 +281,14 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   SweepCounters *cnt = nullptr;
   unsigned long long *outv = nullptr, *certbits = nullptr;
   unsigned *zs = nullptr;
-  if (use_shadow) FJ_CUDA(ws.alloc(&zs, n));
+  // ẑ' and its shadow carry one more entry, 0: the column of the row slices' padding
+  if (use_shadow) {
+    FJ_CUDA(ws.alloc(&zs, n + 1));
+    FJ_CUDA(cudaMemsetAsync(zs + n, 0, sizeof(unsigned), st));
+  }
   FJ_CUDA(ws.alloc(&s_l, n));
-  FJ_CUDA(ws.alloc(&z, n));
+  FJ_CUDA(ws.alloc(&z, n + 1));
+  FJ_CUDA(cudaMemsetAsync(z + n, 0, sizeof(double), st));
   FJ_CUDA(ws.alloc(&smin, 2));
   smax = smin + 1;
   FJ_CUDA(ws.alloc(&S, 1));
@@ -325,8 +340,12 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   p.out = outv;
   p.cert_max = certbits;
 
-  const void *fn = W ? (const void *)k_sweep<true> : (const void *)k_sweep<false>;
-  const size_t sweep_smem = sweep_kernel_smem();
+  // short rows as row slices (fj_opts.slices; the layout carries them unless it is a
+  // shard's) or as warp tiles
+  const bool SL = L.scol != nullptr && o->slices != 0;
+  const void *fn = SL ? (W ? (const void *)k_sweep<true, true> : (const void *)k_sweep<false, true>)
+                      : (W ? (const void *)k_sweep<true, false> : (const void *)k_sweep<false, false>);
+  const size_t sweep_smem = SL ? 0 : sweep_kernel_smem();
   FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem));
   // Shared-memory carveout: the tile staging needs ≈ 68 KB per SM, for which
   // the driver's default picks the 132 KB configuration (124 KB of L1).  On
@@ -338,7 +357,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
 #ifdef FJ_CARVE
   const int carve = FJ_CARVE;  // diagnostic build: forced preference (percent)
 #else
-  const int carve = 2 * L.warp_unit_arcs > L.m ? 31 : -1;
+  const int carve = SL ? 0 : (2 * L.warp_unit_arcs > L.m ? 31 : -1);
 #endif
   // Hub-dominated layouts also claim the last 15 % of each phase's work list
   // dynamically (C4 1.358 → 1.315 ms per sweep, C2 and C3 within ±1 %, C5 +3 %:
@@ -349,7 +368,9 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
                                carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault));
   const int grid = persistent_grid(fn, g->num_sms, sweep_smem);
   // shadow launch: the fp64 kernel's shape (same staging, carveout and grid)
-  const void *shfn = W ? (const void *)k_sweep_sh<true> : (const void *)k_sweep_sh<false>;
+  const void *shfn =
+      SL ? (W ? (const void *)k_sweep_sh<true, true> : (const void *)k_sweep_sh<false, true>)
+         : (W ? (const void *)k_sweep_sh<true, false> : (const void *)k_sweep_sh<false, false>);
   int sh_grid = 0;
   if (use_shadow) {
     FJ_CUDA(cudaFuncSetAttribute(shfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem));

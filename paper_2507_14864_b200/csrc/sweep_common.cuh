@@ -49,6 +49,11 @@ struct KP {
   const Task *__restrict__ wtasks;
   const Task *__restrict__ rtasks;
   const int *rphase_begin;
+  // row slices (k_sweep / k_sweep_sh with SL): the layout's slice sweep list and slots
+  const Task *__restrict__ stasks;
+  const int *sphase_begin;
+  const int32_t *__restrict__ scol;
+  const float *__restrict__ sw;
   const float *__restrict__ s;  // layout order
   double *z;                    // ẑ' (RELAX/CERT) or z (DIS), layout order
   const Scalars *sc;
@@ -106,6 +111,7 @@ __device__ __forceinline__ float ld_stream(const float *q) {
 // and every color phase read current values.
 // (weak loads: the compiler may batch them; __ldca compiles to a strong load)
 __device__ __forceinline__ double ld_z(const double *q) { return *q; }
+__device__ __forceinline__ unsigned ld_zs(const unsigned *q) { return *q; }
 
 // Shadow ẑ (k_sweep_sh): the gathers read a 32-bit fixed-point copy of ẑ'
 // (4 B per gather, the whole copy resident in L2; SURVEY §8(d) "fp32 shadow",
@@ -377,7 +383,7 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
     } else {
       unsigned zu[U];
 #pragma unroll
-      for (int u = 0; u < U; u++) zu[u] = p.zs[j[u]];
+      for (int u = 0; u < U; u++) zu[u] = ld_zs(p.zs + j[u]);
 #pragma unroll
       for (int u = 0; u < U; u++) zj[u] = sh_dec(zu[u], S.sh_scale, S.sh_off);
     }
@@ -491,7 +497,7 @@ __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, c
   } else {
     unsigned zu[U];
 #pragma unroll
-    for (int u = 0; u < U; u++) zu[u] = p.zs[j[u]];
+    for (int u = 0; u < U; u++) zu[u] = ld_zs(p.zs + j[u]);
 #pragma unroll
     for (int u = 0; u < U; u++) zj[u] = sh_dec(zu[u], S.sh_scale, S.sh_off);
   }
@@ -531,6 +537,80 @@ __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, c
     }
   }
   __syncwarp();  // the slice is reused by this warp's next task
+}
+
+// RELAX on a row slice (sliced ELL, Layout::scol / sw): ≤ 32 short rows, one lane per
+// row.  Slot 32 t + lane holds arc t of the lane's row, so every column / weight load of
+// the warp is one 128-byte line, each lane sums its own row in a register (no staging, no
+// shuffles, no shared memory) and all 32 lanes relax at once.  Rows of a slice have the
+// same length but at class boundaries (the layout sorts short rows by length); shorter
+// rows are padded with (column n, weight 0): ẑ'[n] = 0 and its shadow sit after the last
+// row.  Up to 8 column loads, then 8 gathers, per lane in flight (4 and 2 measured slower).
+// (G lanes per row with a shuffle sum — shorter items, more of them — measured slower:
+// C4 1.11 vs 0.99 ms per sweep, profiles/r02_slices_ab.txt.)
+template <bool W, int SH, int U>
+__device__ __forceinline__ void slice_step(const KP &p, const Scalars &S, const int32_t *cp,
+                                           const float *wp, double &a) {
+  int j[U];
+  float wv[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    j[u] = ld_stream(cp + 32 * u);
+    wv[u] = W ? ld_stream(wp + 32 * u) : 1.0f;
+  }
+  double zj[U];
+  if constexpr (SH == 0) {
+#pragma unroll
+    for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
+  } else {
+    unsigned zu[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) zu[u] = ld_zs(p.zs + j[u]);
+#pragma unroll
+    for (int u = 0; u < U; u++) zj[u] = sh_dec(zu[u], S.sh_scale, S.sh_off);
+  }
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    if (W) a = fma((double)wv[u], zj[u], a);
+    else a += zj[u];
+  }
+}
+
+template <bool W, int SH = 0>
+__device__ __forceinline__ void relax_slice(const KP &p, const Scalars &S, const Task &tk, TAcc &t) {
+  const int lane = threadIdx.x & 31;
+  const int row = tk.a + lane;
+  const bool ok = row < tk.b;
+  int wd = tk.slot;
+  const int32_t *cp = p.scol + tk.a0 + lane;
+  const float *wp = W ? p.sw + tk.a0 + lane : nullptr;
+  float sv = 0.f;
+  double zi = 0.0, d1 = 1.0;
+  int len = 0;
+  if (ok) {
+    sv = __ldg(p.s + row);
+    zi = __ldcg(p.z + row);
+    if (W) d1 = __ldg(p.d1 + row);
+    len = (int)(__ldg(p.rp + row + 1) - __ldg(p.rp + row));
+  }
+  double a = 0.0;
+  for (; wd >= 8; wd -= 8) {
+    slice_step<W, SH, 8>(p, S, cp, wp, a);
+    cp += 256;
+    if (W) wp += 256;
+  }
+  if (wd & 4) {
+    slice_step<W, SH, 4>(p, S, cp, wp, a);
+    cp += 128;
+    if (W) wp += 128;
+  }
+  if (wd & 2) {
+    slice_step<W, SH, 2>(p, S, cp, wp, a);
+    cp += 64;
+    if (W) wp += 64;
+  }
+  if (wd & 1) slice_step<W, SH, 1>(p, S, cp, wp, a);
+  if (ok) relax_row_pre<SH>(p, S, row, len, dd{a, 0.0}, sv, zi, W ? d1 : (double)(len + 1), t);
 }
 
 template <int MODE, bool W>
@@ -766,6 +846,10 @@ static KP make_kp(const fj_graph *g, const Layout &L) {
   p.wtasks = L.wtasks;
   p.rtasks = L.rtasks;
   p.rphase_begin = L.d_rphase_begin;
+  p.stasks = L.stasks;
+  p.sphase_begin = L.d_sphase_begin;
+  p.scol = L.scol;
+  p.sw = L.sw;
   p.phase_begin = L.d_phase_begin;
   p.wphase_begin = L.d_wphase_begin;
   p.ncolors = L.ncolors;
@@ -802,7 +886,7 @@ static fj_status finish_status(const Scalars &hs, fj_stats &stats, const fj_opts
 
 
 // implemented in push.cu / batch.cu / solve.cu
-const void *sweep_kernel(bool weighted);  // k_sweep<W, false> (solve.cu)
+const void *sweep_kernel(bool weighted);  // k_sweep<W, false> (solve.cu): the warp-tile list
 size_t sweep_kernel_smem();
 fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double omega,
                           const fj_opts *o, float *z_out, fj_stats *st_out);

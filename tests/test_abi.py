@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(L, name), name
     assert set(fj.EXPORTS) == set(_declared())
-    assert L.fj_abi_version() == 3
+    assert L.fj_abi_version() == 4
 
 
 def test_library_is_sm100a():
@@ -116,3 +116,4 @@ def test_binding_struct_layouts_match_header(tmp_path):
     o = fj._Opts()
     fj.lib().fj_opts_default(ctypes.byref(o))
     assert o.shadow == -1
+    assert o.slices == -1
