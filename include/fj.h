@@ -102,12 +102,13 @@ typedef struct {
                         certificate decides as always; 0 = fp64 sweeps only; < 0
                         (default) → 1 on hub-dominated graphs (rows above 256 arcs hold
                         over half the arcs), else 0                                     */
-  int slices;        /* ASYNC/COLORED: how a sweep walks rows of ≤ 256 arcs.  Nonzero
-                        (default −1): row slices — 32 rows per warp, one lane per row,
-                        arcs stored slice by slice (sliced ELL), sums in registers;
-                        0: warp tiles — a warp per ≤ 256 contiguous CSR arcs, products
-                        staged in shared memory.  Same relaxations either way (the order
-                        of a row's sum differs in rounding only)                        */
+  int slices;        /* ASYNC/COLORED: how a sweep walks rows of ≤ 256 arcs.  1: row slices
+                        — 32 rows per warp, one lane per row, arcs stored slice by slice
+                        (sliced ELL), sums in registers; 0: warp tiles — a warp per ≤ 256
+                        contiguous CSR arcs, products staged in shared memory; < 0
+                        (default): slices, except on colored layouts that have rows above
+                        32 arcs.  Same relaxations either way (the order of a row's sum
+                        differs in rounding only)                                       */
 } fj_opts;
 
 typedef struct {

@@ -245,21 +245,21 @@ __global__ void k_gather_tasks(int64_t n, const int32_t *__restrict__ idx, const
 }
 
 // ---- row slices (sliced ELL for the single-RHS sweeps' short rows) ----
-// slots of every item of the slice sweep list: 32 · (longest row) for a slice, 0 for a unit
+// slots of every item of the slice sweep list: 32 · (longest row) for a slice, 0 for a
+// unit; a warp per item (slots[ntasks] = 0 closes the scan)
 __global__ void k_slice_slots(int ntasks, const Task *__restrict__ tasks,
                               const int64_t *__restrict__ rp, int64_t *__restrict__ slots) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (i > ntasks) return;
-  int64_t v = 0;
+  int mx = 0;
   if (i < ntasks) {
-    const Task t = tasks[i];
-    if ((t.kind & 0xff) == kSlice) {
-      int64_t mx = 0;
-      for (int r = t.a; r < t.b; r++) mx = max(mx, rp[r + 1] - rp[r]);
-      v = 32 * mx;
-    }
+    const int4 t = *reinterpret_cast<const int4 *>(tasks + i);  // a, b, kind, slot
+    if ((t.z & 0xff) == kSlice && t.x + lane < t.y) mx = (int)(rp[t.x + lane + 1] - rp[t.x + lane]);
   }
-  slots[i] = v;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (lane == 0) slots[i] = 32 * (int64_t)mx;
 }
 // a warp per slice: slot 32 t + l = arc t of row a + l, or the padding (column n — the
 // zero entry after ẑ' — and weight 0); the task gets its slot range and width
@@ -545,14 +545,16 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     return FJ_OK;
   };
   if (ncolors == 1 && mix && nrt > 0) FJ_TRY(interleave(L->rtasks, nrt));
-  if (ncolors == 1 && mix && nst > 0) FJ_TRY(interleave(L->stasks, nst));
+  // (the slice list stays units-first: interleaved it is 18–22 % slower per sweep on
+  // C2 / C3, profiles/r02_slices_variants_ab.txt)
+  mark("task lists (pre-slices)");
   // row slices: slots per item, scan, fill (the list order is final by now)
   if (nst > 0) {
     int64_t *slots = nullptr, *soff = nullptr;
     FJ_CUDA(ws.alloc(&slots, (size_t)nst + 1));
     FJ_CUDA(ws.alloc(&soff, (size_t)nst + 1));
     fj::count_launch();
-    k_slice_slots<<<gridn(nst + 1), kBlock, 0, st>>>((int)nst, L->stasks, L->rp, slots);
+    k_slice_slots<<<gridn(32 * (nst + 1)), kBlock, 0, st>>>((int)nst, L->stasks, L->rp, slots);
     FJ_TRY(exclusive_scan_i64(slots, soff, nst + 1, ws));
     int64_t total = 0;
     FJ_CUDA(cudaMemcpyAsync(&total, soff + nst, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -563,6 +565,7 @@ fj_status build_layout_from_out(fj_graph *g, const int64_t *ort, const int32_t *
     fj::count_launch();
     k_slice_fill<<<g->num_sms * 8, kBlock, 0, st>>>((int)nst, L->stasks, soff, L->rp, L->col, L->w,
                                                     (int32_t)n, L->scol, L->sw);
+    mark("slices: slots+scan+fill");
     FJ_CUDA(cudaMallocAsync(&L->d_sphase_begin, sizeof(int) * (ncolors + 1), st));
     FJ_CUDA(cudaMemcpyAsync(L->d_sphase_begin, L->sphase_begin.data(), sizeof(int) * (ncolors + 1),
                             cudaMemcpyHostToDevice, st));

@@ -341,8 +341,12 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   p.cert_max = certbits;
 
   // short rows as row slices (fj_opts.slices; the layout carries them unless it is a
-  // shard's) or as warp tiles
-  const bool SL = L.scol != nullptr && o->slices != 0;
+  // shard's) or as warp tiles.  Default: slices, except on colored layouts with rows
+  // above 32 arcs — every phase then waits for its deepest slice (a lane walks up to 256
+  // arcs): C3 at ω = 1.6, 12 phases, 0.76 vs 0.63 ms per sweep and 130 vs 109 sweeps
+  // (profiles/r02_slices_variants_ab.txt)
+  const bool SL = L.scol != nullptr &&
+                  (o->slices > 0 || (o->slices < 0 && (L.ncolors == 1 || L.max_len <= 32)));
   const void *fn = SL ? (W ? (const void *)k_sweep<true, true> : (const void *)k_sweep<false, true>)
                       : (W ? (const void *)k_sweep<true, false> : (const void *)k_sweep<false, false>);
   const size_t sweep_smem = SL ? 0 : sweep_kernel_smem();
@@ -362,7 +366,11 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   // Hub-dominated layouts also claim the last 15 % of each phase's work list
   // dynamically (C4 1.358 → 1.315 ms per sweep, C2 and C3 within ±1 %, C5 +3 %:
   // profiles/r02_tailclaim_ab.txt); the rest keeps the static order.
+#ifdef FJ_TAILPCT
+  p.tail_pct = FJ_TAILPCT;
+#else
   p.tail_pct = 2 * L.warp_unit_arcs > L.m ? 15 : 0;
+#endif
   // (a per-function setting: set on every solve, −1 = the driver's default)
   FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault));

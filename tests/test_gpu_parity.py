@@ -941,3 +941,53 @@ def test_shadow_divergence_reported(dev):
     else:
         assert st.status == fj.FJ_ERR_NUMERIC and st.reason in (1, 2)
     g.close()
+
+
+# ------------------------------------------------- row slices / warp tiles (fj_opts.slices)
+# Short rows run as row slices (sliced ELL, one lane per row) or as warp tiles (CSR arcs,
+# shared-memory staging); the default picks per layout.  Both walks are held to the bar of
+# every solve on every tiny graph, with and without shadow gathers, and on a graph whose
+# slices mix lengths, padding and hub pieces.
+@pytest.mark.parametrize("slices", [0, 1])
+@pytest.mark.parametrize("name", sorted(TINY))
+def test_row_walks_async(dev, name, slices):
+    rp, col, w, s, directed = TINY[name]()
+    for shadow in (0, 1):
+        st, _, _ = check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async",
+                                slices=slices, shadow=shadow)
+        assert (st.shadow_sweeps > 0) == (shadow == 1)
+
+
+@pytest.mark.parametrize("slices", [0, 1])
+@pytest.mark.parametrize("name,omega", [("er2000", 1.5), ("chunglu4k", 1.6), ("lattice64", 1.25)])
+def test_row_walks_colored_sor(dev, name, omega, slices):
+    rp, col, w, s, directed = TINY[name]()
+    st, _, _ = check_parity(dev, rp, col, w, s, 1e-6, omega, directed, method="colored",
+                            slices=slices)
+    assert st.colors > 1
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_row_slices_mixed_lengths(dev, weighted):
+    """Every row length from 1 to 300 a few times (slices that straddle a length or class
+    boundary are padded), a ragged last slice per class, rows without arcs, and two hub
+    rows cut into pieces: slices and tiles agree with the oracle and with each other."""
+    rng = np.random.default_rng(77)
+    n = 6000
+    lens = np.concatenate([np.repeat(np.arange(1, 301), 3), [5000, 2500], np.zeros(40, np.int64)])
+    lens = np.concatenate([lens, rng.integers(1, 9, n - len(lens))])
+    rng.shuffle(lens)
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.empty(rp[-1], np.int32)
+    for i in range(n):
+        c = rng.choice(n - 1, int(lens[i]), replace=False)
+        c[c >= i] += 1  # no self-loops
+        col[rp[i]:rp[i + 1]] = np.sort(c)
+    w = rng.uniform(0.05, 1.0, rp[-1]).astype(np.float32) if weighted else None
+    s = fjgen.uniform(n, 78)
+    zs = []
+    for slices in (0, 1):
+        _, z, _ = check_parity(dev, rp, col, w, s, 1e-6, 1.0, True, method="async", slices=slices)
+        zs.append(z)
+    assert rel_err(zs[0], zs[1]) <= 2e-6
