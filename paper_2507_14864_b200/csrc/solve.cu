@@ -44,6 +44,19 @@ __device__ __forceinline__ void sweep_item(const KP &p, const Scalars &S, const 
   else relax_warp_tile<W, SH>(p, S, cur, t, wprod);
 }
 
+// dynamic part of a phase's list: warps claim chunks of kClaimChunk consecutive items in
+// list order (lane 0's atomic; one claim per item costs C5 0.33 ms per sweep — 524 K
+// atomics on one address — chunks of 4 or 8 nothing; 16 clump the work again)
+#ifndef FJ_CHUNK
+#define FJ_CHUNK 4
+#endif
+constexpr int kClaimChunk = FJ_CHUNK;
+__device__ __forceinline__ int claim_chunk(unsigned *claim, int ns) {
+  int c = 0;
+  if ((threadIdx.x & 31) == 0) c = ns + kClaimChunk * (int)atomicAdd(claim, 1u);
+  return __shfl_sync(0xffffffffu, c, 0);
+}
+
 template <bool W, bool SL>
 __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
   extern __shared__ double s_prod[];  // per warp: the products of its warp tile (!SL)
@@ -77,8 +90,11 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
       const int stride = gridDim.x * (kBlock / 32);
       double *wprod = SL ? nullptr : s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
       // the first items round-robin (the Gauss–Seidel order of the list), the
-      // last tail_pct percent claimed one by one, so no warp idles at the end
-      const int ns = nr - (int)((long long)nr * p.tail_pct / 100);
+      // last tail_pct percent claimed in chunks, so no SM idles at the end
+      int ns = nr - (int)((long long)nr * p.tail_pct / 100);
+      // (slice lists: the warp units, the head of the list, always stay round-robin —
+      // a chunk of consecutive hub rows in one warp would serialise them)
+      if (SL) ns = max(ns, min(nr, p.wphase_begin[k + 1] - p.wphase_begin[k]));
       unsigned *claim = p.ctr + (phase % 3);
       if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[(phase + 2) % 3] = 0u;
       int wi = warp_id;
@@ -91,13 +107,31 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
         sweep_item<W, 0, SL>(p, S, cur, t, wprod);
         wi = wn;
       }
-      for (; ns < nr;) {
-        int c = 0;
-        if ((threadIdx.x & 31) == 0) c = ns + (int)atomicAdd(claim, 1u);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        if (c >= nr) break;
-        const Task cur = list[r0 + c];
-        sweep_item<W, 0, SL>(p, S, cur, t, wprod);
+      if constexpr (!SL) {
+        for (; ns < nr;) {  // warp tiles: one claim per item
+          int c = 0;
+          if ((threadIdx.x & 31) == 0) c = ns + (int)atomicAdd(claim, 1u);
+          c = __shfl_sync(0xffffffffu, c, 0);
+          if (c >= nr) break;
+          const Task cur = list[r0 + c];
+          sweep_item<W, 0, SL>(p, S, cur, t, wprod);
+        }
+      } else if (ns < nr) {
+        // (the next descriptor, and at a chunk's end the next claim, are in flight behind
+        // the current item)
+        int c = claim_chunk(claim, ns), e = min(c + kClaimChunk, nr);
+        if (c < nr) nxt = list[r0 + c];
+        while (c < nr) {
+          const Task cur = nxt;
+          int cn = c + 1;
+          if (cn >= e) {
+            cn = claim_chunk(claim, ns);
+            e = min(cn + kClaimChunk, nr);
+          }
+          if (cn < nr) nxt = list[r0 + cn];
+          sweep_item<W, 0, SL>(p, S, cur, t, wprod);
+          c = cn;
+        }
       }
       if (k + 1 < p.ncolors) grid_sync(p.bar);
     }
@@ -143,7 +177,10 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_sh(KP p) {
       const int r0 = pb[k], nr = pb[k + 1] - r0;
       const int stride = gridDim.x * (kBlock / 32);
       double *wprod = SL ? nullptr : s_prod + (threadIdx.x >> 5) * kWarpTileArcs;
-      const int ns = nr - (int)((long long)nr * p.tail_pct / 100);
+      int ns = nr - (int)((long long)nr * p.tail_pct / 100);
+      // (slice lists: the warp units, the head of the list, always stay round-robin —
+      // a chunk of consecutive hub rows in one warp would serialise them)
+      if (SL) ns = max(ns, min(nr, p.wphase_begin[k + 1] - p.wphase_begin[k]));
       unsigned *claim = p.ctr + (phase % 3);
       if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[(phase + 2) % 3] = 0u;
       int wi = warp_id;
@@ -156,13 +193,31 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_sh(KP p) {
         sweep_item<W, 1, SL>(p, S, cur, t, wprod);
         wi = wn;
       }
-      for (; ns < nr;) {
-        int c = 0;
-        if ((threadIdx.x & 31) == 0) c = ns + (int)atomicAdd(claim, 1u);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        if (c >= nr) break;
-        const Task cur = list[r0 + c];
-        sweep_item<W, 1, SL>(p, S, cur, t, wprod);
+      if constexpr (!SL) {
+        for (; ns < nr;) {  // warp tiles: one claim per item
+          int c = 0;
+          if ((threadIdx.x & 31) == 0) c = ns + (int)atomicAdd(claim, 1u);
+          c = __shfl_sync(0xffffffffu, c, 0);
+          if (c >= nr) break;
+          const Task cur = list[r0 + c];
+          sweep_item<W, 1, SL>(p, S, cur, t, wprod);
+        }
+      } else if (ns < nr) {
+        // (the next descriptor, and at a chunk's end the next claim, are in flight behind
+        // the current item)
+        int c = claim_chunk(claim, ns), e = min(c + kClaimChunk, nr);
+        if (c < nr) nxt = list[r0 + c];
+        while (c < nr) {
+          const Task cur = nxt;
+          int cn = c + 1;
+          if (cn >= e) {
+            cn = claim_chunk(claim, ns);
+            e = min(cn + kClaimChunk, nr);
+          }
+          if (cn < nr) nxt = list[r0 + cn];
+          sweep_item<W, 1, SL>(p, S, cur, t, wprod);
+          c = cn;
+        }
       }
       if (k + 1 < p.ncolors) grid_sync(p.bar);
     }
@@ -363,18 +418,25 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
 #else
   const int carve = SL ? 0 : (2 * L.warp_unit_arcs > L.m ? 31 : -1);
 #endif
-  // Hub-dominated layouts also claim the last 15 % of each phase's work list
-  // dynamically (C4 1.358 → 1.315 ms per sweep, C2 and C3 within ±1 %, C5 +3 %:
-  // profiles/r02_tailclaim_ab.txt); the rest keeps the static order.
+  // Dynamic share of each phase's work list.  Warp tiles (equal items): the last 15 % on
+  // hub-dominated layouts (C4 1.358 → 1.315 ms per sweep, C2 and C3 within ±1 %, C5 +3 %:
+  // profiles/r02_tailclaim_ab.txt), else none.  Row slices (items from 32 to 8192 arcs, so
+  // round-robin leaves SMs waiting at the sweep's barrier: 12 % of the warp samples): the
+  // last 50 % of the items, chunks of 4 — C4 0.99 → 0.94 ms per sweep, C3 −8 %, C2 −6 %,
+  // C5 ±0 (profiles/r02_slices_variants_ab.txt) — on one-phase lists of at least 4 items
+  // per warp; short lists and color phases stay round-robin (C1 2.6 vs 1.5 ms, C5 at
+  // ω = 1.25 12.1 vs 11.1 ms with claims)
 #ifdef FJ_TAILPCT
   p.tail_pct = FJ_TAILPCT;
 #else
-  p.tail_pct = 2 * L.warp_unit_arcs > L.m ? 15 : 0;
+  p.tail_pct = SL ? -1 : (2 * L.warp_unit_arcs > L.m ? 15 : 0);  // −1: set below (needs the grid)
 #endif
   // (a per-function setting: set on every solve, −1 = the driver's default)
   FJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault));
   const int grid = persistent_grid(fn, g->num_sms, sweep_smem);
+  if (p.tail_pct < 0)
+    p.tail_pct = (L.ncolors == 1 && L.nstasks >= 4 * grid * (kBlock / 32)) ? 50 : 0;
   // shadow launch: the fp64 kernel's shape (same staging, carveout and grid)
   const void *shfn =
       SL ? (W ? (const void *)k_sweep_sh<true, true> : (const void *)k_sweep_sh<false, true>)
