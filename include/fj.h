@@ -109,6 +109,13 @@ typedef struct {
                         (default): slices, except on colored layouts that have rows above
                         32 arcs.  Same relaxations either way (the order of a row's sum
                         differs in rounding only)                                       */
+  int frontier;      /* ASYNC with row slices: the frontier phase (the paper's queue, Alg. 1
+                        P:216-226, on the thin tail of a solve).  Once a sweep relaxes fewer
+                        than T rows, every row's residual is written once and the push form
+                        runs on the rows above threshold only: pop, scatter a·Δ to the rows
+                        that gather them (fp64 atomics), list the rows that cross their
+                        threshold, until the list is empty.  0 = off; > 0: T; < 0 (default):
+                        T = non-empty rows / 256                                         */
 } fj_opts;
 
 typedef struct {
@@ -129,6 +136,9 @@ typedef struct {
   double cert_ms;        /* device time inside the certificate kernel                  */
   int64_t shadow_sweeps; /* of `sweeps`: those that gathered from the shadow           */
   double shadow_ms;      /* of `sweep_ms`: device time of the shadow sweep launch      */
+  int64_t frontier_rounds; /* pop + scatter rounds of the frontier phase                */
+  int64_t frontier_pushes; /* scatter entries of those rounds (≤ 1024 in-arcs each)     */
+  double frontier_ms;    /* of `sweep_ms`: device time of the frontier launches        */
 } fj_stats;
 
 typedef struct {

@@ -44,7 +44,7 @@ class _Opts(ctypes.Structure):
                 ("z_init", ctypes.c_void_p), ("tail_frac", ctypes.c_double),
                 ("coloring", ctypes.c_int), ("push_compact", ctypes.c_int),
                 ("push_sparse_div", ctypes.c_int), ("shadow", ctypes.c_int),
-                ("slices", ctypes.c_int)]
+                ("slices", ctypes.c_int), ("frontier", ctypes.c_int)]
 
 
 class _Stats(ctypes.Structure):
@@ -56,7 +56,8 @@ class _Stats(ctypes.Structure):
                 ("colors", ctypes.c_int), ("status", ctypes.c_int), ("reason", ctypes.c_int),
                 ("solve_ms", ctypes.c_double), ("sweep_ms", ctypes.c_double),
                 ("cert_ms", ctypes.c_double), ("shadow_sweeps", ctypes.c_int64),
-                ("shadow_ms", ctypes.c_double)]
+                ("shadow_ms", ctypes.c_double), ("frontier_rounds", ctypes.c_int64),
+                ("frontier_pushes", ctypes.c_int64), ("frontier_ms", ctypes.c_double)]
 
 
 class _Info(ctypes.Structure):
@@ -190,6 +191,9 @@ class SolveStats:
     cert_ms: float
     shadow_sweeps: int = 0
     shadow_ms: float = 0.0
+    frontier_rounds: int = 0
+    frontier_pushes: int = 0
+    frontier_ms: float = 0.0
 
 
 class Graph:
@@ -238,10 +242,11 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
           certify: bool = True, zprime_out=None, raise_on_numeric: bool = True,
           z_init=None, tail_frac: float = -1.0, coloring: str = "spec",
           push_compact: bool = False, push_sparse_div: int = 8,
-          shadow: int = -1, slices: int = -1) -> SolveStats:
+          shadow: int = -1, slices: int = -1, frontier: int = -1) -> SolveStats:
     """fj_solve_ex: writes z into ``z_out`` (float32[n]); returns the stats.
     ``shadow``: fj_opts.shadow (1 = shadow sweeps, 0 = fp64 only, −1 = library default).
     ``slices``: fj_opts.slices (nonzero = short rows as row slices, 0 = as warp tiles).
+    ``frontier``: fj_opts.frontier (0 = off, > 0 = thin-sweep threshold in rows, −1 = default).
     ``z_init`` (float64[n], optional): warm start / resume from an earlier z.
     Schedule options (fj_opts): ``tail_frac`` (COLORED tail merge, R23; 0 =
     exact multicolor SOR), ``coloring`` ("spec" or "jp"), ``push_compact`` /
@@ -257,6 +262,7 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
     o.push_compact, o.push_sparse_div = int(bool(push_compact)), int(push_sparse_div)
     o.shadow = int(shadow)
     o.slices = int(slices)
+    o.frontier = int(frontier)
     zp = _ptr(zprime_out)
     o.zprime_out = zp.value if zp is not None else None
     _dtype_ok(z_init, "z_init", "float64", g.n)

@@ -91,6 +91,7 @@ void fj_opts_default(fj_opts *o) {
   o->push_sparse_div = 8;
   o->shadow = -1;
   o->slices = -1;
+  o->frontier = -1;
 }
 
 fj_status fj_graph_get_info(fj_graph_t g, fj_graph_info *info) {

@@ -80,6 +80,10 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
     tot_upd = __ldcg(p.prev + 1);
     tot_eu = __ldcg(p.prev + 2);
     max_sweeps = max(1, max_sweeps - sweeps0);
+    if (p.skip_if_done && __ldcg(p.prev + 3) == 0ull) {  // the launch before converged
+      sweep_result(p.out, sweeps0, tot_upd, tot_eu, 0);
+      return;
+    }
   }
   for (int sw = 0; sw < max_sweeps; ++sw) {
     for (int k = 0; k < p.ncolors; ++k, ++phase) {
@@ -144,6 +148,7 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep(KP p) {
     const bool bad = dec[2] != 0, done = dec[0] == 0;
     if (bad) { reason = 2; break; }
     if (done) { reason = 0; break; }
+    if (dec[0] < p.thin) { reason = 3; break; }  // thin sweep: the frontier phase takes over
   }
   sweep_result(p.out, sweeps0 + sweeps, tot_upd, tot_eu, reason);
 }
@@ -229,9 +234,148 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_sh(KP p) {
     // dec[2]: bit 0 = sentinel or shadow range, bit 1 = some move of ≥ 4 quanta
     const bool bad = (dec[2] & 1) != 0, done = dec[0] == 0 || (dec[2] & 2) == 0;
     if (bad) { reason = 2; break; }
-    if (done) { reason = 0; break; }
+    if (done) { reason = 4; break; }  // 4: the shadow loop is done, fp64 sweeps must follow
+    if (dec[0] < p.thin) { reason = 3; break; }  // thin sweep: the frontier phase takes over
   }
   sweep_result(p.out, sweeps, tot_upd, tot_eu, reason);
+}
+
+// Frontier phase: the paper's queue (Alg. 1, Alg. 3) on the thin tail
+// of a solve.  Late sweeps relax a few thousand rows each and still read every arc — on C4
+// the last 30–60 of ≈ 260 sweeps.  Once a sweep relaxes fewer than KP::thin rows the sweep
+// loop ends (reason 3); k_pass<CERT> then writes every row's compensated residual
+// r_v = s'_v − ((I+L)ẑ')_v into KP::fr_r, and this kernel runs the push form of the
+// method on exactly the rows above threshold, round by round:
+//   pop      every listed row v with |r_v| > θ h_v (P:221/453/458; round 0 lists every
+//            non-empty row) takes Δ = ω r_v/(1+d_v), ẑ'_v += Δ (equ:sor1), r_v ← (1−ω) r_v
+//            (equ:sor2) and leaves one scatter entry per kDepChunk rows that gather it;
+//   scatter  a warp per entry adds a_uv Δ to r_u of the rows u that gather v (equ:sor3,
+//            P:452; the canonical in-CSR lists them) with fp64 atomics; a row whose |r_u|
+//            thereby crosses θ h_u joins the next round's list;
+// until a round's list is empty (reason 0: every residual is ≤ θ h — the paper's Q = ∅,
+// P:216), a list overflows or the round limit is hit (reason 3: the fp64 sweeps that
+// follow carry on from ẑ'; every update made here was a valid relaxation, Lemma 3).
+// Pops take r_v by atomic exchange, so a row listed twice is relaxed once.  The residuals
+// are exact up to the rounding of their increments (≈ 1e-16 relative); the fp64
+// certificate after the solve re-checks every row from ẑ' as always.
+// out[4] = rounds, out[5] = scatter entries.
+#ifndef FJ_THIN_DIV
+#define FJ_THIN_DIV 256  // default thin-sweep threshold: non-empty rows / 256
+#endif
+template <bool W>
+__global__ void __launch_bounds__(kBlock, 4) k_front(KP p) {
+  __shared__ unsigned long long s_dec[3];
+  __shared__ Scalars sS;
+  unsigned long long tot_upd = 0, tot_eu = 0;
+  int sweeps0 = 0;
+  if (p.prev) {
+    sweeps0 = (int)__ldcg(p.prev);
+    tot_upd = __ldcg(p.prev + 1);
+    tot_eu = __ldcg(p.prev + 2);
+    if (__ldcg(p.prev + 3) != 3ull) {  // the sweeps did not end on a thin sweep: pass through
+      sweep_result(p.out, sweeps0, tot_upd, tot_eu, (int)__ldcg(p.prev + 3));
+      return;
+    }
+  }
+  if (threadIdx.x == 0) sS = *p.sc;
+  __syncthreads();
+  const Scalars &S = sS;
+  TAcc t{};
+  const int lane = threadIdx.x & 31;
+  const int64_t gtid = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * kBlock;
+  const int warp_id = (int)(gtid >> 5), nwarps = (int)(nthr >> 5);
+  int reason = 3, cur = 0;
+  unsigned long long rounds = 0, entries = 0;
+  for (int r = 0; r < p.fr_max_rounds; ++r) {
+    // ---- pop
+    const int64_t cnt = r == 0 ? p.empty0 : (int64_t)__ldcg(p.fr_cnt + cur);
+    if (cnt == 0) { reason = 0; break; }
+    if (r > 0 && cnt > p.fr_cap) break;  // the list overflowed: the sweeps carry on
+    const int *F = p.fr_rows + (size_t)cur * p.fr_cap;
+    int *Fn = p.fr_rows + (size_t)(cur ^ 1) * p.fr_cap;
+    unsigned *pcnt = p.fr_cnt + 2 + (r & 1);
+    for (int64_t e = gtid; e < cnt; e += nthr) {
+      const int i = r == 0 ? (int)e : __ldcg(F + e);
+      const double h = p.theta * threshold(S, (double)p.s[i] + S.c);
+      if (!(fabs(__ldcg(p.fr_r + i)) > h)) continue;
+      const double rv = __longlong_as_double(
+          (long long)atomicExch((unsigned long long *)(p.fr_r + i), 0ull));
+      if (!(fabs(rv) <= S.sentinel)) t.bad |= 1;
+      if (!(fabs(rv) > h)) {  // another entry of the same row popped it
+        if (rv != 0.0) atomicAdd(p.fr_r + i, rv);
+        continue;
+      }
+      const int len = (int)(p.rp[i + 1] - p.rp[i]);
+      const double d1 = W ? p.d1[i] : (double)(len + 1);
+      // the step ẑ' actually takes (ẑ'_v + Δ rounds; near the fp64 floor of a hub row Δ is a
+      // few ulps of ẑ'_v): r_v and the scattered amounts follow the stored value, so the
+      // residuals stay those of ẑ' itself — r_v ← r_v − (1+d_v)Δ, (1−ω) r_v in exact terms
+      const double zo = __ldcg(p.z + i), zn = zo + p.omega * rv / d1;
+      const double dz = zn - zo;
+      __stcg(p.z + i, zn);
+      const double rem = fma(-d1, dz, rv);
+      if (rem != 0.0) {
+        atomicAdd(p.fr_r + i, rem);
+        if (fabs(rem) > h && dz != 0.0) {  // still above threshold (ω far from 1): stays listed
+          // (dz == 0: ẑ'_v cannot move by so little — the row is at fp64's floor and is left
+          // to the certificate)
+          const unsigned pos = atomicAdd(p.fr_cnt + (cur ^ 1), 1u);
+          if (pos < (unsigned)p.fr_cap) Fn[pos] = i;
+        }
+      }
+      if (dz == 0.0) continue;
+      t.upd++;
+      t.eu += (unsigned long long)len;
+      const int u = p.perm[i];
+      const unsigned nd = (unsigned)(p.in_rp[u + 1] - p.in_rp[u]);
+      const unsigned nc = (nd + kDepChunk - 1) / kDepChunk;
+      if (nc) {
+        const unsigned pos = atomicAdd(pcnt, nc);
+        const long long bits = __double_as_longlong(dz);
+        for (unsigned c = 0; c < nc && pos + c < (unsigned)p.fr_pcap; c++)
+          p.fr_push[pos + c] = make_int4(i, (int)c, (int)(bits & 0xffffffffll), (int)(bits >> 32));
+      }
+    }
+    grid_sync(p.bar);
+    // ---- scatter
+    const unsigned np = __ldcg(pcnt);
+    if (np > (unsigned)p.fr_pcap) break;  // entries were dropped: ẑ' is valid, r is not
+    for (unsigned e = warp_id; e < np; e += nwarps) {
+      const int4 q = p.fr_push[e];
+      const double dz = __longlong_as_double(((long long)q.w << 32) | (unsigned)q.z);
+      const int u = p.perm[q.x];
+      const int64_t k0 = p.in_rp[u] + (int64_t)q.y * kDepChunk;
+      const int64_t k1 = min(p.in_rp[u + 1], k0 + kDepChunk);
+      for (int64_t k = k0 + lane; k < k1; k += 32) {
+        const int v = p.iperm[p.in_col[k]];
+        const double inc = (W ? (double)p.in_w[k] : 1.0) * dz;
+        const double old = atomicAdd(p.fr_r + v, inc);
+        const double hv = p.theta * threshold(S, (double)p.s[v] + S.c);
+        if (fabs(old) <= hv && fabs(old + inc) > hv) {
+          const unsigned pos = atomicAdd(p.fr_cnt + (cur ^ 1), 1u);
+          if (pos < (unsigned)p.fr_cap) Fn[pos] = v;
+        }
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.fr_cnt[cur] = 0u;                // this round's list is used up
+      p.fr_cnt[2 + ((r + 1) & 1)] = 0u;  // the next round's scatter count
+    }
+    unsigned long long dec[3];
+    sweep_totals(p.cnt, p.bar, r, t, s_dec, dec);
+    tot_upd += dec[0];
+    tot_eu += dec[1];
+    rounds = (unsigned long long)(r + 1);
+    entries += np;
+    cur ^= 1;
+    if (dec[2] != 0) { reason = 2; break; }
+  }
+  sweep_result(p.out, sweeps0, tot_upd, tot_eu, reason);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.out[4] = rounds;
+    p.out[5] = entries;
+  }
 }
 
 // shadow init: zs = encode(ẑ') for every row
@@ -351,7 +495,8 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   FJ_CUDA(ws.alloc(&arrive, std::max(1, L.npartials)));
   FJ_CUDA(ws.alloc(&ctl, kCtlWords));
   FJ_CUDA(ws.alloc(&cnt, 3));
-  FJ_CUDA(ws.alloc(&outv, 12));  // [0..3] sweep result, [4] certificate, [8..11] shadow result
+  FJ_CUDA(ws.alloc(&outv, 48));  // [0..3] sweep result, [4] certificate; stage results of the
+                                 // chain at 8 (first sweeps), 16 / 32 (frontier), 24 (fp64)
   certbits = outv + 4;
   if (!zdev) FJ_CUDA(ws.alloc(&zo, n));
   if (o->zprime_out && !zpdev) FJ_CUDA(ws.alloc(&zp, n));
@@ -448,22 +593,86 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
                                  carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault));
     sh_grid = persistent_grid(shfn, g->num_sms, sweep_smem);
   }
-  cudaEvent_t esh;
+  cudaEvent_t esh, ef[4];
   FJ_CUDA(ws.event(&esh));
-  float ms_sweep = 0, ms_cert = 0, ms_shadow = 0;
+  for (cudaEvent_t &e : ef) FJ_CUDA(ws.event(&e));
+  // Frontier phase (fj_opts.frontier): once a sweep relaxes fewer than `thin` rows, k_front
+  // evaluates only the items whose rows can have changed.  One-phase slice layouts only.
+  const bool use_front = SL && L.ncolors == 1 && o->frontier != 0 && L.active_rows > 0;
+  const void *ffn = W ? (const void *)k_front<true> : (const void *)k_front<false>;
+  int fgrid = 0;
+  if (use_front) {
+    const int64_t act = std::max<int64_t>(1, L.active_rows);
+    p.thin = o->frontier > 0 ? (unsigned long long)o->frontier
+                             : (unsigned long long)std::max<int64_t>(32, act / FJ_THIN_DIV);
+    p.fr_cap = (int)std::min<int64_t>(std::max<int64_t>(4096, act / 4), 1 << 30);
+    p.fr_pcap = (int)std::min<int64_t>((int64_t)p.fr_cap + L.m / kDepChunk, 1 << 30);
+    FJ_CUDA(ws.alloc(&p.fr_r, (size_t)n));
+    FJ_CUDA(ws.alloc(&p.fr_rows, 2 * (size_t)p.fr_cap));
+    FJ_CUDA(ws.alloc(&p.fr_push, (size_t)p.fr_pcap));
+    FJ_CUDA(ws.alloc(&p.fr_cnt, 4));
+    p.in_rp = g->in_rp;
+    p.in_col = g->in_col;
+    p.in_w = g->in_w;
+    p.perm = L.perm;
+    p.iperm = L.iperm;
+    p.fr_max_rounds = 100000;
+    FJ_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    fgrid = persistent_grid(ffn, g->num_sms, 0);
+  }
+  const unsigned long long thin = p.thin;
+  float ms_sweep = 0, ms_cert = 0, ms_shadow = 0, ms_front = 0;
   int rounds = 0;
   stats.colors = L.ncolors;
-  for (;;) {
-    // a3–a5: persistent sweeps with on-device loop control
+  // counters at rest before every launch of the chain (ring slots, claim words, arrivals)
+  auto rest = [&]() -> fj_status {
     FJ_CUDA(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * kCtlWords, st));
     FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(SweepCounters) * 3, st));
-    FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 12, st));
     // hub-piece arrival counters start at 0 for every launch (a resumed
     // sweep or the certificate never inherits a half-finished count)
     FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
+    return FJ_OK;
+  };
+  const void *rfn = W ? (const void *)k_pass<CERT, true> : (const void *)k_pass<CERT, false>;
+  unsigned long long *scratch_max = nullptr;
+  if (use_front) FJ_CUDA(ws.alloc(&scratch_max, 1));
+  auto launch_front = [&](unsigned long long *prev, unsigned long long *out, int ev) -> fj_status {
+    FJ_TRY(rest());
+    FJ_CUDA(cudaMemsetAsync(p.fr_cnt, 0, sizeof(unsigned) * 4, st));
+    FJ_CUDA(cudaMemsetAsync(scratch_max, 0, sizeof(unsigned long long), st));
+    FJ_CUDA(cudaEventRecord(ef[ev], st));
+    {  // residuals of every row from ẑ' (compensated; runs only after a thin exit)
+      KP q = p;
+      q.prev = prev;
+      q.ctr = ctl + 5;
+      q.rout = p.fr_r;
+      q.cert_max = scratch_max;
+      void *args[] = {&q};
+      fj::count_launch();
+      FJ_CUDA(cudaLaunchKernel(rfn, persistent_grid(rfn, g->num_sms), kBlock, args, 0, st));
+    }
+    FJ_TRY(rest());
+    KP q = p;
+    q.prev = prev;
+    q.out = out;
+    void *args[] = {&q};
+    fj::count_launch();
+    FJ_CUDA(cudaLaunchCooperativeKernel(ffn, fgrid, kBlock, args, 0, st));
+    FJ_CUDA(cudaEventRecord(ef[ev + 1], st));
+    return FJ_OK;
+  };
+  for (;;) {
+    // a3–a5: persistent sweeps with on-device loop control.  The chain of a round:
+    //   [shadow sweeps | fp64 sweeps] (thin exit) → frontier → fp64 sweeps (thin exit) →
+    //   frontier → fp64 sweeps; every stage continues the totals of the one before and
+    //   passes through at once if that one converged (frontier: unless it ended thin)
+    FJ_TRY(rest());
+    FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 48, st));
     FJ_CUDA(cudaEventRecord(es0, st));
     const bool sh_round = use_shadow && rounds == 0;  // resumes run in fp64 only
     p.prev = nullptr;
+    p.thin = thin;
+    p.skip_if_done = 0;
     if (sh_round) {
       KP q = p;
       q.out = outv + 8;
@@ -471,12 +680,31 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
       fj::count_launch();
       FJ_CUDA(cudaLaunchCooperativeKernel(shfn, sh_grid, kBlock, args, sweep_smem, st));
       FJ_CUDA(cudaEventRecord(esh, st));
-      // the fp64 sweeps start from counters at rest (ring slots, claim words, arrivals)
-      FJ_CUDA(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * kCtlWords, st));
-      FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(SweepCounters) * 3, st));
-      FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
+      p.prev = outv + 8;
+    } else if (use_front) {
+      KP q = p;
+      q.out = outv + 8;
+      void *args[] = {&q};
+      fj::count_launch();
+      FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, sweep_smem, st));
       p.prev = outv + 8;
     }
+    if (use_front) {
+      FJ_TRY(launch_front(outv + 8, outv + 16, 0));
+      FJ_TRY(rest());
+      KP q = p;  // fp64 sweeps; they may end thin again (rows the shadow sweeps left)
+      q.prev = outv + 16;
+      q.out = outv + 24;
+      q.skip_if_done = 1;
+      void *args[] = {&q};
+      fj::count_launch();
+      FJ_CUDA(cudaLaunchCooperativeKernel(fn, grid, kBlock, args, sweep_smem, st));
+      FJ_TRY(launch_front(outv + 24, outv + 32, 2));
+      p.prev = outv + 32;
+      p.skip_if_done = 1;
+      p.thin = 0;
+    }
+    if (p.prev) FJ_TRY(rest());
     {
       void *args[] = {&p};
       fj::count_launch();
@@ -487,6 +715,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     if (o->certify) {
       KP q = p;
       q.ctr = ctl + 5;
+      q.prev = nullptr;  // (with prev set the pass is the frontier phase's conditional one)
       FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * std::max(1, L.npartials), st));
       FJ_CUDA(cudaEventRecord(ec0, st));
       const void *cf = W ? (const void *)k_pass<CERT, true> : (const void *)k_pass<CERT, false>;
@@ -495,7 +724,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
       FJ_CUDA(cudaLaunchKernel(cf, persistent_grid(cf, g->num_sms), kBlock, cargs, 0, st));
       FJ_CUDA(cudaEventRecord(ec1, st));
     }
-    unsigned long long h[12];
+    unsigned long long h[48];
     FJ_CUDA(cudaMemcpyAsync(h, outv, sizeof(h), cudaMemcpyDeviceToHost, st));
     FJ_CUDA(cudaStreamSynchronize(st));
     float a = 0;
@@ -505,6 +734,14 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
       FJ_CUDA(cudaEventElapsedTime(&a, es0, esh));
       ms_shadow += a;
       stats.shadow_sweeps += (int64_t)h[8];
+    }
+    if (use_front) {
+      for (int e = 0; e < 4; e += 2) {
+        FJ_CUDA(cudaEventElapsedTime(&a, ef[e], ef[e + 1]));
+        ms_front += a;
+      }
+      stats.frontier_rounds += (int64_t)(h[16 + 4] + h[32 + 4]);
+      stats.frontier_pushes += (int64_t)(h[16 + 5] + h[32 + 5]);
     }
     if (o->certify) {
       FJ_CUDA(cudaEventElapsedTime(&a, ec0, ec1));
@@ -546,6 +783,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   stats.solve_ms = ms;
   stats.sweep_ms = ms_sweep;
   stats.shadow_ms = ms_shadow;
+  stats.frontier_ms = ms_front;
   stats.cert_ms = ms_cert;
   stats.c = hs.c;
   stats.eps_prime = hs.eps_p;

@@ -19,6 +19,10 @@ struct NvtxRange {  // tracing: one NVTX range per library phase (nsys/ncu timel
 };
 
 enum Mode { RELAX = 0, CERT = 1, DIS = 2, SPMV = 3 };
+#ifndef FJ_DEPCHUNK
+#define FJ_DEPCHUNK 256  // (1024: 2–6 % slower, the scatter of a hub's entry is one long chain)
+#endif
+constexpr int kDepChunk = FJ_DEPCHUNK;  // frontier phase: dependents of a relaxed row per list entry
 constexpr int kCtlWords = 256;  // control block: [0..2] claim counters, [5] cert counter, [8..] barrier
 
 struct Scalars {
@@ -87,6 +91,20 @@ struct KP {
   // shadow sweeps (k_sweep_sh, solve.cu): 32-bit fixed-point copy of ẑ' for the gathers
   unsigned *zs;            // [n] layout order: u = round(ẑ'·S.sh_enc), ẑ' ≈ u·S.sh_scale
   const unsigned long long *prev;  // out[] of the launch before this one (fp64 tail after shadow)
+  int skip_if_done;        // k_sweep: return at once if the launch before converged (prev[3] == 0)
+  // frontier phase (k_front, solve.cu): thin = a sweep that relaxes fewer rows (but some)
+  // ends the sweep loop with reason 3; the residuals, lists and maps of the phase
+  unsigned long long thin;
+  double *fr_r;            // [n] residuals r = s' − (I+L)ẑ', layout order (k_pass<CERT> writes them)
+  int *fr_rows;            // [2][fr_cap] rows to pop this / next round
+  int4 *fr_push;           // [fr_pcap] (row, chunk of its dependents, Δẑ bits) to scatter
+  unsigned *fr_cnt;        // [0,1] row-list counts, [2,3] scatter entries of an even / odd round
+  int fr_cap, fr_pcap;
+  const int64_t *in_rp;    // canonical in-CSR, original ids: row u lists the rows that gather u
+  const int32_t *in_col;
+  const float *in_w;       // their weights a (null: 1)
+  const int32_t *perm, *iperm;
+  int fr_max_rounds;
 };
 
 // CSR streams are read once per sweep: read-only path, no L1 allocation, so
@@ -224,7 +242,7 @@ __device__ __forceinline__ void relax_row_pre(const KP &p, const Scalars &S, int
   const double sp = (double)sv + S.c;
   const double h = threshold(S, sp);
   // shadow sweeps: plain fp64 combination (the shadow's rounding is far above its error)
-  const double rho = SH != 0 ? fma(-d1, zi, sp + total.hi) : residual_dd(total, sp, d1, zi);
+  const double rho = SH == 1 ? fma(-d1, zi, sp + total.hi) : residual_dd(total, sp, d1, zi);
   const double ar = fabs(rho);
   if (ar > p.theta * h) {
     // tail phase (R23): ω_i = min(ω, 1.98/(1+β_i)) keeps |1−ω_i| + ω_i β_i < 1
@@ -232,10 +250,10 @@ __device__ __forceinline__ void relax_row_pre(const KP &p, const Scalars &S, int
     if (p.tail_phase >= 0 && row >= p.tail_row0 && row < p.tail_row1)
       om = fmin(om, 1.98 / (1.0 + (double)p.tail_beta[row - p.tail_row0]));
     // (the fp64 kernel keeps the division: the reciprocal form costs it registers — spills)
-    const double dz = SH != 0 ? om * rho * rcp_newton(d1) : om * rho / d1;
+    const double dz = SH == 1 ? om * rho * rcp_newton(d1) : om * rho / d1;
     const double zn = zi + dz;
     __stcg(p.z + row, zn);
-    if constexpr (SH != 0) {
+    if constexpr (SH == 1) {
       // outside the shadow's range [0, 2^e): the shadow loop ends and the fp64 sweeps
       // carry on from ẑ (Lemma 3: any ẑ is a valid state)
       const double ze = zn * S.sh_enc;
@@ -339,9 +357,9 @@ __device__ __forceinline__ A block_reduce(A a, A *sm) {
 // above what double-double would recover; the fp64 tail sweeps and the certificate follow.
 template <int MODE, bool W, int SH = 0>
 __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Task &tk, TAcc &t) {
-  static_assert(SH == 0 || MODE == RELAX, "shadow gathers are a RELAX path");
+  static_assert(SH != 1 || MODE == RELAX, "shadow gathers are a RELAX path");
   // rows above 256 arcs accumulate in double-double for RELAX and CERT
-  using A = typename std::conditional<MODE == DIS || MODE == SPMV || SH != 0, double, dd>::type;
+  using A = typename std::conditional<MODE == DIS || MODE == SPMV || SH == 1, double, dd>::type;
 #ifndef FJ_WU
 #define FJ_WU 4
 #endif
@@ -377,7 +395,7 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
     }
     // stage 2: all gathers
     double zj[U];
-    if constexpr (SH == 0) {
+    if constexpr (SH != 1) {
 #pragma unroll
       for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
     } else {
@@ -390,7 +408,7 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
     // stage 3: accumulate
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      if constexpr (SH != 0) {
+      if constexpr (SH == 1) {
         a = fma((double)wv[u], zj[u], a);
       } else if constexpr (MODE == SPMV) {
         a = fma((double)wv[u], zj[u], a);
@@ -427,7 +445,7 @@ __device__ __forceinline__ void do_warp(const KP &p, const Scalars &S, const Tas
     return;
   } else {
     dd ad;
-    if constexpr (SH != 0) ad = dd{a, 0.0};
+    if constexpr (SH == 1) ad = dd{a, 0.0};
     else ad = a;
     if (np > 1) {
       __stcg(p.partial + slot + piece, make_double2(ad.hi, ad.lo));
@@ -491,7 +509,7 @@ __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, c
     wv[u] = W ? ld_stream(p.w + a0 + (ok ? e : 0)) : 1.0f;
   }
   double zj[U];
-  if constexpr (SH == 0) {
+  if constexpr (SH != 1) {
 #pragma unroll
     for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
   } else {
@@ -509,7 +527,7 @@ __device__ __forceinline__ void relax_warp_tile(const KP &p, const Scalars &S, c
   __syncwarp();
 #pragma unroll
   for (int q = 0; q < 2; q++) {
-    if (SH != 0 && q == 1 && tk.a + ng >= tk.b) break;  // no rows left for the second step (uniform)
+    if (SH == 1 && q == 1 && tk.a + ng >= tk.b) break;  // no rows left for the second step (uniform)
     {
       const int row = tk.a + q * ng + (lane >> cls);
       rb[q] = re[q] = 0;
@@ -559,7 +577,7 @@ __device__ __forceinline__ void slice_step(const KP &p, const Scalars &S, const 
     wv[u] = W ? ld_stream(wp + 32 * u) : 1.0f;
   }
   double zj[U];
-  if constexpr (SH == 0) {
+  if constexpr (SH != 1) {
 #pragma unroll
     for (int u = 0; u < U; u++) zj[u] = ld_z(p.z + j[u]);
   } else {
@@ -706,6 +724,8 @@ __device__ __forceinline__ void sweep_result(unsigned long long *out, int sweeps
 // ------------------------------------------ one pass over all tasks (CERT/DIS)
 template <int MODE, bool W>
 __global__ void __launch_bounds__(kBlock, 4) k_pass(KP p) {
+  // (frontier phase: the residual pass runs only if the sweeps before ended on a thin sweep)
+  if (MODE == CERT && p.prev && __ldcg(p.prev + 3) != 3ull) return;
   Scalars S{};
   if (MODE == CERT) S = *p.sc;
   TAcc t{};

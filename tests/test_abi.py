@@ -117,3 +117,4 @@ def test_binding_struct_layouts_match_header(tmp_path):
     fj.lib().fj_opts_default(ctypes.byref(o))
     assert o.shadow == -1
     assert o.slices == -1
+    assert o.frontier == -1

@@ -878,7 +878,7 @@ def test_batch_omega_columns(dev, name):
 def test_shadow_async(dev, name):
     rp, col, w, s, directed = TINY[name]()
     st, z, ref = check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async", shadow=1)
-    assert 0 < st.shadow_sweeps < st.sweeps
+    assert 0 < st.shadow_sweeps <= st.sweeps  # (the frontier phase may finish without an fp64 sweep)
     # the shadow changes the path, not the answer: fp64-only solve of the same input
     _, z0, _, st0 = gpu_solve(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async", shadow=0)
     assert st0.shadow_sweeps == 0
@@ -893,7 +893,7 @@ def test_shadow_colored_sor(dev, name, omega):
     # not die out) instead of running into the watchdog
     rp, col, w, s, directed = TINY[name]()
     st, _, _ = check_parity(dev, rp, col, w, s, 1e-6, omega, directed, shadow=1, max_sweeps=20000)
-    assert 0 < st.shadow_sweeps < st.sweeps
+    assert 0 < st.shadow_sweeps <= st.sweeps
 
 
 @pytest.mark.parametrize("name", ["rmat12", "rmat12w"])
@@ -991,3 +991,71 @@ def test_row_slices_mixed_lengths(dev, weighted):
         _, z, _ = check_parity(dev, rp, col, w, s, 1e-6, 1.0, True, method="async", slices=slices)
         zs.append(z)
     assert rel_err(zs[0], zs[1]) <= 2e-6
+
+
+# ------------------------------------------------- frontier phase (fj_opts.frontier)
+# After a thin sweep the solve switches to the push form on the rows above threshold
+# (k_front).  A huge threshold makes every sweep "thin", so the push rounds do nearly the
+# whole solve: the strictest test of their residual bookkeeping against the oracle.
+@pytest.mark.parametrize("frontier", [10**9, 64])
+@pytest.mark.parametrize("name", sorted(TINY))
+def test_frontier_phase_async(dev, name, frontier):
+    rp, col, w, s, directed = TINY[name]()
+    st, z, _ = check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async",
+                            frontier=frontier)
+    assert st.frontier_rounds > 0 and st.frontier_pushes > 0
+    # same answer as the sweeps alone (both meet the ε rule: they differ by ≤ 2ε relative)
+    g, z0, _, st0 = gpu_solve(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async", frontier=0)
+    g.close()
+    assert st0.frontier_rounds == 0 and st0.frontier_ms == 0.0
+    assert rel_err(z, z0) <= 2.5e-6
+    if frontier == 10**9:
+        assert st.sweeps < st0.sweeps
+
+
+@pytest.mark.parametrize("name,omega", [("rmat12", 1.3), ("rmat12w", 1.2), ("dirw-dense", 1.4),
+                                        ("rmat12w", 0.7)])
+def test_frontier_phase_sor_directed(dev, name, omega):
+    """ω ≠ 1: a popped row keeps (1−ω) r_v and is listed again while that is above h."""
+    rp, col, w, s, directed = TINY[name]()
+    st, _, _ = check_parity(dev, rp, col, w, s, 1e-6, omega, directed, method="async",
+                            ref_omega=1.0, frontier=10**9)
+    assert st.frontier_rounds > 0
+
+
+@pytest.mark.parametrize("shadow", [0, 1])
+@pytest.mark.parametrize("hub_deg", [3000, 70000])
+def test_frontier_phase_hub_rows(dev, hub_deg, shadow):
+    """A hub that gathers and is gathered by tens of thousands of rows: its scatter is cut
+    into chunks, its residual is the compensated one of the hub-piece path."""
+    n = hub_deg + 50
+    # undirected star (node 0 ↔ 1..hub_deg) plus a ring over the other nodes
+    src = np.concatenate([np.zeros(hub_deg, np.int64), np.arange(1, hub_deg + 1),
+                          np.arange(1, n), np.r_[np.arange(2, n), 1]])
+    dst = np.concatenate([np.arange(1, hub_deg + 1), np.zeros(hub_deg, np.int64),
+                          np.r_[np.arange(2, n), 1], np.arange(1, n)])
+    key = np.unique(src * n + dst)
+    src, dst = key // n, key % n
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, src + 1, 1)
+    rp = np.cumsum(rp)
+    col = dst.astype(np.int32)
+    s = fjgen.uniform(n, 91)
+    st, _, _ = check_parity(dev, rp, col, None, s, 1e-6, 1.0, False, method="async",
+                            frontier=n // 16, shadow=shadow)
+    assert st.frontier_rounds > 0
+    # every sweep "thin": after sweep 1 nearly all rows are above threshold and the phase's
+    # lists (a quarter of the rows) overflow on the larger star — it must hand back to the
+    # sweeps (reason 3) with ẑ' intact, and the solve must still meet the bar
+    st, _, _ = check_parity(dev, rp, col, None, s, 1e-6, 1.0, False, method="async",
+                            frontier=10**9, shadow=shadow)
+    assert st.status == 0
+
+
+def test_frontier_phase_zero_heavy_floored(dev):
+    """Signed, zero-heavy opinions (floored thresholds h ≈ 1e-11, the fp64 floor of hub
+    rows): the phase must leave rows it cannot move to the certificate, not spin."""
+    rp, col, w, s, directed = TINY["chunglu4k"]()
+    st, _, _ = check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async",
+                            frontier=10**9, max_sweeps=20000)
+    assert st.frontier_rounds > 0 and st.status == 0
