@@ -396,15 +396,21 @@ def run_ours(args, prob, world, rank, local):
             "sweep_kernel_ms": sweep_ms,
             "step_breakdown": {"solve_ms": solve_ms, "sweeps": st0.sweeps,
                                "shadow_sweeps": st0.shadow_sweeps, "shadow_ms": st0.shadow_ms,
+                               "frontier_rounds": st0.frontier_rounds,
+                               "frontier_pushes": st0.frontier_pushes,
+                               "frontier_ms": st0.frontier_ms,
                                "relaxations": st0.relaxations, "edge_updates": st0.edge_updates,
                                "cert_ratio": st0.cert_ratio, "colors": st0.colors,
                                "polarization": m0["P"], "disagreement": m0["D"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
-                         "kernel": "k_sweep_sh + k_sweep (persistent tile/unit sweeps: shadow "
-                                   "gathers, then the fp64 tail; both launches timed together)"
-                         if st0.shadow_sweeps else "k_sweep (persistent tile/unit sweep)",
+                         "kernel": "k_sweep_sh (persistent sweeps: warp units + row slices, shadow "
+                                   "gathers) + the frontier phase (k_pass<CERT> residuals, k_front) "
+                                   "+ any fp64 k_sweep tail; every launch of the sweep stage timed "
+                                   "together"
+                         if st0.shadow_sweeps else "k_sweep (persistent sweeps: warp units + row "
+                                                   "slices) + the frontier phase",
                          "algorithmic_bytes_per_launch": ab,
                          "bytes_model": "SURVEY 8(d): 12 B per edge-update (col, w, gathered z_j) "
                                         "+ 36 B per relaxation (row_ptr, s, z_i r/w, 1+d)",
