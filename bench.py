@@ -352,7 +352,8 @@ def run_ours(args, prob, world, rank, local):
                "frac": probe_ms / sweep_per,
                "note": "fj_gather_probe over the same layout: every arc's col+w streamed and "
                        "one fp64 gathered per arc; frac = probe / sweep time (1 = at the gather "
-                       "ceiling)"}
+                       "ceiling; above 1 when the sweeps gather from the 4-byte shadow, which the "
+                       "8-byte probe does not)"}
 
     # f2: the same graph with k = 4 opinion vectors in one batched solve
     batched = None

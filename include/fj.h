@@ -137,7 +137,7 @@ typedef struct {
   int64_t shadow_sweeps; /* of `sweeps`: those that gathered from the shadow           */
   double shadow_ms;      /* of `sweep_ms`: device time of the shadow sweep launch      */
   int64_t frontier_rounds; /* pop + scatter rounds of the frontier phase                */
-  int64_t frontier_pushes; /* scatter entries of those rounds (≤ 1024 in-arcs each)     */
+  int64_t frontier_pushes; /* scatter entries of those rounds (≤ 256 in-arcs each)      */
   double frontier_ms;    /* of `sweep_ms`: device time of the frontier launches        */
 } fj_stats;
 

@@ -598,7 +598,9 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   for (cudaEvent_t &e : ef) FJ_CUDA(ws.event(&e));
   // Frontier phase (fj_opts.frontier): once a sweep relaxes fewer than `thin` rows, k_front
   // evaluates only the items whose rows can have changed.  One-phase slice layouts only.
-  const bool use_front = SL && L.ncolors == 1 && o->frontier != 0 && L.active_rows > 0;
+  // (colored layouts: the rounds pop with ω = 1 — Jacobi-ordered rounds carry no SOR
+  // guarantee, plain pops converge in any order and Lemma 3 allows any amount)
+  const bool use_front = o->frontier != 0 && L.active_rows > 0;
   const void *ffn = W ? (const void *)k_front<true> : (const void *)k_front<false>;
   int fgrid = 0;
   if (use_front) {
@@ -655,6 +657,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
     KP q = p;
     q.prev = prev;
     q.out = out;
+    if (L.ncolors > 1) q.omega = 1.0;
     void *args[] = {&q};
     fj::count_launch();
     FJ_CUDA(cudaLaunchCooperativeKernel(ffn, fgrid, kBlock, args, 0, st));
