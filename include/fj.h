@@ -109,13 +109,15 @@ typedef struct {
                         (default): slices, except on colored layouts that have rows above
                         32 arcs.  Same relaxations either way (the order of a row's sum
                         differs in rounding only)                                       */
-  int frontier;      /* ASYNC with row slices: the frontier phase (the paper's queue, Alg. 1
+  int frontier;      /* ASYNC/COLORED: the frontier phase (the paper's queue, Alg. 1
                         P:216-226, on the thin tail of a solve).  Once a sweep relaxes fewer
                         than T rows, every row's residual is written once and the push form
                         runs on the rows above threshold only: pop, scatter a·Δ to the rows
                         that gather them (fp64 atomics), list the rows that cross their
-                        threshold, until the list is empty.  0 = off; > 0: T; < 0 (default):
-                        T = non-empty rows / 256                                         */
+                        threshold, until the list is empty (after COLORED sweeps the pops
+                        use ω = 1: the rounds are Jacobi-ordered, for which SOR carries no
+                        guarantee, and Lemma 3 allows any amount).  0 = off; > 0: T; < 0
+                        (default): T = non-empty rows / 256                              */
 } fj_opts;
 
 typedef struct {

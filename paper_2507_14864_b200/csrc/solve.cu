@@ -597,7 +597,7 @@ fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, c
   FJ_CUDA(ws.event(&esh));
   for (cudaEvent_t &e : ef) FJ_CUDA(ws.event(&e));
   // Frontier phase (fj_opts.frontier): once a sweep relaxes fewer than `thin` rows, k_front
-  // evaluates only the items whose rows can have changed.  One-phase slice layouts only.
+  // runs the push form on the rows above threshold (any layout: it works on rows, not items).
   // (colored layouts: the rounds pop with ω = 1 — Jacobi-ordered rounds carry no SOR
   // guarantee, plain pops converge in any order and Lemma 3 allows any amount)
   const bool use_front = o->frontier != 0 && L.active_rows > 0;

@@ -1059,3 +1059,22 @@ def test_frontier_phase_zero_heavy_floored(dev):
     st, _, _ = check_parity(dev, rp, col, w, s, 1e-6, 1.0, directed, method="async",
                             frontier=10**9, max_sweeps=20000)
     assert st.frontier_rounds > 0 and st.status == 0
+
+
+@pytest.mark.parametrize("frontier", [10**9, 64])
+@pytest.mark.parametrize("name,omega", [("er2000", 1.5), ("chunglu4k", 1.6), ("lattice64", 1.25),
+                                        ("lattice64", 1.8)])
+def test_frontier_phase_after_colored_sor(dev, name, omega, frontier):
+    """COLORED BLISOR sweeps, then the frontier phase with plain (ω = 1) pops: the oracle at
+    the same ω is the reference (both meet the ε rule), certificate and measures as always."""
+    rp, col, w, s, directed = TINY[name]()
+    st, z, _ = check_parity(dev, rp, col, w, s, 1e-6, omega, directed, method="colored",
+                            frontier=frontier, max_sweeps=20000)
+    assert st.colors > 1
+    # (with a small threshold fast SOR may go from many relaxations to none in one sweep)
+    assert st.frontier_rounds > 0 or frontier == 64
+    g, z0, _, st0 = gpu_solve(dev, rp, col, w, s, 1e-6, omega, directed, method="colored",
+                              frontier=0, max_sweeps=20000)
+    g.close()
+    assert st0.frontier_rounds == 0
+    assert rel_err(z, z0) <= 2.5e-6
