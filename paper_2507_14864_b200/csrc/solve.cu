@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_front(KP p) {
     unsigned *pcnt = p.fr_cnt + 2 + (r & 1);
     for (int64_t e = gtid; e < cnt; e += nthr) {
       const int i = r == 0 ? (int)e : __ldcg(F + e);
+      FJ_CHECK(i >= 0 && i < p.empty0);
       const double h = p.theta * threshold(S, (double)p.s[i] + S.c);
       if (!(fabs(__ldcg(p.fr_r + i)) > h)) continue;
       const double rv = __longlong_as_double(
@@ -344,11 +345,13 @@ __global__ void __launch_bounds__(kBlock, 4) k_front(KP p) {
     for (unsigned e = warp_id; e < np; e += nwarps) {
       const int4 q = p.fr_push[e];
       const double dz = __longlong_as_double(((long long)q.w << 32) | (unsigned)q.z);
+      FJ_CHECK(q.x >= 0 && q.x < p.empty0 && q.y >= 0);
       const int u = p.perm[q.x];
       const int64_t k0 = p.in_rp[u] + (int64_t)q.y * kDepChunk;
       const int64_t k1 = min(p.in_rp[u + 1], k0 + kDepChunk);
       for (int64_t k = k0 + lane; k < k1; k += 32) {
         const int v = p.iperm[p.in_col[k]];
+        FJ_CHECK(k >= p.in_rp[u] && k < p.in_rp[u + 1] && v >= 0 && v < p.empty0);
         const double inc = (W ? (double)p.in_w[k] : 1.0) * dz;
         const double old = atomicAdd(p.fr_r + v, inc);
         const double hv = p.theta * threshold(S, (double)p.s[v] + S.c);

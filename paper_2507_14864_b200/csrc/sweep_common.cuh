@@ -11,6 +11,15 @@
 
 #include "fj_internal.cuh"
 
+// -DFJ_BOUNDS: diagnostic build with device-side bounds checks (compute-sanitizer is not
+// available on the GPU pool): a failed check traps the kernel and the call returns
+// FJ_ERR_CUDA.  Used by tools/bounds_check.sh over the tiny GPU tests.
+#ifdef FJ_BOUNDS
+#define FJ_CHECK(cond) do { if (!(cond)) { printf("FJ_BOUNDS %s:%d: %s\n", __FILE__, __LINE__, #cond); __trap(); } } while (0)
+#else
+#define FJ_CHECK(cond) do { } while (0)
+#endif
+
 namespace fj {
 
 struct NvtxRange {  // tracing: one NVTX range per library phase (nsys/ncu timelines)
@@ -58,6 +67,9 @@ struct KP {
   const int *sphase_begin;
   const int32_t *__restrict__ scol;
   const float *__restrict__ sw;
+#ifdef FJ_BOUNDS
+  int64_t nslots;
+#endif
   const float *__restrict__ s;  // layout order
   double *z;                    // ẑ' (RELAX/CERT) or z (DIS), layout order
   const Scalars *sc;
@@ -573,8 +585,10 @@ __device__ __forceinline__ void slice_step(const KP &p, const Scalars &S, const 
   float wv[U];
 #pragma unroll
   for (int u = 0; u < U; u++) {
+    FJ_CHECK(cp + 32 * u >= p.scol && cp + 32 * u < p.scol + p.nslots);
     j[u] = ld_stream(cp + 32 * u);
     wv[u] = W ? ld_stream(wp + 32 * u) : 1.0f;
+    FJ_CHECK(j[u] >= 0 && j[u] <= p.empty1);  // a row, or the padding column n
   }
   double zj[U];
   if constexpr (SH != 1) {
@@ -600,6 +614,7 @@ __device__ __forceinline__ void relax_slice(const KP &p, const Scalars &S, const
   const int row = tk.a + lane;
   const bool ok = row < tk.b;
   int wd = tk.slot;
+  FJ_CHECK(tk.a >= 0 && tk.b <= p.empty0 && tk.b - tk.a <= 32 && tk.a1 - tk.a0 == 32 * (int64_t)wd);
   const int32_t *cp = p.scol + tk.a0 + lane;
   const float *wp = W ? p.sw + tk.a0 + lane : nullptr;
   float sv = 0.f;
@@ -870,6 +885,9 @@ static KP make_kp(const fj_graph *g, const Layout &L) {
   p.sphase_begin = L.d_sphase_begin;
   p.scol = L.scol;
   p.sw = L.sw;
+#ifdef FJ_BOUNDS
+  p.nslots = L.nslots;
+#endif
   p.phase_begin = L.d_phase_begin;
   p.wphase_begin = L.d_wphase_begin;
   p.ncolors = L.ncolors;
