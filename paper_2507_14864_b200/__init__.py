@@ -280,7 +280,7 @@ def solve(g: Graph, s, z_out, eps: float, omega: float = 1.0, method: str = "aut
 
 def solve_batch(g: Graph, S, Z_out, k: int, eps: float, omega: float = 1.0,
                 sigma: float = 1e-5, max_sweeps: int = 0, raise_on_numeric: bool = True,
-                method: str = "auto", tail_frac: float = -1.0) -> SolveStats:
+                method: str = "auto", tail_frac: float = -1.0, frontier: int = -1) -> SolveStats:
     """fj_solve_batch: k ≤ 8 opinion vectors (node-major fp32[n*k]) in one
     solve; AUTO runs ASYNC at ω = 1 or on directed graphs, else COLORED."""
     _dtype_ok(S, "S", "float32", g.n * int(k))
@@ -289,6 +289,7 @@ def solve_batch(g: Graph, S, Z_out, k: int, eps: float, omega: float = 1.0,
     lib().fj_opts_default(ctypes.byref(o))
     o.sigma, o.max_sweeps = sigma, max_sweeps
     o.method, o.tail_frac = METHODS[method], float(tail_frac)
+    o.frontier = int(frontier)
     st = _Stats()
     rc = lib().fj_solve_batch(g._h, _ptr(S), int(k), float(eps), float(omega), ctypes.byref(o),
                               _ptr(Z_out), ctypes.byref(st))

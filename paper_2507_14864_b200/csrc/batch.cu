@@ -243,6 +243,16 @@ __global__ void __launch_bounds__(kBlock, K >= 8 ? 2 : (K >= 4 ? FJ_BMIN4 : 4)) 
   TAcc t{};
   unsigned long long tot_upd = 0, tot_eu = 0;
   int sweeps = 0, reason = 1;
+  if (p.skip_if_done) {
+    // second launch of a solve with the frontier phase: nothing to do if every column's
+    // k_front (or the sweeps before it) ended converged — prev holds their out[] blocks
+    bool all0 = true;
+    for (int r = 0; r < p.kreal; r++) all0 = all0 && __ldcg(p.prev + 8 * r + 3) == 0ull;
+    if (all0) {
+      sweep_result(p.out, 0, 0ull, 0ull, 0);
+      return;
+    }
+  }
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
     for (int k = 0; k < p.ncolors; ++k) {
       const int r0 = p.rphase_begin[k], nr = p.rphase_begin[k + 1] - r0;
@@ -283,6 +293,7 @@ __global__ void __launch_bounds__(kBlock, K >= 8 ? 2 : (K >= 4 ? FJ_BMIN4 : 4)) 
     const bool bad = dec[2] != 0 || (bc.omb && s_nbad == p.kreal), done = dec[0] == 0;
     if (bad) { reason = 2; break; }
     if (done) { reason = 0; break; }
+    if (dec[0] < p.thin) { reason = 3; break; }  // thin sweep: the frontier phase takes over
   }
   sweep_result(p.out, sweeps, tot_upd, tot_eu, reason);
 }
@@ -322,6 +333,15 @@ __global__ void k_columnL(int64_t n, int K, int r, const float *__restrict__ sK,
   if (i >= n) return;
   s1[i] = sK[i * K + r];
   z1[i] = zK[i * K + r];
+}
+// frontier phase: a column's ẑ' back into the K-wide state (the last real column also into
+// the padding columns, which duplicate it)
+__global__ void k_column_back(int64_t n, int K, int r0, int r1, const double *__restrict__ z1,
+                              double *__restrict__ zK) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = z1[i];
+  for (int r = r0; r < r1; r++) zK[i * K + r] = v;
 }
 __global__ void k_finalize_batch(int64_t n, int k, int K, const int32_t *__restrict__ iperm,
                                  const double *__restrict__ zK, const Scalars *__restrict__ SK,
@@ -416,7 +436,7 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
   FJ_CUDA(ws.alloc(&arrive2, np));
   FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * np, st));
   FJ_CUDA(ws.alloc(&SK, K));
-  FJ_CUDA(ws.alloc(&outv, 8));
+  FJ_CUDA(ws.alloc(&outv, 8 + 16 + 8 * 8));  // sweeps, certificate, second launch, k_front per column
   FJ_CUDA(ws.alloc(&ctl, 8));
   FJ_CUDA(ws.alloc(&ctlb, kCtlWords));
   FJ_CUDA(ws.alloc(&cnt, 3));
@@ -456,18 +476,107 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
   p.bar = ctlb + 8;
   p.cnt = cnt;
   p.out = outv;
-  for (;;) {
-    FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * 8, st));
+  // Frontier phase (fj_opts.frontier, solve.cu k_front): once a batched sweep relaxes fewer
+  // than T·k rows over all right-hand sides, every column finishes on its own in the push
+  // form (column extracted to contiguous s1 / z1, compensated residuals, pop / scatter
+  // rounds, column written back); a second launch of the batched sweeps follows and
+  // returns at once when every column converged.  Not for the ω batch (its per-column
+  // relaxation counts and divergence flags belong to the sweeps).
+  const bool use_front = o->frontier != 0 && !omegas && L.active_rows > 0;
+  const void *ffn = front_kernel(W);
+  unsigned long long *outB = outv + 16, *outF = outv + 24, *scratch_max = outv + 5;
+  KP pf = make_kp(g, L);
+  int fgrid = 0;
+  unsigned long long thin = 0;
+  if (use_front) {
+    const int64_t act = std::max<int64_t>(1, L.active_rows);
+    const int64_t T = o->frontier > 0 ? (int64_t)o->frontier : std::max<int64_t>(32, act / FJ_THIN_DIV);
+    thin = (unsigned long long)(T * k);
+    pf.fr_cap = (int)std::min<int64_t>(std::max<int64_t>(4096, act / 4), 1 << 30);
+    pf.fr_pcap = (int)std::min<int64_t>((int64_t)pf.fr_cap + L.m / kDepChunk, 1 << 30);
+    FJ_CUDA(ws.alloc(&pf.fr_r, (size_t)n));
+    FJ_CUDA(ws.alloc(&pf.fr_rows, 2 * (size_t)pf.fr_cap));
+    FJ_CUDA(ws.alloc(&pf.fr_push, (size_t)pf.fr_pcap));
+    FJ_CUDA(ws.alloc(&pf.fr_cnt, 4));
+    pf.in_rp = g->in_rp;
+    pf.in_col = g->in_col;
+    pf.in_w = g->in_w;
+    pf.perm = L.perm;
+    pf.iperm = L.iperm;
+    pf.fr_max_rounds = 100000;
+    pf.s = s1;
+    pf.z = z1;
+    pf.partial = partial;
+    pf.arrive = arrive2;
+    pf.ctr = ctl;
+    pf.bar = ctlb + 8;
+    pf.cnt = cnt;
+    pf.cert_max = scratch_max;
+    pf.omega = L.ncolors > 1 ? 1.0 : omega;  // after colored sweeps: plain pops (solve.cu)
+    FJ_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    fgrid = persistent_grid(ffn, g->num_sms, 0);
+  }
+  auto rest = [&]() -> fj_status {
     FJ_CUDA(cudaMemsetAsync(ctlb, 0, sizeof(unsigned) * kCtlWords, st));
     FJ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(SweepCounters) * 3, st));
+    return FJ_OK;
+  };
+  for (;;) {
+    FJ_CUDA(cudaMemsetAsync(outv, 0, sizeof(unsigned long long) * (8 + 16 + 8 * 8), st));
+    FJ_TRY(rest());
     FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * np, st));
     FJ_CUDA(cudaEventRecord(es0, st));
-    void *args[] = {&p};
-    fj::count_launch();
-    FJ_CUDA(cudaLaunchCooperativeKernel(fb, bgrid, kBlock, args, 0, st));
+    p.thin = thin;
+    p.skip_if_done = 0;
+    p.prev = nullptr;
+    p.out = outv;
+    {
+      void *args[] = {&p};
+      fj::count_launch();
+      FJ_CUDA(cudaLaunchCooperativeKernel(fb, bgrid, kBlock, args, 0, st));
+    }
+    if (use_front) {
+      pf.theta = p.theta;
+      for (int r = 0; r < k; r++) {
+        fj::count_launch();
+        k_columnL<<<gridn(n), kBlock, 0, st>>>(n, K, r, sK, zK, s1, z1);
+        KP q = pf;
+        q.sc = SK + r;
+        q.prev = outv;
+        q.out = outF + 8 * r;
+        FJ_TRY(rest());
+        FJ_CUDA(cudaMemsetAsync(arrive2, 0, sizeof(int) * np, st));
+        FJ_CUDA(cudaMemsetAsync(pf.fr_cnt, 0, sizeof(unsigned) * 4, st));
+        {  // residuals of the column (runs only after a thin exit)
+          KP qr = q;
+          qr.rout = pf.fr_r;
+          void *rargs[] = {&qr};
+          fj::count_launch();
+          FJ_CUDA(cudaLaunchKernel(cf, cgrid, kBlock, rargs, 0, st));
+        }
+        FJ_TRY(rest());
+        void *fargs[] = {&q};
+        fj::count_launch();
+        FJ_CUDA(cudaLaunchCooperativeKernel(ffn, fgrid, kBlock, fargs, 0, st));
+        fj::count_launch();
+        k_column_back<<<gridn(n), kBlock, 0, st>>>(n, K, r, r + 1 == k ? K : r + 1, z1, zK);
+      }
+      // the batched sweeps again: at once done if every column converged, else they carry on
+      FJ_TRY(rest());
+      FJ_CUDA(cudaMemsetAsync(arrive, 0, sizeof(int) * np, st));
+      KP q = p;
+      q.thin = 0;
+      q.skip_if_done = 1;
+      q.prev = outF;
+      q.out = outB;
+      void *args[] = {&q};
+      fj::count_launch();
+      FJ_CUDA(cudaLaunchCooperativeKernel(fb, bgrid, kBlock, args, 0, st));
+    }
     FJ_CUDA(cudaEventRecord(es1, st));
-    unsigned long long h[8];
+    unsigned long long h[8], hx[8 + 64];
     FJ_CUDA(cudaMemcpyAsync(h, outv, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FJ_CUDA(cudaMemcpyAsync(hx, outB, sizeof(hx), cudaMemcpyDeviceToHost, st));
     // compensated certificate of every right-hand side (ω batch: of every
     // column that did not diverge)
     double worst = 0.0;
@@ -511,6 +620,21 @@ fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, do
     stats.relaxations += (int64_t)h[1];
     stats.edge_updates += (int64_t)h[2];
     stats.reason = (int)h[3];
+    if (use_front) {
+      // every column's k_front continued the first launch's totals: its own part on top,
+      // then the second launch of the sweeps (whose reason is the round's)
+      for (int r = 0; r < k; r++) {
+        const unsigned long long *f = hx + 8 + 8 * r;
+        stats.relaxations += (int64_t)(f[1] - h[1]);
+        stats.edge_updates += (int64_t)(f[2] - h[2]);
+        stats.frontier_rounds += (int64_t)f[4];
+        stats.frontier_pushes += (int64_t)f[5];
+      }
+      stats.sweeps += (int64_t)hx[0];
+      stats.relaxations += (int64_t)hx[1];
+      stats.edge_updates += (int64_t)hx[2];
+      stats.reason = (int)hx[3];
+    }
     stats.cert_ratio = worst;
     if (stats.reason != 0 || stats.cert_ratio <= 1.0 || rounds >= o->cert_rounds) break;
     rounds++;

@@ -259,9 +259,6 @@ __global__ void __launch_bounds__(kBlock, FJ_MINB) k_sweep_sh(KP p) {
 // are exact up to the rounding of their increments (≈ 1e-16 relative); the fp64
 // certificate after the solve re-checks every row from ẑ' as always.
 // out[4] = rounds, out[5] = scatter entries.
-#ifndef FJ_THIN_DIV
-#define FJ_THIN_DIV 256  // default thin-sweep threshold: non-empty rows / 256
-#endif
 template <bool W>
 __global__ void __launch_bounds__(kBlock, 4) k_front(KP p) {
   __shared__ unsigned long long s_dec[3];
@@ -431,6 +428,10 @@ const void *sweep_kernel(bool weighted) {
   return weighted ? (const void *)k_sweep<true, false> : (const void *)k_sweep<false, false>;
 }
 size_t sweep_kernel_smem() { return (kBlock / 32) * kWarpTileArcs * sizeof(double); }
+// the frontier phase's kernel, for the batched solve (batch.cu runs it column by column)
+const void *front_kernel(bool weighted) {
+  return weighted ? (const void *)k_front<true> : (const void *)k_front<false>;
+}
 
 fj_status solve_impl(fj_graph *g, const float *s_in, double eps, double omega, const fj_opts *o,
                      float *z_out, fj_stats *st_out) {

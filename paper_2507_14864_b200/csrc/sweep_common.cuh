@@ -28,6 +28,9 @@ struct NvtxRange {  // tracing: one NVTX range per library phase (nsys/ncu timel
 };
 
 enum Mode { RELAX = 0, CERT = 1, DIS = 2, SPMV = 3 };
+#ifndef FJ_THIN_DIV
+#define FJ_THIN_DIV 256  // default thin-sweep threshold: non-empty rows / 256
+#endif
 #ifndef FJ_DEPCHUNK
 #define FJ_DEPCHUNK 256  // (1024: 2–6 % slower, the scatter of a hub's entry is one long chain)
 #endif
@@ -926,6 +929,7 @@ static fj_status finish_status(const Scalars &hs, fj_stats &stats, const fj_opts
 // implemented in push.cu / batch.cu / solve.cu
 const void *sweep_kernel(bool weighted);  // k_sweep<W, false> (solve.cu): the warp-tile list
 size_t sweep_kernel_smem();
+const void *front_kernel(bool weighted);  // k_front<W> (solve.cu)
 fj_status push_solve_impl(fj_graph *g, const float *s_in, double eps, double omega,
                           const fj_opts *o, float *z_out, fj_stats *st_out);
 fj_status batch_solve_impl(fj_graph *g, const float *S_in, int k, double eps, double omega,

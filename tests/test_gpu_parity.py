@@ -1078,3 +1078,28 @@ def test_frontier_phase_after_colored_sor(dev, name, omega, frontier):
     g.close()
     assert st0.frontier_rounds == 0
     assert rel_err(z, z0) <= 2.5e-6
+
+
+@pytest.mark.parametrize("name,omega", [("rmat12w", 1.0), ("er2000", 1.0), ("er2000", 1.5),
+                                        ("chunglu4k", 1.0)])
+@pytest.mark.parametrize("k", [3, 8])
+def test_batch_solve_frontier_phase(dev, name, omega, k):
+    """Batched solve with the frontier phase forced early (every sweep "thin"): each column
+    finishes on its own in the push form and is written back; the padding columns follow the
+    last real one; the second launch of the batched sweeps confirms.  Columns vs the oracle."""
+    rp, col, w, s0, directed = TINY[name]()
+    n = len(rp) - 1
+    S = _batch_columns(n, s0, k)
+    g = fj.Graph(n, _t(rp, dev), _t(col, dev), _t(w, dev), directed=directed)
+    Z = torch.empty(n * k, dtype=torch.float32, device=dev)
+    st = fj.solve_batch(g, _t(S.ravel(), dev), Z, k, 1e-6, omega, frontier=10**9)
+    st0 = fj.solve_batch(g, _t(S.ravel(), dev), torch.empty_like(Z), k, 1e-6, omega, frontier=0)
+    torch.cuda.synchronize()
+    g.close()
+    assert st.status == 0 and st.cert_ratio <= 1.0, st
+    assert st.frontier_rounds > 0 and st0.frontier_rounds == 0
+    assert st.sweeps < st0.sweeps
+    Zh = Z.cpu().numpy().reshape(n, k).astype(np.float64)
+    for r in range(k):
+        ref = oracle.solve(rp, col, w, S[:, r], 1e-6, omega)
+        assert rel_err(Zh[:, r], ref.z) <= 1e-4, r
