@@ -214,7 +214,10 @@ fj_status fj_solve_ex(fj_graph_t g, const float *s, double eps, double omega,
  * (multicolor SOR, tail merge per o->tail_frac) for ω ≠ 1 on undirected
  * graphs, as fj_solve; ASYNC or COLORED explicitly; PUSH and z_init →
  * FJ_ERR_INVALID.  The loop stops after a sweep in which no right-hand side
- * relaxed any row; FJ_ERR_NUMERIC as fj_solve_ex.
+ * relaxed any row; FJ_ERR_NUMERIC as fj_solve_ex.  With o->frontier != 0
+ * (default) a batched sweep that relaxes fewer than T·k rows hands over to
+ * the frontier phase, which finishes every right-hand side on its own (see
+ * fj_opts.frontier); st->frontier_rounds / frontier_pushes sum over them.
  */
 fj_status fj_solve_batch(fj_graph_t g, const float *S, int k, double eps, double omega,
                          const fj_opts *o, float *Z_out, fj_stats *st);
