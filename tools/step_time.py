@@ -1,6 +1,8 @@
+"""Wall time of the pieces of one bench step on config 4 (diagnostics): graph create,
+solve, measures, close, each synchronised.  usage: python tools/step_time.py"""
 import os, sys, time
 import torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import fjgen
 import paper_2507_14864_b200 as fj
 dev = torch.device("cuda:0")
